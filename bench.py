@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark: fp32 GEMM GFLOP/s of the ELEVATE parallel schedule on B200.
+
+Workload (default, BASELINE.json configs[3]): the `parallel` schedule applied
+to mm(M=32768, N=32768, K=8192), row-sharded over N GPUs (strong scaling: the
+problem is fixed, rank r computes rows [row0_r, row0_r+rows_r) of C).  One
+step = broadcast B from rank 0 over NCCL (the path's one exchange, skipped at
+N=1) + the operand prepass (packB / tf32 split) + the GEMM kernel, on
+synthetic U(-1,1) inputs already resident in HBM (1 GiB A, 1 GiB B, 4 GiB C:
+every operand is larger than the 126 MB L2, so no flush is needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--variant parallel_tf32x3|parallel|...] [--M --N --K]
+                    [--workload rowshard|ladder]
+
+Prints ONE JSON line on rank 0 (see the task contract).  `--workload ladder`
+instead prints one line per (strategy, shape) for configs[1]/configs[2].
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "fp32 GEMM GFLOP/s per ELEVATE strategy (1024³; 8192³; sharded at 1/2/4/8 GPU)"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def roofline_peak(variant: str, peaks: dict, n_sms: int):
+    """(peak TFLOP/s of useful fp32 flops, bound, note)."""
+    if variant == "parallel_tf32x3":
+        # tf32 tensor rate = 1/2 the bf16 rate; 3 MMAs per useful MAC
+        tf32 = peaks["bf16_tflops_sustained"] / 2.0
+        return tf32 / 3.0, "tensor", (
+            "tf32 tensor peak = MEASURED_PEAKS bf16_tflops_sustained/2; 3xTF32 issues 3 MMAs per "
+            "useful MAC, so the useful-fp32 ceiling is that /3")
+    fp32 = n_sms * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    return fp32, "fp32-simt", (
+        f"fp32 FFMA peak = {n_sms} SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS); no "
+        "measured SIMT peak exists")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def traffic_from_profiles(kernel_key: str):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines: the reference interpreter itself (stratir.interp.run)
+
+def _interp_sample(args):
+    """Evaluate the parallel-schedule term on one bounded slice; returns seconds."""
+    m, n, k, seed = args
+    sys.path.insert(0, REPO)
+    from paper_2002_02268_b200 import schedules, synth
+    from paper_2002_02268_b200._ref import S
+    s = S()
+    term = schedules.apply("parallel", m, n, k).term
+    A = synth.matrix(m, k, seed, 0).tolist()
+    B = synth.matrix(k, n, seed, 1).tolist()
+    t0 = time.perf_counter()
+    s.interp.run(term, [A, B])
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_single(m=32, n=32, k=1024):
+    """Reference interpreter, 1 core, bounded sample (~10 s)."""
+    try:
+        dt = _interp_sample((m, n, k, 0))
+        kind = "reference"
+        sample = (f"stratir.interp.run (reference interpreter, baseline/_ref) on the parallel-schedule "
+                  f"term at {m}x{n}x{k} (row/column slice of the workload; cost is per MAC)")
+    except ImportError:
+        import numpy as np
+        import oracle   # cpu_baseline leg: the C restatement when the reference is absent
+        from paper_2002_02268_b200 import synth
+        m, n, k = 256, 256, 1024
+        A, B = synth.matrix(m, k, 0, 0), synth.matrix(k, n, 0, 1)
+        t0 = time.perf_counter()
+        oracle.mm_interp_f64(A, B, "parallel")
+        dt = time.perf_counter() - t0
+        kind = "port"
+        sample = f"oracle/mm_oracle.c chunk4 f64 port, {m}x{n}x{k}"
+    return {"value": 2.0 * m * n * k / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": kind,
+            "sample": sample, "seconds": round(dt, 3)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's own CPU path on all host cores."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    m, n, k = 32, 32, 256
+    try:
+        _interp_sample((m, n, 32, 0))
+    except ImportError as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"stratir not importable: {e}"}))
+        return
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        def step():
+            t0 = time.perf_counter()
+            pool.map(_interp_sample, [(m, n, k, i + 1) for i in range(cores)])
+            return time.perf_counter() - t0
+        for _ in range(args.warmup):
+            step()
+        times = [step() for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = cores * 2.0 * m * n * k / t / 1e9
+    sample = (f"{cores} concurrent stratir.interp.run evaluations of the parallel-schedule term, "
+              f"each a {m}x{n}x{k} slice (disjoint seeds); aggregate GFLOP/s")
+    out = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(args, world):
+    return {"workload": f"parallel schedule mm({args.M},{args.N},{args.K}) row-sharded "
+                        f"(BASELINE.json configs[3]; M x N x K)",
+            "model": "ELEVATE mm, parallel schedule", "M": args.M, "N": args.N, "K": args.K,
+            "kernel_variant": args.variant, "parallelism": f"rowshard{world}",
+            "l2": "inputs larger than L2 (A,B 1 GiB; C 4 GiB)"}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="parallel_tf32x3")
+    ap.add_argument("--M", type=int, default=32768)
+    ap.add_argument("--N", type=int, default=32768)
+    ap.add_argument("--K", type=int, default=8192)
+    ap.add_argument("--workload", default="rowshard", choices=["rowshard", "ladder"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2002_02268_b200 import dispatch, distributed as D, interp, schedules, synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    if args.workload == "ladder":
+        run_ladder(args, dev)
+        return
+
+    M, N, K = args.M, args.N, args.K
+    sched, tf32x3 = ("parallel", True) if args.variant == "parallel_tf32x3" else (args.variant, False)
+    term = schedules.apply(sched, M, N, K).term
+    full_plan = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf32x3)
+    sh = D.shard_rows(M, world, rank)
+    import dataclasses
+    plan = dataclasses.replace(full_plan, M=sh.rows)
+
+    stream = torch.cuda.current_stream(dev)
+    A = torch.empty((sh.rows, K), device=dev)
+    B = torch.empty((K, N), device=dev)
+    C = torch.empty((sh.rows, N), device=dev)
+    synth.fill_device(A, 0, 0, offset=sh.row0 * K)
+    if rank == 0:
+        synth.fill_device(B, 0, 1)
+    else:
+        B.zero_()
+    call = interp.GemmCall(plan, A, B, C, stream)
+    rsg = D.RowShardGemm(plan, compute=lambda a, b, c: None)   # broadcast helper only
+
+    ev = []
+
+    def step(record=False):
+        rsg.broadcast_b(B)
+        if record:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            call.prepare()
+            e1.record(stream)
+            call.compute()
+            e2.record(stream)
+            ev.append((e0, e1, e2))
+        else:
+            call.prepare()
+            call.compute()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(end) / args.steps
+    prep_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
+    comp_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev)
+    if world > 1:
+        t = torch.tensor([ms, comp_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, comp_ms_max = t.tolist()
+    else:
+        comp_ms_max = comp_ms
+    flops = 2.0 * M * N * K
+    value = flops / (ms * 1e-3) / 1e9
+
+    # ---------------- end to end through the public API (host buffers) ----------------
+    e2e = None
+    if not args.no_e2e:
+        A_h = torch.empty((sh.rows, K), dtype=torch.float32, pin_memory=True)
+        A_h.copy_(A)
+        B_h = torch.empty((K, N), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+        if rank == 0:
+            B_h.copy_(B)
+        C_h = torch.empty((sh.rows, N), dtype=torch.float32, pin_memory=True)
+        shard_term = term if world == 1 else None
+
+        def e2e_step():
+            if world == 1:
+                interp.run(shard_term, [A_h, B_h], out=C_h, tf32x3=tf32x3)
+            else:
+                if rank == 0:
+                    B.copy_(B_h, non_blocking=True)
+                A.copy_(A_h, non_blocking=True)
+                rsg.broadcast_b(B)
+                interp.gemm(plan, A, B, out=C, stream=stream)
+                C_h.copy_(C, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+
+        e2e_step()
+        barrier()
+        k2 = max(2, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            e2e_step()
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / k2
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        h2d = M * K * 4 + K * N * 4
+        d2h = M * N * 4
+        e2e = {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "interp.run(term, [A_host_pinned, B_host_pinned], out=C_host_pinned)"
+               if world == 1 else "H2D A-shard (+B on rank 0), NCCL broadcast, interp.gemm, D2H C-shard"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, peaks_src = load_peaks()
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak, bound, note = roofline_peak(args.variant, peaks, n_sms)
+    achieved = 2.0 * sh.rows * N * K / (comp_ms * 1e-3) / 1e12
+    kernel = {"parallel_tf32x3": "k7_tf32x3", "parallel": "k56_packed_8x8<true>"}.get(args.variant, args.variant)
+    roof = {"bound": "tensor" if bound == "tensor" else "fp32-simt", "achieved": achieved,
+            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic_from_profiles(f"{kernel}@{sh.rows}x{N}x{K}"),
+            "kernel": kernel, "kernel_ms": comp_ms, "prepass_ms": prep_ms,
+            "kernel_share_of_step": comp_ms / ms, "peak_source": f"{peaks_src}: {note}",
+            "algorithmic_flops_per_launch": 2.0 * sh.rows * N * K}
+    out = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic U(-1,1) (counter-based, on device)",
+        "config": workload_config(args, world),
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * call.launches,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_single()
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_ladder(args, dev):
+    """configs[1] (all strategies at 1024^3) and configs[2] (8192^3 subset)."""
+    import torch
+    from paper_2002_02268_b200 import dispatch, interp, schedules, synth
+    peaks, src = load_peaks()
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cases = [(v, 1024) for v in list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]]
+    cases += [(v, 8192) for v in ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3")]
+    stream = torch.cuda.current_stream(dev)
+    for v, n in cases:
+        sched, tf = ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+        term = schedules.apply(sched, n, n, n).term
+        p = dispatch.decode(term, [(n, n), (n, n)], tf32x3=tf)
+        A = torch.empty((n, n), device=dev); synth.fill_device(A, 0, 0)
+        B = torch.empty((n, n), device=dev); synth.fill_device(B, 0, 1)
+        C = torch.empty((n, n), device=dev)
+        call = interp.GemmCall(p, A, B, C, stream)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MB > L2
+        reps = 20 if n <= 1024 else 5
+        if v == "baseline" and n > 1024:
+            reps = 2
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        tot, comp = [], []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream); call.prepare(); e1.record(stream); call.compute(); e2.record(stream)
+            torch.cuda.synchronize()
+            tot.append(e0.elapsed_time(e2)); comp.append(e1.elapsed_time(e2))
+        ms = statistics.median(tot)
+        peak, bound, note = roofline_peak(v, peaks, n_sms)
+        ach = 2.0 * n ** 3 / (statistics.median(comp) * 1e-3) / 1e12
+        print(json.dumps({"workload": f"{v} mm({n},{n},{n})", "variant": v, "M": n, "N": n, "K": n,
+                          "gflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "ms": ms,
+                          "kernel_ms": statistics.median(comp), "kernel_tflops": ach,
+                          "roofline_bound": bound, "peak_tflops": peak, "frac": ach / peak,
+                          "l2": "flushed (256 MB write) before every rep"}), flush=True)
+        del A, B, C, call, flush
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

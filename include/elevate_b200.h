@@ -1,0 +1,129 @@
+/*
+ * elevate_b200.h -- C ABI of the B200 execution backend for the ELEVATE
+ * (arXiv 2002.02268) GEMM hot path.
+ *
+ * The reference has no FFI: its hot path is the Python tree-walking
+ * interpreter `stratir.interp.run(e, args)` (reference
+ * pkg/src/stratir/interp.py:157-162) evaluating the rewritten `mm` term with
+ * f64 scalars on nested lists.  Every entry point below replaces one piece of
+ * that evaluation for the seven scheduled `mm` terms; the Python drop-in
+ * (`paper_2002_02268_b200.interp.run`) decodes the term and binds these with
+ * ctypes.  The shape of the calls follows the reference SPEC's codegen-c
+ * contract `void fn(float* out, const float* in0, ...)` (reference
+ * SPEC.md:525), extended with sizes, leading dimensions and a stream.
+ *
+ * Conventions
+ *  - All matrices are fp32, row-major, device pointers.  C = A(MxK) . B(KxN).
+ *  - The caller owns every buffer (A, B, C, workspace).  The library never
+ *    allocates or frees user memory; size workspaces with
+ *    elv_gemm_workspace_bytes().
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous on that stream.
+ *  - Return value: ELV_OK (0) or a negative ELV_E* code; elv_last_error()
+ *    returns a thread-local message for the last failure on this thread.
+ *    The Python layer maps ELV_EINVAL/ELV_EVARIANT to the reference's
+ *    EvalError (interp.py:16) and ELV_ECUDA/ELV_ENCCL to RuntimeError.
+ */
+#ifndef ELEVATE_B200_H
+#define ELEVATE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ELV_ABI_VERSION 1
+
+enum {
+  ELV_OK = 0,
+  ELV_EINVAL = -1,      /* bad size / pointer / leading dimension          */
+  ELV_EVARIANT = -2,    /* unknown kernel variant                          */
+  ELV_ECUDA = -3,       /* CUDA launch or runtime error                    */
+  ELV_ENCCL = -4,       /* NCCL error (row-shard driver)                   */
+  ELV_EWORKSPACE = -5   /* workspace missing or too small                  */
+};
+
+/* Kernel variants: one per ELEVATE/TVM schedule (reference PAPER.md:269-315;
+ * SPEC.md:482-488), decoded from the lowered term by the dispatch. */
+enum {
+  ELV_BASELINE = 0,        /* mapSeq/mapSeq/reduceSeq: one thread per C(i,j)  */
+  ELV_BLOCKING = 1,        /* tile(32,32) + split(4): 32x32 SMEM tiles        */
+  ELV_VECTORIZED = 2,      /* + vectorize(32): 128-bit loads/stores           */
+  ELV_LOOPPERM = 3,        /* + reorder: register outer-product micro-tiles   */
+  ELV_ARRAYPACKING = 4,    /* + packB/toMem: GEMM over packedB[N/32][K][32]   */
+  ELV_CACHEBLOCKS = 5,     /* + toMem(acc) + unroll: 8x8 register accumulators*/
+  ELV_PARALLEL = 6,        /* + mapPar: persistent, double-buffered, 148 SMs  */
+  ELV_PARALLEL_TF32X3 = 7, /* parallel term on tcgen05: 3xTF32, TMEM accum    */
+  ELV_NUM_VARIANTS = 8
+};
+
+/* C = A . B with the kernel of `variant`.
+ * Replaces interp.run(schedule(mm), [A, B]) (interp.py:157-162) for the
+ * decoded schedule.  Variants 4..7 need a workspace (packed / split copies of
+ * the operands); pass NULL/0 for 0..3.  Any M, N, K >= 1 (tails predicated).
+ */
+int elv_gemm(int variant, const float* A, const float* B, float* C,
+             int M, int N, int K, int lda, int ldb, int ldc,
+             void* workspace, size_t workspace_bytes, void* stream);
+
+/* The two phases of elv_gemm, for callers that time or overlap them:
+ * prepare = the operand layout transform into `workspace` (packB for 4..6,
+ * the hi/lo split + K-major transpose for 7, nothing for 0..3);
+ * compute = the GEMM kernel reading the prepared workspace.
+ * elv_gemm == elv_gemm_prepare ; elv_gemm_compute on the same stream. */
+int elv_gemm_prepare(int variant, const float* A, const float* B, int M, int N, int K,
+                     int lda, int ldb, void* workspace, size_t workspace_bytes, void* stream);
+int elv_gemm_compute(int variant, const float* A, const float* B, float* C,
+                     int M, int N, int K, int lda, int ldb, int ldc,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Bytes of workspace elv_gemm(variant, ...) needs at this shape. */
+size_t elv_gemm_workspace_bytes(int variant, int M, int N, int K);
+
+/* Same as elv_gemm for variants 4..6, but B is already packed by
+ * elv_pack_b (used by the row-shard driver after a packedB broadcast). */
+int elv_gemm_prepacked(int variant, const float* A, const float* packedB,
+                       float* C, int M, int N, int K, int lda, int ldc,
+                       void* stream);
+
+/* packedB[p][k][c] = B[k][p*blk + c] (0 past N); p < ceil(N/128)*128/blk.
+ * The toMem of the packB rule (reference rules.py:516-549; TVM packedB,
+ * PAPER.md:49-50).  blk must be 32. */
+int elv_pack_b(const float* B, float* packedB, int K, int N, int ldb, int blk,
+               void* stream);
+size_t elv_pack_b_bytes(int K, int N);
+
+/* hi = rna_tf32(x), lo = rna_tf32(x - hi), elementwise over n floats. */
+int elv_split_tf32(const float* X, float* hi, float* lo, long long n,
+                   void* stream);
+
+/* Synthetic inputs: X[i] = U(-1,1) with 24-bit resolution from
+ * splitmix64((seed << 48) ^ (tensor_id << 40) ^ (offset + i)); bit-identical
+ * to paper_2002_02268_b200.synth.uniform() on the host. */
+int elv_fill_uniform(float* X, long long n, unsigned long long seed,
+                     unsigned int tensor_id, long long offset, void* stream);
+
+/* Row-sharded GEMM over ndev GPUs in ONE process (mapPar(xo) of the parallel
+ * schedule as the shard axis): B is broadcast from devs[0] with
+ * NCCL (elv_nccl_init must have been called with the same devices), each
+ * device packs it and computes its rows C_shards[d] = A_shards[d] . B.
+ * rows[d] is the row count of shard d.  packedB_per_dev[d] and B_per_dev[d]
+ * are caller-owned device buffers on device devs[d] (B_per_dev[0] == B root). */
+int elv_nccl_init(int ndev, const int* devs);
+int elv_nccl_destroy(void);
+int elv_gemm_rowshard(int variant, int ndev, const int* devs,
+                      const float* const* A_shards, float* const* B_per_dev,
+                      float* const* packedB_per_dev, float* const* C_shards,
+                      const int* rows, int N, int K, void* const* streams);
+
+/* Thread-local message describing the last error on this thread. */
+const char* elv_last_error(void);
+int elv_abi_version(void);
+const char* elv_variant_name(int variant);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELEVATE_B200_H */

@@ -1,0 +1,87 @@
+/*
+ * TEST INFRASTRUCTURE ONLY -- the CPU oracle for the ELEVATE GEMM hot path.
+ * Never linked into, loaded by, or called from the product path
+ * (paper_2002_02268_b200/); only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg use it.
+ *
+ * Plain-C restatement of what the reference interpreter computes for the
+ * seven scheduled `mm` terms (reference pkg/src/stratir/interp.py):
+ *   - scalars are IEEE f64 (Python float): `mult` is a*b, `add` is a+b
+ *     (interp.py:145-148); an fp32 x fp32 product is exact in f64;
+ *   - `reduce`/`reduceSeq`/`reduceSeqUnroll` are left folds
+ *     acc = op(acc)(x) from the init value (interp.py:84-89);
+ *   - the baseline term folds acc + a_k*b_k over k in order
+ *     (reduceSeq(fun acc p => add(acc)(mult(fst p)(snd p)))(0.0), the term
+ *     DFNF;topDown(fuseReduceMap);lowerToC produces);
+ *   - every schedule that applies split(4) to the reduction and lifts it
+ *     (blocking ... parallel) folds acc + (((0 + p0) + p1) + p2) + p3 over
+ *     chunks of 4 (reduceSeq(add)(0.0) per chunk inside the lifted reduce,
+ *     rules.py:197-222 and 328-358).
+ * Compiled with -ffp-contract=off so the f64 operations round exactly like
+ * CPython's, which makes this bit-identical to interp.run on the same
+ * inputs (pinned in tests/test_oracle.py against tests/golden/).
+ */
+#include <stddef.h>
+#include <stdlib.h>
+
+/* B^T copy so the k loops read contiguously; the arithmetic is unchanged. */
+static double* transpose_b(const float* B, int N, int K) {
+  double* t = (double*)malloc((size_t)N * K * sizeof(double));
+  for (int k = 0; k < K; ++k)
+    for (int j = 0; j < N; ++j) t[(size_t)j * K + k] = (double)B[(size_t)k * N + j];
+  return t;
+}
+
+/* C[i][j] = sum_k A[i][k]*B[k][j], sequential fold (baseline). */
+void oracle_mm_seq_f64(const float* A, const float* B, double* C, int M, int N, int K) {
+  double* bt = transpose_b(B, N, K);
+  for (int i = 0; i < M; ++i) {
+    const float* a = A + (size_t)i * K;
+    for (int j = 0; j < N; ++j) {
+      const double* b = bt + (size_t)j * K;
+      double acc = 0.0;
+      for (int k = 0; k < K; ++k) acc = acc + (double)a[k] * b[k];
+      C[(size_t)i * N + j] = acc;
+    }
+  }
+  free(bt);
+}
+
+/* split(4) + liftReduce association: acc + (((0+p0)+p1)+p2)+p3 per chunk.
+ * K must be a multiple of 4 (the schedule's own divisibility requirement;
+ * zero-padded K for the padded route contributes exact zeros). */
+void oracle_mm_chunk4_f64(const float* A, const float* B, double* C, int M, int N, int K) {
+  double* bt = transpose_b(B, N, K);
+  for (int i = 0; i < M; ++i) {
+    const float* a = A + (size_t)i * K;
+    for (int j = 0; j < N; ++j) {
+      const double* b = bt + (size_t)j * K;
+      double acc = 0.0;
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        double part = 0.0;
+        for (int k = k0; k < k0 + 4 && k < K; ++k) part = part + (double)a[k] * b[k];
+        acc = acc + part;
+      }
+      C[(size_t)i * N + j] = acc;
+    }
+  }
+  free(bt);
+}
+
+/* (|A| |B|)_ij in f64: the magnitude term of the parity bound. */
+void oracle_absprod_f64(const float* A, const float* B, double* C, int M, int N, int K) {
+  double* bt = transpose_b(B, N, K);
+  for (int i = 0; i < M; ++i) {
+    const float* a = A + (size_t)i * K;
+    for (int j = 0; j < N; ++j) {
+      const double* b = bt + (size_t)j * K;
+      double acc = 0.0;
+      for (int k = 0; k < K; ++k) {
+        double x = (double)a[k] * b[k];
+        acc += x < 0 ? -x : x;
+      }
+      C[(size_t)i * N + j] = acc;
+    }
+  }
+  free(bt);
+}

@@ -1,0 +1,326 @@
+// extern "C" boundary of libelevate_b200 (declared in include/elevate_b200.h).
+//
+// Replaces the evaluation of the seven scheduled `mm` terms by the reference
+// interpreter (reference pkg/src/stratir/interp.py:157-162, `run`) with
+// sm_100a kernels.  Plain pointers, sizes and a cudaStream_t only: no torch
+// types cross this boundary.  Errors are reported as negative codes with a
+// thread-local message (elv_last_error), never by aborting.
+
+#include "elv_common.cuh"
+
+#include <dlfcn.h>
+#include <string.h>
+#include <mutex>
+#include <vector>
+
+namespace elv {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return ELV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// synthetic inputs: counter-based, identical on the host
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fill_uniform(float* __restrict__ X, long long n, uint64_t key, long long offset) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t h = splitmix64(key ^ (uint64_t)(offset + i));
+    const int m = (int)(h >> 40);                 // 24 random bits
+    X[i] = (float)(m - (1 << 23)) * (1.0f / (float)(1 << 23));   // exact: [-1, 1)
+  }
+}
+
+// hi = rna_tf32(x); lo = rna_tf32(x - hi)  (x - hi is exact in fp32)
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void k_split_tf32(const float* __restrict__ X, float* __restrict__ hi,
+                             float* __restrict__ lo, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float x = X[i];
+    const float h = tf32_rna(x);
+    hi[i] = h;
+    lo[i] = tf32_rna(x - h);
+  }
+}
+
+int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st) {
+  long long blocks = (n + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_split_tf32<<<(unsigned)blocks, 256, 0, st>>>(X, hi, lo, n);
+  return check_launch("split_tf32");
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved lazily with dlopen so the library loads without it.  The
+// soname libnccl.so.2 resolves to the copy torch already loaded, if any.
+typedef int ncclResult_t_;
+typedef struct { char internal[128]; } ncclUniqueId_;
+typedef void* ncclComm_t_;
+enum { ncclFloat32_ = 7 };
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t_ (*CommInitAll)(ncclComm_t_*, int, const int*) = nullptr;
+  ncclResult_t_ (*CommDestroy)(ncclComm_t_) = nullptr;
+  ncclResult_t_ (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+  ncclResult_t_ (*GroupStart)() = nullptr;
+  ncclResult_t_ (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+};
+static NcclApi g_nccl;
+static std::vector<ncclComm_t_> g_comms;
+static std::vector<int> g_comm_devs;
+static std::mutex g_nccl_mu;
+
+static int nccl_load() {
+  if (g_nccl.h) return ELV_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return set_error(ELV_ENCCL, "dlopen(libnccl.so.2) failed: %s", dlerror());
+  g_nccl.CommInitAll = (decltype(g_nccl.CommInitAll))dlsym(h, "ncclCommInitAll");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
+  g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.CommInitAll || !g_nccl.CommDestroy || !g_nccl.Broadcast || !g_nccl.GroupStart ||
+      !g_nccl.GroupEnd)
+    return set_error(ELV_ENCCL, "libnccl.so.2 lacks a required symbol");
+  g_nccl.h = h;
+  return ELV_OK;
+}
+
+static int nccl_err(ncclResult_t_ r, const char* what) {
+  return set_error(ELV_ENCCL, "%s: %s", what,
+                   g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error");
+}
+
+}  // namespace elv
+
+using namespace elv;
+
+static bool bad_ptr(const void* p) { return p == nullptr; }
+
+extern "C" {
+
+const char* elv_last_error(void) { return g_err; }
+int elv_abi_version(void) { return ELV_ABI_VERSION; }
+
+const char* elv_variant_name(int v) {
+  static const char* names[ELV_NUM_VARIANTS] = {
+      "baseline", "blocking", "vectorized", "loopPerm", "arrayPacking",
+      "cacheBlocks", "parallel", "parallel_tf32x3"};
+  return (v >= 0 && v < ELV_NUM_VARIANTS) ? names[v] : "unknown";
+}
+
+size_t elv_pack_b_bytes(int K, int N) {
+  if (K < 1 || N < 1) return 0;
+  return packed_cols(N) * (size_t)K * sizeof(float);
+}
+
+size_t elv_gemm_workspace_bytes(int variant, int M, int N, int K) {
+  if (M < 1 || N < 1 || K < 1) return 0;
+  switch (variant) {
+    case ELV_ARRAYPACKING:
+    case ELV_CACHEBLOCKS:
+    case ELV_PARALLEL: return elv_pack_b_bytes(K, N);
+    case ELV_PARALLEL_TF32X3: return tf32x3_workspace_bytes(M, N, K);
+    default: return 0;
+  }
+}
+
+static int check_args(const float* A, const float* B, const float* C, int M, int N, int K,
+                      int lda, int ldb, int ldc, bool need_ldb) {
+  if (bad_ptr(A) || bad_ptr(B) || bad_ptr(C))
+    return set_error(ELV_EINVAL, "null matrix pointer");
+  if (M < 1 || N < 1 || K < 1)
+    return set_error(ELV_EINVAL, "sizes must be positive (M=%d N=%d K=%d)", M, N, K);
+  if (lda < K || (need_ldb && ldb < N) || ldc < N)
+    return set_error(ELV_EINVAL, "leading dimension too small (lda=%d ldb=%d ldc=%d)", lda, ldb, ldc);
+  return ELV_OK;
+}
+
+int elv_pack_b(const float* B, float* packedB, int K, int N, int ldb, int blk, void* stream) {
+  if (blk != kPanel) return set_error(ELV_EINVAL, "pack_b: block %d unsupported (32 only)", blk);
+  if (bad_ptr(B) || bad_ptr(packedB)) return set_error(ELV_EINVAL, "pack_b: null pointer");
+  if (K < 1 || N < 1 || ldb < N) return set_error(ELV_EINVAL, "pack_b: bad shape");
+  return launch_pack_b(B, packedB, K, N, ldb, (cudaStream_t)stream);
+}
+
+int elv_split_tf32(const float* X, float* hi, float* lo, long long n, void* stream) {
+  if (bad_ptr(X) || bad_ptr(hi) || bad_ptr(lo) || n < 0)
+    return set_error(ELV_EINVAL, "split_tf32: bad arguments");
+  if (n == 0) return ELV_OK;
+  return launch_split_tf32(X, hi, lo, n, (cudaStream_t)stream);
+}
+
+int elv_fill_uniform(float* X, long long n, unsigned long long seed, unsigned int tensor_id,
+                     long long offset, void* stream) {
+  if (bad_ptr(X) || n < 0 || offset < 0) return set_error(ELV_EINVAL, "fill_uniform: bad arguments");
+  if (n == 0) return ELV_OK;
+  const uint64_t key = (seed << 48) ^ ((uint64_t)tensor_id << 40);
+  long long blocks = (n + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  k_fill_uniform<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(X, n, key, offset);
+  return check_launch("fill_uniform");
+}
+
+int elv_gemm_prepacked(int variant, const float* A, const float* packedB, float* C,
+                       int M, int N, int K, int lda, int ldc, void* stream) {
+  int rc = check_args(A, packedB, C, M, N, K, lda, 0, ldc, false);
+  if (rc) return rc;
+  if (variant != ELV_ARRAYPACKING && variant != ELV_CACHEBLOCKS && variant != ELV_PARALLEL)
+    return set_error(ELV_EVARIANT, "gemm_prepacked: variant %d does not consume packedB", variant);
+  return launch_simt(variant, A, nullptr, packedB, C, M, N, K, lda, 0, ldc, (cudaStream_t)stream);
+}
+
+static int check_variant_ws(int variant, int M, int N, int K, void* workspace, size_t workspace_bytes) {
+  if (variant < 0 || variant >= ELV_NUM_VARIANTS)
+    return set_error(ELV_EVARIANT, "unknown variant %d", variant);
+  const size_t need = elv_gemm_workspace_bytes(variant, M, N, K);
+  if (need > 0 && (workspace == nullptr || workspace_bytes < need))
+    return set_error(ELV_EWORKSPACE, "variant %s needs %zu workspace bytes, got %zu",
+                     elv_variant_name(variant), need, workspace_bytes);
+  return ELV_OK;
+}
+
+int elv_gemm_prepare(int variant, const float* A, const float* B, int M, int N, int K, int lda,
+                     int ldb, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_args(A, B, B, M, N, K, lda, ldb, N, true);
+  if (!rc) rc = check_variant_ws(variant, M, N, K, workspace, workspace_bytes);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (variant) {
+    case ELV_ARRAYPACKING:
+    case ELV_CACHEBLOCKS:
+    case ELV_PARALLEL:
+      return launch_pack_b(B, static_cast<float*>(workspace), K, N, ldb, st);
+    case ELV_PARALLEL_TF32X3:
+      return tf32x3_prepare(A, B, M, N, K, lda, ldb, workspace, workspace_bytes, st);
+    default:
+      return ELV_OK;   // 0..3 read A and B in place
+  }
+}
+
+int elv_gemm_compute(int variant, const float* A, const float* B, float* C, int M, int N, int K,
+                     int lda, int ldb, int ldc, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_args(A, B, C, M, N, K, lda, ldb, ldc, true);
+  if (!rc) rc = check_variant_ws(variant, M, N, K, workspace, workspace_bytes);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (variant) {
+    case ELV_BASELINE:
+    case ELV_BLOCKING:
+    case ELV_VECTORIZED:
+    case ELV_LOOPPERM:
+      return launch_simt(variant, A, B, nullptr, C, M, N, K, lda, ldb, ldc, st);
+    case ELV_ARRAYPACKING:
+    case ELV_CACHEBLOCKS:
+    case ELV_PARALLEL:
+      return launch_simt(variant, A, nullptr, static_cast<const float*>(workspace), C, M, N, K, lda, 0,
+                         ldc, st);
+    case ELV_PARALLEL_TF32X3:
+      return tf32x3_compute(C, M, N, K, ldc, workspace, workspace_bytes, st);
+  }
+  return set_error(ELV_EVARIANT, "unknown variant %d", variant);
+}
+
+int elv_gemm(int variant, const float* A, const float* B, float* C, int M, int N, int K,
+             int lda, int ldb, int ldc, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_args(A, B, C, M, N, K, lda, ldb, ldc, true);
+  if (rc) return rc;
+  rc = elv_gemm_prepare(variant, A, B, M, N, K, lda, ldb, workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  return elv_gemm_compute(variant, A, B, C, M, N, K, lda, ldb, ldc, workspace, workspace_bytes, stream);
+}
+
+int elv_nccl_init(int ndev, const int* devs) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (ndev < 1 || devs == nullptr) return set_error(ELV_EINVAL, "nccl_init: bad device list");
+  int rc = nccl_load();
+  if (rc) return rc;
+  for (auto c : g_comms) g_nccl.CommDestroy(c);
+  g_comms.assign(ndev, nullptr);
+  g_comm_devs.assign(devs, devs + ndev);
+  ncclResult_t_ r = g_nccl.CommInitAll(g_comms.data(), ndev, devs);
+  if (r != 0) {
+    g_comms.clear();
+    g_comm_devs.clear();
+    return nccl_err(r, "ncclCommInitAll");
+  }
+  return ELV_OK;
+}
+
+int elv_nccl_destroy(void) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  for (auto c : g_comms) if (g_nccl.CommDestroy) g_nccl.CommDestroy(c);
+  g_comms.clear();
+  g_comm_devs.clear();
+  return ELV_OK;
+}
+
+int elv_gemm_rowshard(int variant, int ndev, const int* devs, const float* const* A_shards,
+                      float* const* B_per_dev, float* const* packedB_per_dev,
+                      float* const* C_shards, const int* rows, int N, int K,
+                      void* const* streams) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (variant != ELV_ARRAYPACKING && variant != ELV_CACHEBLOCKS && variant != ELV_PARALLEL)
+    return set_error(ELV_EVARIANT, "gemm_rowshard: variant %d not supported (4..6)", variant);
+  if (ndev < 1 || !devs || !A_shards || !B_per_dev || !packedB_per_dev || !C_shards || !rows ||
+      !streams || N < 1 || K < 1)
+    return set_error(ELV_EINVAL, "gemm_rowshard: bad arguments");
+  if ((int)g_comms.size() != ndev) return set_error(ELV_ENCCL, "gemm_rowshard: call elv_nccl_init first");
+  for (int d = 0; d < ndev; ++d)
+    if (g_comm_devs[d] != devs[d]) return set_error(ELV_ENCCL, "gemm_rowshard: device list differs from elv_nccl_init");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  const size_t count = (size_t)K * N;
+  // B lives in B_per_dev[0] on devs[0]: broadcast it to every device
+  ncclResult_t_ r = g_nccl.GroupStart();
+  if (r != 0) return nccl_err(r, "ncclGroupStart");
+  for (int d = 0; d < ndev; ++d) {
+    cudaSetDevice(devs[d]);
+    r = g_nccl.Broadcast(B_per_dev[0], B_per_dev[d], count, ncclFloat32_, 0, g_comms[d],
+                         (cudaStream_t)streams[d]);
+    if (r != 0) { g_nccl.GroupEnd(); cudaSetDevice(prev); return nccl_err(r, "ncclBroadcast"); }
+  }
+  r = g_nccl.GroupEnd();
+  if (r != 0) { cudaSetDevice(prev); return nccl_err(r, "ncclGroupEnd"); }
+  for (int d = 0; d < ndev; ++d) {
+    cudaSetDevice(devs[d]);
+    if (rows[d] <= 0) continue;
+    int rc = launch_pack_b(B_per_dev[d], packedB_per_dev[d], K, N, N, (cudaStream_t)streams[d]);
+    if (!rc) rc = launch_simt(variant, A_shards[d], nullptr, packedB_per_dev[d], C_shards[d],
+                              rows[d], N, K, K, 0, N, (cudaStream_t)streams[d]);
+    if (rc) { cudaSetDevice(prev); return rc; }
+  }
+  cudaSetDevice(prev);
+  return ELV_OK;
+}
+
+}  // extern "C"

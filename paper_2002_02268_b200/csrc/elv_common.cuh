@@ -1,0 +1,45 @@
+// Shared internals of libelevate_b200: error plumbing and launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "../../include/elevate_b200.h"
+
+namespace elv {
+
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+
+constexpr int kPanel = 32;          // packB block (rules.py:516 default 32)
+constexpr int kPackAlign = 128;     // packed column count padded to 4 panels
+
+inline size_t packed_cols(int N) { return (size_t)((N + kPackAlign - 1) / kPackAlign) * kPackAlign; }
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// SIMT ladder (simt_gemm.cu)
+int launch_simt(int variant, const float* A, const float* B, const float* packedB,
+                float* C, int M, int N, int K, int lda, int ldb, int ldc, cudaStream_t st);
+int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStream_t st);
+
+// tcgen05 3xTF32 (tf32x3_gemm.cu)
+size_t tf32x3_workspace_bytes(int M, int N, int K);
+int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb,
+                   void* ws, size_t ws_bytes, cudaStream_t st);
+int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st);
+
+}  // namespace elv

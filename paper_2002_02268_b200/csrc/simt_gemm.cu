@@ -1,0 +1,484 @@
+// SIMT fp32 kernel ladder: one sm_100a kernel per ELEVATE/TVM schedule.
+//
+// Each kernel is the B200 lowering of the low-level patterns the schedule's
+// rewrite leaves in the `mm` term (reference rules.py:391-456, 516-549):
+//   mapSeq/reduceSeq           -> per-thread loops             (K0)
+//   split(32) of rows/cols     -> 32x32 CTA tile in SMEM       (K1, K2)
+//   split(4) + liftReduce      -> k strip-mined by 4, chunk partial sums
+//   mapVec (vectorize(32))     -> 128-bit loads/stores         (K2..K6)
+//   reorder (loopPerm)         -> register outer-product tiles (K3..K6)
+//   packB / toMem(packed)      -> packedB[N/32][K][32] panels  (K4..K6)
+//   toMem(acc) + unroll        -> 8x8 register accumulators    (K5, K6)
+//   mapPar (outer row blocks)  -> persistent grid over all SMs (K6)
+// Everything computes in fp32 with FFMA; the f64 reference (interp.py:145-148)
+// is matched within the sqrt(K)-scaled bound of SURVEY.md §8(d).
+//
+// All kernels take arbitrary M, N, K >= 1 (predicated tails, SURVEY.md §7
+// hard part 2) and any leading dimensions; 128-bit paths are used only when
+// the operand is 16-byte aligned, otherwise the same kernel loads scalars.
+
+#include "elv_common.cuh"
+
+namespace elv {
+namespace {
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+// ---------------------------------------------------------------------------
+// K0 baseline: mapSeq(arow => mapSeq(bcol => reduceSeq(acc + a*b)(0)(zip)))
+// One thread per C(i,j); `transpose(b)` is a strided view (column reads of B
+// are coalesced across the warp's j), the k loop is the reduceSeq.
+__global__ void __launch_bounds__(256)
+k0_baseline(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+            int M, int N, int K, int lda, int ldb, int ldc) {
+  const int j = blockIdx.x * 32 + threadIdx.x;
+  const int i = blockIdx.y * 8 + threadIdx.y;
+  if (i >= M || j >= N) return;
+  const float* a = A + (size_t)i * lda;
+  const float* b = B + j;
+  float acc = 0.f;
+  for (int k = 0; k < K; ++k) acc = fmaf(__ldg(a + k), __ldg(b + (size_t)k * ldb), acc);
+  C[(size_t)i * ldc + j] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K1 blocking: tile(32,32) -> 32x32 C tile per CTA, A/B tiles staged in SMEM;
+// split(4) of the reduction + liftReduce -> the k loop runs in chunks of 4
+// whose partial sums start at 0 and are added to the accumulator, the same
+// association the lowered term has (reduceSeq(add)(0.0) per chunk).
+constexpr int K1_BK = 32;
+__global__ void __launch_bounds__(256)
+k1_blocking(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+            int M, int N, int K, int lda, int ldb, int ldc) {
+  __shared__ float As[32][K1_BK + 1];
+  __shared__ float Bs[K1_BK][32];
+  const int tx = threadIdx.x, ty = threadIdx.y;    // 32 x 8
+  const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < K; k0 += K1_BK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int rr = ty + 8 * r;
+      const int gi = row0 + rr, gk = k0 + tx;
+      As[rr][tx] = (gi < M && gk < K) ? __ldg(A + (size_t)gi * lda + gk) : 0.f;
+      const int bk = k0 + rr, bj = col0 + tx;
+      Bs[rr][tx] = (bk < K && bj < N) ? __ldg(B + (size_t)bk * ldb + bj) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kc = 0; kc < K1_BK; kc += 4) {          // split(4): chunk loop
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        float part = 0.f;                             // reduceSeq(add)(0.0)(chunk)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) part = fmaf(As[ty + 8 * r][kc + kk], Bs[kc + kk][tx], part);
+        acc[r] += part;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gi = row0 + ty + 8 * r, gj = col0 + tx;
+    if (gi < M && gj < N) C[(size_t)gi * ldc + gj] = acc[r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 vectorized: K1 plus vectorize(32) -> 128-bit (float4) global loads and
+// stores and float4 SMEM reads of B; each thread owns 1 row x 4 columns.
+__global__ void __launch_bounds__(256)
+k2_vectorized(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+              int M, int N, int K, int lda, int ldb, int ldc) {
+  __shared__ float As[32][K1_BK + 1];
+  __shared__ __align__(16) float Bs[K1_BK][32];
+  const int tid = threadIdx.x;
+  const int r = tid >> 3, c4 = (tid & 7) * 4;
+  const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
+  const bool vecA = aligned16(A) && (lda & 3) == 0;
+  const bool vecB = aligned16(B) && (ldb & 3) == 0;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < K; k0 += K1_BK) {
+    {  // A tile: row r, k = k0 + c4 .. +3
+      const int gi = row0 + r, gk = k0 + c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gi < M) {
+        const float* p = A + (size_t)gi * lda + gk;
+        if (vecA && gk + 3 < K) v = __ldg(reinterpret_cast<const float4*>(p));
+        else {
+          if (gk + 0 < K) v.x = __ldg(p + 0);
+          if (gk + 1 < K) v.y = __ldg(p + 1);
+          if (gk + 2 < K) v.z = __ldg(p + 2);
+          if (gk + 3 < K) v.w = __ldg(p + 3);
+        }
+      }
+      As[r][c4 + 0] = v.x; As[r][c4 + 1] = v.y; As[r][c4 + 2] = v.z; As[r][c4 + 3] = v.w;
+    }
+    {  // B tile: k row r, columns col0 + c4 .. +3
+      const int gk = k0 + r, gj = col0 + c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gk < K) {
+        const float* p = B + (size_t)gk * ldb + gj;
+        if (vecB && gj + 3 < N) v = __ldg(reinterpret_cast<const float4*>(p));
+        else {
+          if (gj + 0 < N) v.x = __ldg(p + 0);
+          if (gj + 1 < N) v.y = __ldg(p + 1);
+          if (gj + 2 < N) v.z = __ldg(p + 2);
+          if (gj + 3 < N) v.w = __ldg(p + 3);
+        }
+      }
+      *reinterpret_cast<float4*>(&Bs[r][c4]) = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kc = 0; kc < K1_BK; kc += 4) {
+      float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float a = As[r][kc + kk];
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[kc + kk][c4]);
+        part[0] = fmaf(a, b.x, part[0]); part[1] = fmaf(a, b.y, part[1]);
+        part[2] = fmaf(a, b.z, part[2]); part[3] = fmaf(a, b.w, part[3]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += part[q];
+    }
+    __syncthreads();
+  }
+  const int gi = row0 + r, gj = col0 + c4;
+  if (gi < M) {
+    float* p = C + (size_t)gi * ldc + gj;
+    if (aligned16(C) && (ldc & 3) == 0 && gj + 3 < N) {
+      *reinterpret_cast<float4*>(p) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) if (gj + q < N) p[q] = acc[q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Shared loaders for the register-tiled kernels.
+// A tile (BM rows x BK k) is stored transposed in SMEM: As[k][m].
+template <int BM, int BK>
+__device__ __forceinline__ float4 load_a4(const float* __restrict__ A, int M, int K, int lda,
+                                          bool vecA, int gi, int gk) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (gi < M) {
+    const float* p = A + (size_t)gi * lda + gk;
+    if (vecA && gk + 3 < K) v = __ldg(reinterpret_cast<const float4*>(p));
+    else {
+      if (gk + 0 < K) v.x = __ldg(p + 0);
+      if (gk + 1 < K) v.y = __ldg(p + 1);
+      if (gk + 2 < K) v.z = __ldg(p + 2);
+      if (gk + 3 < K) v.w = __ldg(p + 3);
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ float4 load_b4_rowmajor(const float* __restrict__ B, int N, int K, int ldb,
+                                                   bool vecB, int gk, int gj) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (gk < K) {
+    const float* p = B + (size_t)gk * ldb + gj;
+    if (vecB && gj + 3 < N) v = __ldg(reinterpret_cast<const float4*>(p));
+    else {
+      if (gj + 0 < N) v.x = __ldg(p + 0);
+      if (gj + 1 < N) v.y = __ldg(p + 1);
+      if (gj + 2 < N) v.z = __ldg(p + 2);
+      if (gj + 3 < N) v.w = __ldg(p + 3);
+    }
+  }
+  return v;
+}
+
+// packedB[p][k][c]: rows of 32 floats; always 16B-aligned, zero past N
+__device__ __forceinline__ float4 load_b4_packed(const float* __restrict__ P, int K, int gk, int gj) {
+  if (gk >= K) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const int p = gj >> 5, c = gj & 31;
+  return __ldg(reinterpret_cast<const float4*>(P + ((size_t)p * K + gk) * kPanel + c));
+}
+
+// ---------------------------------------------------------------------------
+// K3 loopPerm / K4 arrayPacking: 64x64 CTA tile, 16x16 threads, each thread a
+// 4x4 register outer product per k (A-stationary micro-tile: the reordered
+// nest keeps a k-slice of A and B in registers and sweeps the 4x4 block).
+// PACKED selects packedB panels (arrayPacking's toMem) over row-major B.
+template <bool PACKED>
+__global__ void __launch_bounds__(256)
+k34_outer4x4(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+             int M, int N, int K, int lda, int ldb, int ldc) {
+  constexpr int BM = 64, BN = 64, BK = 8;
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+  const bool vecA = aligned16(A) && (lda & 3) == 0;
+  const bool vecB = PACKED || (aligned16(B) && (ldb & 3) == 0);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  // A: 64 rows x 8 k = 128 float4 (threads 0..127); B: 8 x 64 = 128 float4 (threads 128..255)
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    if (tid < 128) {
+      const int r = tid >> 1, kq = (tid & 1) * 4;
+      const float4 v = load_a4<BM, BK>(A, M, K, lda, vecA, row0 + r, k0 + kq);
+      As[kq + 0][r] = v.x; As[kq + 1][r] = v.y; As[kq + 2][r] = v.z; As[kq + 3][r] = v.w;
+    } else {
+      const int t = tid - 128;
+      const int kr = t >> 4, c4 = (t & 15) * 4;
+      float4 v;
+      if (PACKED) v = load_b4_packed(B, K, k0 + kr, col0 + c4);
+      else v = load_b4_rowmajor(B, N, K, ldb, vecB, k0 + kr, col0 + c4);
+      *reinterpret_cast<float4*>(&Bs[kr][c4]) = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w};
+      const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gi = row0 + ty * 4 + i, gj = col0 + tx * 4;
+    if (gi >= M) continue;
+    float* p = C + (size_t)gi * ldc + gj;
+    if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    else
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = acc[i][j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5 cacheBlocks / K6 parallel: 128x128 CTA tile over packedB, 8 warps laid
+// out 2 (M) x 4 (N), warp tile 64x32, lane grid 8 x 4, each thread an 8x8
+// register accumulator block (the toMem'd block accumulator of cache_write),
+// k unrolled by BK=8 (reduceSeqUnroll).
+//   K5: one tile per CTA, single-buffered SMEM.
+//   K6: mapPar -> persistent CTAs (2 per SM) sweeping an L2-grouped tile
+//       order, SMEM double-buffered with register prefetch of the next
+//       k-block so global latency overlaps the FFMA stream.
+constexpr int G_BM = 128, G_BN = 128, G_BK = 8, G_APAD = 4;
+
+struct TileCoord { int m, n; };
+
+__device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
+  constexpr int GROUP = 8;                        // row-tiles per L2 group
+  const int per_group = GROUP * tiles_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP;
+  const int gm = min(tiles_m - first_m, GROUP);
+  const int in = t - g * per_group;
+  return {first_m + in % gm, in / gm};
+}
+
+template <bool PARALLEL>
+__global__ void __launch_bounds__(256, 2)
+k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* __restrict__ C,
+               int M, int N, int K, int lda, int ldc) {
+  constexpr int NBUF = PARALLEL ? 2 : 1;
+  __shared__ __align__(16) float As[NBUF][G_BK][G_BM + G_APAD];
+  __shared__ __align__(16) float Bs[NBUF][G_BK][G_BN];
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;         // 2 x 4 warps
+  const int lm = lane >> 2, ln = lane & 3;         // 8 x 4 lanes
+  const int trow = wm * 64 + lm * 4;               // + {0..3} and +32
+  const int tcol = wn * 32 + ln * 4;               // + {0..3} and +16
+  const bool vecA = aligned16(A) && (lda & 3) == 0;
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+
+  // loader roles: A float4 (row = tid/2, k = (tid&1)*4); B float4 from panel tid/64
+  const int a_r = tid >> 1, a_k = (tid & 1) * 4;
+  const int b_p = tid >> 6, b_in = tid & 63, b_k = b_in >> 3, b_c = (b_in & 7) * 4;
+
+  const int tiles_m = (M + G_BM - 1) / G_BM, tiles_n = (N + G_BN - 1) / G_BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int first = PARALLEL ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+  const int stride = PARALLEL ? (int)gridDim.x : num_tiles;
+
+  for (int t = first; t < num_tiles; t += stride) {
+    TileCoord tc = PARALLEL ? tile_of(t, tiles_m, tiles_n) : TileCoord{(int)blockIdx.y, (int)blockIdx.x};
+    const int row0 = tc.m * G_BM, col0 = tc.n * G_BN;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    const float* Bpanel = P + (size_t)((col0 >> 5) + b_p) * K * kPanel + b_c;
+    auto ldA = [&](int k0) { return load_a4<G_BM, G_BK>(A, M, K, lda, vecA, row0 + a_r, k0 + a_k); };
+    auto ldB = [&](int k0) {
+      const int gk = k0 + b_k;
+      return gk < K ? __ldg(reinterpret_cast<const float4*>(Bpanel + (size_t)gk * kPanel))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto stage = [&](int buf, float4 va, float4 vb) {
+      As[buf][a_k + 0][a_r] = va.x; As[buf][a_k + 1][a_r] = va.y;
+      As[buf][a_k + 2][a_r] = va.z; As[buf][a_k + 3][a_r] = va.w;
+      *reinterpret_cast<float4*>(&Bs[buf][b_k][b_p * 32 + b_c]) = vb;
+    };
+    auto compute = [&](int buf) {
+#pragma unroll
+      for (int k = 0; k < G_BK; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][trow]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][trow + 32]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol + 16]);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+    };
+
+    if (PARALLEL) {
+      float4 va = ldA(0), vb = ldB(0);
+      stage(0, va, vb);
+      __syncthreads();
+      int buf = 0;
+      for (int k0 = 0; k0 < K; k0 += G_BK) {
+        const bool more = k0 + G_BK < K;
+        if (more) { va = ldA(k0 + G_BK); vb = ldB(k0 + G_BK); }
+        compute(buf);
+        if (more) stage(buf ^ 1, va, vb);
+        __syncthreads();
+        buf ^= 1;
+      }
+    } else {
+      for (int k0 = 0; k0 < K; k0 += G_BK) {
+        stage(0, ldA(k0), ldB(k0));
+        __syncthreads();
+        compute(0);
+        __syncthreads();
+      }
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = col0 + tcol + h * 16;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float* v = &acc[i][h * 4];
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// packB: packedB[p][k][c] = B[k][32p + c], zero-filled past N (rules.py:516-549,
+// TVM packedB PAPER.md:49-50).  Pure layout transform, HBM-bound: every
+// thread moves one float4; reads are coalesced along B's rows, writes along
+// the panel rows.
+__global__ void __launch_bounds__(256)
+k_pack_b(const float* __restrict__ B, float* __restrict__ P, int K, int N, int ldb,
+         int panels, bool vecB) {
+  const long long total4 = (long long)panels * K * (kPanel / 4);
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total4;
+       q += (long long)gridDim.x * blockDim.x) {
+    // q enumerates (k, p, c4) with c4 fastest so reads of a B row coalesce
+    const int c4 = (int)(q & 7) * 4;
+    const long long kp = q >> 3;
+    const int p = (int)(kp % panels);
+    const int k = (int)(kp / panels);
+    const int j = p * kPanel + c4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* src = B + (size_t)k * ldb + j;
+    if (vecB && j + 3 < N) v = __ldg(reinterpret_cast<const float4*>(src));
+    else {
+      if (j + 0 < N) v.x = __ldg(src + 0);
+      if (j + 1 < N) v.y = __ldg(src + 1);
+      if (j + 2 < N) v.z = __ldg(src + 2);
+      if (j + 3 < N) v.w = __ldg(src + 3);
+    }
+    *reinterpret_cast<float4*>(P + ((size_t)p * K + k) * kPanel + c4) = v;
+  }
+}
+
+}  // namespace
+
+int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStream_t st) {
+  const int panels = (int)(packed_cols(N) / kPanel);
+  const bool vecB = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && (ldb & 3) == 0;
+  const long long total4 = (long long)panels * K * (kPanel / 4);
+  long long blocks = (total4 + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_pack_b<<<(unsigned)blocks, 256, 0, st>>>(B, packedB, K, N, ldb, panels, vecB);
+  return check_launch("pack_b");
+}
+
+int launch_simt(int variant, const float* A, const float* B, const float* packedB,
+                float* C, int M, int N, int K, int lda, int ldb, int ldc, cudaStream_t st) {
+  switch (variant) {
+    case ELV_BASELINE: {
+      dim3 grid((N + 31) / 32, (M + 7) / 8);
+      k0_baseline<<<grid, dim3(32, 8), 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc);
+      return check_launch("gemm_baseline");
+    }
+    case ELV_BLOCKING: {
+      dim3 grid((N + 31) / 32, (M + 31) / 32);
+      k1_blocking<<<grid, dim3(32, 8), 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc);
+      return check_launch("gemm_blocking");
+    }
+    case ELV_VECTORIZED: {
+      dim3 grid((N + 31) / 32, (M + 31) / 32);
+      k2_vectorized<<<grid, 256, 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc);
+      return check_launch("gemm_vectorized");
+    }
+    case ELV_LOOPPERM: {
+      dim3 grid((N + 63) / 64, (M + 63) / 64);
+      k34_outer4x4<false><<<grid, 256, 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc);
+      return check_launch("gemm_loopperm");
+    }
+    case ELV_ARRAYPACKING: {
+      dim3 grid((N + 63) / 64, (M + 63) / 64);
+      k34_outer4x4<true><<<grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, 0, ldc);
+      return check_launch("gemm_arraypacking");
+    }
+    case ELV_CACHEBLOCKS: {
+      dim3 grid((N + G_BN - 1) / G_BN, (M + G_BM - 1) / G_BM);
+      k56_packed_8x8<false><<<grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, ldc);
+      return check_launch("gemm_cacheblocks");
+    }
+    case ELV_PARALLEL: {
+      const long long tiles = (long long)((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN);
+      long long grid = (long long)num_sms() * 2;
+      if (grid > tiles) grid = tiles;
+      k56_packed_8x8<true><<<(unsigned)grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, ldc);
+      return check_launch("gemm_parallel");
+    }
+    default:
+      return set_error(ELV_EVARIANT, "launch_simt: variant %d is not a SIMT variant", variant);
+  }
+}
+
+}  // namespace elv

@@ -1,0 +1,418 @@
+// K7: the parallel schedule's dense contraction on the 5th-generation tensor
+// cores, in fp32-accurate 3xTF32 form.
+//
+//   x = hi + lo,  hi = rna_tf32(x), lo = rna_tf32(x - hi)
+//   C = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi       (A_lo.B_lo ~ 2^-24, dropped)
+//
+// accumulated in fp32 in TMEM.  The result meets the same sqrt(K)-scaled fp32
+// bound as the SIMT kernels; a single TF32 product does not.
+//
+// Pipeline (one persistent CTA per SM, 6 warps):
+//   warp 0      TMA producer: A_hi/A_lo (BM x BK) and Bt_hi/Bt_lo (BN x BK)
+//               tiles into a STAGES-deep SMEM ring (64B swizzle), mbarrier
+//               complete_tx signalling.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::tf32, M=128, N=256, K=8 per instruction, 3 per k-step),
+//               tcgen05.commit frees SMEM slots and publishes accumulators.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> global C, with
+//               two TMEM accumulators (2 x 256 columns) so the epilogue of
+//               tile i overlaps the MMAs of tile i+1.
+// The split prepass (split_a / split_transpose_b below) is the packB of this
+// variant: it writes the hi/lo planes K-major, zero-padded to BK, so TMA
+// boxes and UMMA K-major descriptors apply to both operands.
+
+#include "elv_common.cuh"
+
+#include <cuda.h>
+#include <mutex>
+
+namespace elv {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 16;        // BK fp32 = 64 B rows (SWIZZLE_64B)
+constexpr int STAGES = 4;
+constexpr int NUM_THREADS = 192;
+constexpr int A_TILE_BYTES = BM * BK * 4;         // 8 KB
+constexpr int B_TILE_BYTES = BN * BK * 4;         // 16 KB
+constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;   // 48 KB
+constexpr int TMEM_COLS = 512;                    // 2 accumulators x 256 fp32 columns
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+
+inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+
+// ----------------------------------------------------------------------------
+// PTX wrappers (sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 64B swizzle, 8-row atoms of 512 B.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                         // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;                // SBO: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;                         // SWIZZLE_64B
+  return d;
+}
+
+// instruction descriptor: D=f32, A=B=tf32, both K-major, N=256, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+struct TileSched {
+  int tiles_m, tiles_n;
+  __device__ void coords(int t, int& m0, int& n0) const {
+    constexpr int GROUP = 16;                       // row-tiles per L2 group
+    const int per_group = GROUP * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * GROUP;
+    const int gm = min(tiles_m - first_m, GROUP);
+    const int in = t - g * per_group;
+    m0 = (first_m + in % gm) * BM;
+    n0 = (in / gm) * BN;
+  }
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+          const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+          float* __restrict__ C, int M, int N, int ldc, int num_kb) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN};
+  const int num_tiles = sched.tiles_m * sched.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_ahi); tma_prefetch_desc(&map_alo);
+    tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int s = 0; uint32_t ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int m0, n0;
+        sched.coords(t, m0, n0);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          const int k0 = kb * BK;
+          tma_load_2d(&map_ahi, &full[s], st, k0, m0);
+          tma_load_2d(&map_alo, &full[s], st + A_TILE_BYTES, k0, m0);
+          tma_load_2d(&map_bhi, &full[s], st + 2 * A_TILE_BYTES, k0, n0);
+          tma_load_2d(&map_blo, &full[s], st + 2 * A_TILE_BYTES + B_TILE_BYTES, k0, n0);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      int s = 0; uint32_t ph = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t use = (uint32_t)(it >> 1);
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+          const uint64_t ahi = umma_desc_sw64(st);
+          const uint64_t alo = umma_desc_sw64(st + A_TILE_BYTES);
+          const uint64_t bhi = umma_desc_sw64(st + 2 * A_TILE_BYTES);
+          const uint64_t blo = umma_desc_sw64(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t koff = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along the row
+            const uint32_t first = (kb | k) != 0;
+            tc_mma_tf32(d, ahi + koff, bhi + koff, kIdesc, first);
+            tc_mma_tf32(d, ahi + koff, blo + koff, kIdesc, 1u);
+            tc_mma_tf32(d, alo + koff, bhi + koff, kIdesc, 1u);
+          }
+          tc_commit(&empty[s]);                 // frees the slot when these MMAs finish
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);                 // accumulator complete
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int g = warp & 3;                      // TMEM lane group this warp may access
+    const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int m0, n0;
+      sched.coords(t, m0, n0);
+      const int acc = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int row = m0 + g * 32 + lane;
+      float* crow = C + (size_t)row * ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+        const int col = n0 + c * 32;
+        if (row < M && col < N) {
+          if (vecC && col + 31 < N) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(crow + col + 4 * q) =
+                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                              __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (col + q < N) crow[col + q] = __uint_as_float(r[q]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// split prepass: A -> A_hi, A_lo (M x Kp, K-major);  B -> Bt_hi, Bt_lo (N x Kp)
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void __launch_bounds__(256)
+k_split_a(const float* __restrict__ A, float* __restrict__ hi, float* __restrict__ lo, int M, int K,
+          int lda, int Kp) {
+  const long long total = (long long)M * Kp;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / Kp), k = (int)(i - (long long)r * Kp);
+    const float x = k < K ? __ldg(A + (size_t)r * lda + k) : 0.f;
+    const float h = tf32_rna(x);
+    hi[i] = h;
+    lo[i] = tf32_rna(x - h);
+  }
+}
+
+// 32x32 tiles through SMEM: reads of B rows and writes of Bt rows coalesce
+__global__ void __launch_bounds__(256)
+k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* __restrict__ lo,
+                    int K, int N, int ldb, int Kp) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int k = k0 + ty + 8 * r, n = n0 + tx;
+    t[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int n = n0 + ty + 8 * r, k = k0 + tx;
+    if (n < N && k < Kp) {
+      const float x = t[tx][ty + 8 * r];
+      const float h = tf32_rna(x);
+      hi[(size_t)n * Kp + k] = h;
+      lo[(size_t)n * Kp + k] = tf32_rna(x - h);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ELV_OK;
+}
+
+}  // namespace
+
+size_t tf32x3_workspace_bytes(int M, int N, int K) {
+  const long long Kp = round_up(K, BK);
+  return (size_t)(2 * (long long)M * Kp + 2 * (long long)N * Kp) * sizeof(float) + 256;
+}
+
+struct Planes { float *a_hi, *a_lo, *b_hi, *b_lo; int Kp; };
+
+static Planes carve(void* ws, int M, int N, int K) {
+  Planes p;
+  p.Kp = (int)round_up(K, BK);
+  float* base = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127));
+  p.a_hi = base;
+  p.a_lo = p.a_hi + (size_t)M * p.Kp;
+  p.b_hi = p.a_lo + (size_t)M * p.Kp;
+  p.b_lo = p.b_hi + (size_t)N * p.Kp;
+  return p;
+}
+
+int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
+    return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
+  const Planes p = carve(ws, M, N, K);
+  long long blocks = ((long long)M * p.Kp + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  k_split_a<<<(unsigned)blocks, 256, 0, st>>>(A, p.a_hi, p.a_lo, M, K, lda, p.Kp);
+  int rc = check_launch("tf32x3_split_a");
+  if (rc) return rc;
+  dim3 grid((N + 31) / 32, (p.Kp + 31) / 32);
+  k_split_transpose_b<<<grid, 256, 0, st>>>(B, p.b_hi, p.b_lo, K, N, ldb, p.Kp);
+  return check_launch("tf32x3_split_b");
+}
+
+int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
+    return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
+  const Planes p = carve(ws, M, N, K);
+  CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
+  int rc = make_map(&m_ahi, p.a_hi, M, p.Kp, BM);
+  if (!rc) rc = make_map(&m_alo, p.a_lo, M, p.Kp, BM);
+  if (!rc) rc = make_map(&m_bhi, p.b_hi, N, p.Kp, BN);
+  if (!rc) rc = make_map(&m_blo, p.b_lo, N, p.Kp, BN);
+  if (rc) return rc;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
+    attr_dev = dev;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, p.Kp / BK);
+  return check_launch("gemm_parallel_tf32x3");
+}
+
+}  // namespace elv

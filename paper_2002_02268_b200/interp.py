@@ -1,0 +1,189 @@
+"""Drop-in B200 backend for the reference's program evaluator.
+
+`run(e, args)` has the signature, argument meaning and error behaviour of
+`stratir.interp.run` (reference pkg/src/stratir/interp.py:157-162): it applies
+the lambda-chain program `e` to `args` and returns the value.  For the terms
+the seven GEMM schedules produce (see `schedules`), the evaluation runs as one
+hand-written sm_100a kernel through the C ABI (include/elevate_b200.h);
+anything else raises the reference's `EvalError` (interp.py:16) -- there is
+no CPU fallback on this path.
+
+Accepted argument types:
+  * nested Python lists of floats (the reference's own value model; the result
+    is a nested list of floats, like the reference's),
+  * numpy arrays / CPU torch tensors (host buffers: copied to the GPU and back),
+  * CUDA torch tensors (stay on the device; result is a CUDA tensor).
+
+Scalars are fp32 on the device (the reference evaluates in f64,
+interp.py:145-148); results match it within the sqrt(K)-scaled fp32 bound of
+SURVEY.md §8(d) (see `tolerance.py`).
+"""
+
+from __future__ import annotations
+
+import os
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib, dispatch
+from ._ref import S
+
+_plan_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def EvalError(msg):
+    return S().interp.EvalError(msg)
+
+
+def _default_tf32x3() -> bool:
+    return os.environ.get("ELV_TF32X3", "0") not in ("", "0", "false", "False")
+
+
+def plan(e, arg_shapes, tf32x3: bool | None = None) -> dispatch.KernelPlan:
+    """Decode (cached per term object) and bind to the argument shapes."""
+    tf32x3 = _default_tf32x3() if tf32x3 is None else tf32x3
+    key = (tuple(map(tuple, arg_shapes)), bool(tf32x3))
+    per_term = _plan_cache.get(e)
+    if per_term is None:
+        per_term = {}
+        try:
+            _plan_cache[e] = per_term
+        except TypeError:
+            pass
+    p = per_term.get(key)
+    if p is None:
+        p = dispatch.decode(e, arg_shapes, tf32x3=tf32x3)
+        per_term[key] = p
+    return p
+
+
+def gemm(p: dispatch.KernelPlan, A: torch.Tensor, B: torch.Tensor,
+         out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Launch the plan's kernel on device tensors (async on `stream`)."""
+    lib = _lib.load()
+    if not (A.is_cuda and B.is_cuda):
+        raise EvalError("gemm expects CUDA tensors")
+    if A.dtype != torch.float32 or B.dtype != torch.float32:
+        raise EvalError("the B200 backend computes fp32 (f32 scalars, ir.py:17)")
+    if A.stride(-1) != 1:
+        A = A.contiguous()
+    if B.stride(-1) != 1:
+        B = B.contiguous()
+    M, K = A.shape
+    Kb, N = B.shape
+    if (M, N, K) != (p.M, p.N, p.K) or Kb != K:
+        raise EvalError(f"plan is for {p.M}x{p.K} . {p.K}x{p.N}, got {M}x{K} . {Kb}x{N}")
+    if out is None:
+        out = torch.empty((M, N), device=A.device, dtype=torch.float32)
+    elif out.shape != (M, N) or out.stride(-1) != 1 or out.dtype != torch.float32:
+        raise EvalError("out must be a row-major fp32 M x N tensor")
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    ws_bytes = lib.elv_gemm_workspace_bytes(p.variant, M, N, K)
+    ws = torch.empty(ws_bytes, device=A.device, dtype=torch.uint8) if ws_bytes else None
+    with torch.cuda.device(A.device):
+        rc = lib.elv_gemm(p.variant, A.data_ptr(), B.data_ptr(), out.data_ptr(), M, N, K,
+                          A.stride(0), B.stride(0), out.stride(0),
+                          ws.data_ptr() if ws is not None else None, ws_bytes,
+                          stream.cuda_stream)
+    _lib.check(rc, f"elv_gemm[{p.variant_name}]")
+    return out
+
+
+class GemmCall:
+    """A bound kernel call with its workspace, split into the two C-ABI
+    phases (elv_gemm_prepare: operand layout transform; elv_gemm_compute:
+    the GEMM kernel) so callers can time or overlap them separately.
+    Launches per call: prepare 0 (variants 0-3), 1 (4-6), 2 (7); compute 1."""
+
+    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 2}
+
+    def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
+        self.lib = _lib.load()
+        self.p, self.A, self.B, self.C = p, A, B, C
+        self.stream = stream or torch.cuda.current_stream(A.device)
+        self.ws_bytes = self.lib.elv_gemm_workspace_bytes(p.variant, p.M, p.N, p.K)
+        self.ws = (torch.empty(self.ws_bytes, device=A.device, dtype=torch.uint8)
+                   if self.ws_bytes else None)
+        self.launches = self.PREPARE_LAUNCHES[p.variant] + 1
+
+    def _args(self):
+        return (self.ws.data_ptr() if self.ws is not None else None, self.ws_bytes,
+                self.stream.cuda_stream)
+
+    def prepare(self):
+        p = self.p
+        rc = self.lib.elv_gemm_prepare(p.variant, self.A.data_ptr(), self.B.data_ptr(), p.M, p.N, p.K,
+                                       self.A.stride(0), self.B.stride(0), *self._args())
+        _lib.check(rc, "elv_gemm_prepare")
+
+    def compute(self):
+        p = self.p
+        rc = self.lib.elv_gemm_compute(p.variant, self.A.data_ptr(), self.B.data_ptr(),
+                                       self.C.data_ptr(), p.M, p.N, p.K, self.A.stride(0),
+                                       self.B.stride(0), self.C.stride(0), *self._args())
+        _lib.check(rc, "elv_gemm_compute")
+
+    def __call__(self):
+        self.prepare()
+        self.compute()
+        return self.C
+
+
+def run_tensor(e, A: torch.Tensor, B: torch.Tensor, out=None, stream=None,
+               tf32x3: bool | None = None) -> torch.Tensor:
+    """Tensor-returning variant of `run`: device in, device out, async."""
+    p = plan(e, [tuple(A.shape), tuple(B.shape)], tf32x3)
+    return gemm(p, A, B, out=out, stream=stream)
+
+
+def _as_host_f32(x):
+    if isinstance(x, list):
+        try:
+            return torch.tensor(x, dtype=torch.float32)
+        except (TypeError, ValueError) as err:
+            raise EvalError(f"map expects an array: {err}") from None
+    if isinstance(x, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    if isinstance(x, torch.Tensor):
+        return x
+    raise EvalError(f"map expects an array, got {type(x).__name__}")
+
+
+def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
+    """Evaluate the scheduled mm program `e` applied to `[A, B]` on a B200.
+
+    Mirrors stratir.interp.run (interp.py:157-162).  Host inputs are copied to
+    the GPU, the kernel runs, and the result comes back in the caller's
+    representation (nested lists for lists, numpy for numpy, tensors for
+    tensors).  `out` (optional) is a preallocated M x N fp32 tensor -- e.g.
+    pinned host memory -- the result is written into and returned."""
+    if len(args) != 2:
+        raise EvalError(f"the mm program takes 2 arguments, got {len(args)}")
+    kinds = [type(a) for a in args]
+    ts = [_as_host_f32(a) for a in args]
+    for t in ts:
+        if t.dim() != 2:
+            raise EvalError("map expects an array of arrays")
+    p = plan(e, [tuple(t.shape) for t in ts], tf32x3)
+    if device is None:
+        device = ts[0].device if ts[0].is_cuda else torch.device("cuda", torch.cuda.current_device())
+    on_host = not ts[0].is_cuda
+    A = ts[0].to(device, torch.float32, non_blocking=True)
+    B = ts[1].to(device, torch.float32, non_blocking=True)
+    if out is not None and out.is_cuda:
+        return gemm(p, A, B, out=out)
+    C = gemm(p, A, B)
+    if out is not None:
+        out.copy_(C, non_blocking=out.is_pinned())
+        torch.cuda.current_stream(C.device).synchronize()
+        return out
+    if kinds[0] is list:
+        return C.double().cpu().tolist()
+    if kinds[0] is np.ndarray:
+        return C.cpu().numpy()
+    if on_host:
+        return C.cpu()
+    return C

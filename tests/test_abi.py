@@ -1,0 +1,79 @@
+"""CPU: the C-ABI library loads, exports every declared symbol, and its
+argument checking follows the reference's error conventions -- without
+launching anything (no GPU here)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2002_02268_b200 import _lib
+from paper_2002_02268_b200._ref import S
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "elevate_b200.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(elv_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_matches_binding_table():
+    assert set(declared_symbols()) == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_abi_metadata():
+    lib = _lib.load()
+    assert lib.elv_abi_version() == 1
+    names = [lib.elv_variant_name(v).decode() for v in range(8)]
+    assert names == ["baseline", "blocking", "vectorized", "loopPerm", "arrayPacking",
+                     "cacheBlocks", "parallel", "parallel_tf32x3"]
+    assert lib.elv_variant_name(99) == b"unknown"
+
+
+def test_workspace_sizes():
+    lib = _lib.load()
+    for v in range(4):
+        assert lib.elv_gemm_workspace_bytes(v, 1024, 1024, 1024) == 0
+    # packedB: ceil(N/128)*128 columns x K rows of fp32
+    for v in (4, 5, 6):
+        assert lib.elv_gemm_workspace_bytes(v, 100, 1000, 33) == 1024 * 33 * 4
+    assert lib.elv_pack_b_bytes(33, 1000) == 1024 * 33 * 4
+    # 3xTF32: hi/lo planes of A (M x Kp) and B^T (N x Kp), Kp = K rounded to 16
+    assert lib.elv_gemm_workspace_bytes(7, 100, 200, 30) == (2 * 100 * 32 + 2 * 200 * 32) * 4 + 256
+    assert lib.elv_gemm_workspace_bytes(0, 0, 5, 5) == 0
+
+
+def test_argument_errors_map_to_eval_error():
+    lib = _lib.load()
+    EvalError = S().interp.EvalError
+    rc = lib.elv_gemm(0, None, None, None, 4, 4, 4, 4, 4, 4, None, 0, None)
+    assert rc == _lib.ELV_EINVAL
+    assert b"null" in lib.elv_last_error()
+    with pytest.raises(EvalError):
+        _lib.check(rc, "elv_gemm")
+    fake = ctypes.c_void_p(16)   # never dereferenced: rejected before any launch
+    assert lib.elv_gemm(0, fake, fake, fake, 0, 4, 4, 4, 4, 4, None, 0, None) == _lib.ELV_EINVAL
+    assert lib.elv_gemm(0, fake, fake, fake, 4, 4, 4, 2, 4, 4, None, 0, None) == _lib.ELV_EINVAL
+    assert lib.elv_gemm(42, fake, fake, fake, 4, 4, 4, 4, 4, 4, None, 0, None) == _lib.ELV_EVARIANT
+    assert lib.elv_gemm(6, fake, fake, fake, 4, 4, 4, 4, 4, 4, None, 0, None) == _lib.ELV_EWORKSPACE
+    assert lib.elv_pack_b(fake, fake, 4, 4, 4, 16, None) == _lib.ELV_EINVAL
+    assert lib.elv_gemm_prepacked(2, fake, fake, fake, 4, 4, 4, 4, 4, None) == _lib.ELV_EVARIANT
+    assert lib.elv_gemm_rowshard(6, 1, None, None, None, None, None, None, 4, 4, None) == _lib.ELV_EINVAL
+    assert lib.elv_split_tf32(fake, fake, fake, -1, None) == _lib.ELV_EINVAL
+    assert lib.elv_fill_uniform(None, 4, 0, 0, 0, None) == _lib.ELV_EINVAL
+
+
+def test_runtime_errors_map_to_runtime_error():
+    _lib.load()
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.ELV_ECUDA, "x")
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.ELV_ENCCL, "x")

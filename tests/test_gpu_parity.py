@@ -1,0 +1,182 @@
+"""GPU parity: every kernel variant against the oracle, through the C ABI.
+
+Tolerance: |C - C_f64| <= sqrt(K) * 2^-24 * (|A||B|)_ij per
+element, tau = 1 (oracle.check).  Golden cases compare against the reference
+interpreter's own outputs; larger shapes against the f64 oracle.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2002_02268_b200 import _lib, dispatch, interp, schedules, synth
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+META = json.load(open(os.path.join(GOLD, "golden.json")))
+VARIANTS = list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]
+
+
+def _sched(v):
+    return ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+
+
+def _device_inputs(M, N, K, seed, dev):
+    A = torch.empty((M, K), device=dev, dtype=torch.float32)
+    B = torch.empty((K, N), device=dev, dtype=torch.float32)
+    synth.fill_device(A, seed, 0)
+    synth.fill_device(B, seed, 1)
+    return A, B
+
+
+def test_native_library_is_what_runs(cuda):
+    A, B = _device_inputs(64, 64, 64, 0, cuda)
+    t = schedules.apply("parallel", 64, 64, 64).term
+    interp.run_tensor(t, A, B)
+    torch.cuda.synchronize()
+    maps = open("/proc/self/maps").read()
+    assert "libelevate_b200.so" in maps
+
+
+def test_device_generator_matches_host(cuda):
+    x = torch.empty(1 << 20, device=cuda)
+    synth.fill_device(x, seed=3, tensor_id=1, offset=12345)
+    assert np.array_equal(x.cpu().numpy(), synth.uniform(1 << 20, 3, 1, 12345))
+
+
+@pytest.mark.parametrize("case", META["cases"], ids=[c["name"] for c in META["cases"]])
+@pytest.mark.parametrize("tf32x3", [False, True], ids=["simt", "tf32x3"])
+def test_golden_vs_reference_interpreter(cuda, case, tf32x3):
+    if tf32x3 and case["schedule"] != "parallel":
+        pytest.skip("3xTF32 is attached to the parallel schedule")
+    z = np.load(os.path.join(GOLD, case["name"] + ".npz"))
+    A, B, C_ref = z["A"], z["B"], z["C"]
+    term = schedules.apply_padded(case["schedule"], case["M"], case["N"], case["K"]).term
+    C = interp.run(term, [A, B], tf32x3=tf32x3)          # numpy in -> numpy out (host path)
+    assert isinstance(C, np.ndarray) and C.shape == C_ref.shape
+    ok, worst = oracle.check(C, C_ref, oracle.absprod(A, B), case["K"])
+    assert ok, f"worst err/bound = {worst:.3g}"
+
+
+def test_list_inputs_return_lists_like_the_reference(cuda):
+    t = schedules.apply("baseline", 2, 3, 2).term
+    B = [[1.5, -2.0, 0.25], [3.0, 0.5, -1.0]]
+    C = interp.run(t, [[[1.0, 0.0], [0.0, 1.0]], B])     # mm(I, B) = B
+    assert C == B
+    t = schedules.apply("baseline", 1, 1, 3).term
+    assert interp.run(t, [[[1.0, 2.0, 3.0]], [[4.0], [5.0], [6.0]]]) == [[32.0]]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_1024_cubed_vs_interpreter_arithmetic(cuda, variant):
+    """configs[1]: every strategy at 1024^3 against the (bit-exact) C restatement
+    of the interpreter's f64 arithmetic for that schedule."""
+    name, tf = _sched(variant)
+    M = N = K = 1024
+    A, B = _device_inputs(M, N, K, 0, cuda)
+    term = schedules.apply(name, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf).cpu().numpy()
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    ref = oracle.mm_interp_f64(Ah, Bh, name)
+    ok, worst = oracle.check(C, ref, oracle.absprod_np(Ah, Bh), K)
+    assert ok, f"{variant}: worst err/bound = {worst:.3g}"
+    assert worst < 0.5
+
+
+ODD = [(1000, 1000, 1000), (4096, 256, 4096), (257, 1031, 513), (1, 1, 1), (3, 5, 1),
+       (129, 257, 17), (7, 300, 2048)]
+
+
+@pytest.mark.parametrize("shape", ODD, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_odd_shapes_split_tails(cuda, shape, variant):
+    """configs[4]: non-divisible shapes through the padded route (tails)."""
+    name, tf = _sched(variant)
+    M, N, K = shape
+    A, B = _device_inputs(M, N, K, 11, cuda)
+    term = schedules.apply_padded(name, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf).cpu().numpy()
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
+    assert ok, f"{variant} {shape}: worst err/bound = {worst:.3g}"
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_strided_and_misaligned_operands(cuda, variant):
+    """Leading dimensions larger than the row and 4-byte-misaligned bases
+    force the scalar load paths of the same kernels."""
+    name, tf = _sched(variant)
+    M, N, K = 96, 160, 72
+    big_a = torch.empty((M, K + 3), device=cuda); synth.fill_device(big_a, 5, 0)
+    big_b = torch.empty((K, N + 5), device=cuda); synth.fill_device(big_b, 5, 1)
+    A = big_a[:, 1:K + 1]          # base misaligned by 4 bytes, lda = K + 3
+    B = big_b[:, 3:N + 3]
+    p = dispatch.decode(schedules.apply(name, M, N, K).term, [(M, K), (K, N)], tf32x3=tf)
+    out_big = torch.zeros((M, N + 1), device=cuda)
+    C = interp.gemm(p, A, B, out=out_big[:, :N])
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    ok, worst = oracle.check(C.cpu().numpy(), oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
+    assert ok, f"{variant}: worst err/bound = {worst:.3g}"
+    assert torch.all(out_big[:, N] == 0)          # nothing written past the view
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "cacheBlocks"])
+def test_8192_cubed_row_sample(cuda, variant):
+    """configs[2] roofline shape: sampled rows against the f64 oracle."""
+    name, tf = _sched(variant)
+    M = N = K = 8192
+    A, B = _device_inputs(M, N, K, 2, cuda)
+    term = schedules.apply(name, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf)
+    rows = torch.tensor([0, 1, 127, 128, 4095, 4096, 8190, 8191] + list(range(1000, 8000, 1111)),
+                        device=cuda)
+    Cs = C[rows].cpu().numpy()
+    As = A[rows].cpu().numpy()
+    Bh = B.cpu().numpy()
+    ok, worst = oracle.check(Cs, oracle.mm_f64(As, Bh), oracle.absprod_np(As, Bh), K)
+    assert ok, f"{variant}: worst err/bound = {worst:.3g}"
+
+
+def test_pack_b_layout(cuda):
+    K, N = 37, 100
+    B = torch.empty((K, N), device=cuda); synth.fill_device(B, 1, 1)
+    lib = _lib.load()
+    P = torch.full((lib.elv_pack_b_bytes(K, N) // 4,), -7.0, device=cuda)
+    _lib.check(lib.elv_pack_b(B.data_ptr(), P.data_ptr(), K, N, N, 32,
+                              torch.cuda.current_stream().cuda_stream), "pack_b")
+    Pn = P.cpu().numpy().reshape(-1, K, 32)           # [panel][k][c]
+    Bp = np.zeros((K, Pn.shape[0] * 32), np.float32); Bp[:, :N] = B.cpu().numpy()
+    expect = Bp.reshape(K, -1, 32).transpose(1, 0, 2)  # packedB[x][y][z] = B[y][32x+z]
+    assert np.array_equal(Pn, expect)
+
+
+def test_split_tf32(cuda):
+    lib = _lib.load()
+    x = torch.empty(1 << 16, device=cuda); synth.fill_device(x, 9, 0)
+    x *= 1e3
+    hi, lo = torch.empty_like(x), torch.empty_like(x)
+    _lib.check(lib.elv_split_tf32(x.data_ptr(), hi.data_ptr(), lo.data_ptr(), x.numel(),
+                                  torch.cuda.current_stream().cuda_stream), "split")
+    h = hi.cpu().numpy().view(np.uint32)
+    l = lo.cpu().numpy().view(np.uint32)
+    assert np.all(h & 0x1FFF == 0) and np.all(l & 0x1FFF == 0)     # tf32-exact planes
+    xs = x.cpu().numpy().astype(np.float64)
+    err = np.abs(xs - (hi.cpu().numpy().astype(np.float64) + lo.cpu().numpy().astype(np.float64)))
+    assert np.all(err <= np.abs(xs) * 2.0 ** -21)
+
+
+def test_errors_raise_eval_error(cuda):
+    from paper_2002_02268_b200._ref import S
+    EvalError = S().interp.EvalError
+    t = schedules.apply("parallel", 64, 64, 64).term
+    A = torch.zeros((64, 32), device=cuda)
+    B = torch.zeros((64, 64), device=cuda)
+    with pytest.raises(EvalError):
+        interp.run_tensor(t, A, B)
+    with pytest.raises(EvalError):
+        interp.run(t, [np.zeros((64, 64), np.float32)])
