@@ -84,15 +84,27 @@ def absprod_np(A, B) -> np.ndarray:
     return np.abs(np.asarray(A, np.float64)) @ np.abs(np.asarray(B, np.float64))
 
 
-def bound(K: int, absAB: np.ndarray, tau: float = 1.0) -> np.ndarray:
+def default_tau(K: int) -> float:
+    """tau = 1 for K >= 32; tau = 2 below.
+
+    The sqrt(K) law is probabilistic: at K <= 8 even correctly rounded
+    sequential fp32 FFMA reaches 1.23x the tau=1 bound on 65k outputs
+    (measured on B200, scripts/tf32x3_numerics.py), because K-1 roundings of
+    partial sums are not yet averaged.  From K = 32 on every kernel stays
+    below 0.5 (SIMT) / 0.4 (3xTF32)."""
+    return 1.0 if K >= 32 else 2.0
+
+
+def bound(K: int, absAB: np.ndarray, tau: float | None = None) -> np.ndarray:
     """Per-element parity bound tau * sqrt(K) * 2^-24 * (|A||B|)_ij.
 
-    Calibrated in SURVEY.md §8(d): sequential fp32 and 3xTF32 reach ~0.1 of
-    it at K=1024; a single TF32 product violates it by ~59x."""
+    Calibrated in SURVEY.md §8(d): sequential fp32 reaches ~0.1 of it at
+    K=1024; a single TF32 product violates it by ~29x at K=1024 (measured)."""
+    tau = default_tau(K) if tau is None else tau
     return tau * np.sqrt(K) * 2.0 ** -24 * absAB
 
 
-def check(C, ref_f64, absAB, K: int, tau: float = 1.0):
+def check(C, ref_f64, absAB, K: int, tau: float | None = None):
     """(ok, worst ratio err/bound) for a device result against the f64 oracle."""
     C = np.asarray(C, np.float64)
     err = np.abs(C - ref_f64)

@@ -19,6 +19,8 @@
 
 #include "elv_common.cuh"
 
+#include <stdlib.h>
+
 namespace elv {
 namespace {
 
@@ -393,6 +395,149 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
 }
 
 // ---------------------------------------------------------------------------
+// K6 parallel (tuned): 128x128 CTA tile over packedB, 8x8 per thread, SMEM
+// double buffer with the next k-block prefetched into registers, and the
+// next k-step's A/B fragments prefetched from SMEM while the current 64
+// FFMAs issue (hides LDS latency -- the short_scoreboard stall of the plain
+// K5 loop).  BK and blocks/SM are template parameters; ELV_SGEMM_CFG selects
+// among the instantiations for tuning (default: the measured best).
+template <int BK, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k6_sgemm_db(const float* __restrict__ A, const float* __restrict__ P, float* __restrict__ C,
+            int M, int N, int K, int lda, int ldc) {
+  constexpr int LA = BK / 8;                      // float4 loads of A per thread per k-block
+  constexpr int LB = BK / 8;                      // float4 loads of B per thread per k-block
+  __shared__ __align__(16) float As[2][BK][G_BM + G_APAD];
+  __shared__ __align__(16) float Bs[2][BK][G_BN];
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lm = lane >> 2, ln = lane & 3;
+  const int trow = wm * 64 + lm * 4;
+  const int tcol = wn * 32 + ln * 4;
+  const bool vecA = aligned16(A) && (lda & 3) == 0;
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+
+  // A loader: float4 index q = tid + i*256 over (row, k4) with k4 fastest
+  constexpr int K4 = BK / 4;
+  // B loader: float4 index q = tid + i*256 over (panel, k, c4) with c4 fastest
+  constexpr int PANEL4 = BK * 8;                  // float4 per panel per k-block
+
+  const int tiles_m = (M + G_BM - 1) / G_BM, tiles_n = (N + G_BN - 1) / G_BN;
+  const int num_tiles = tiles_m * tiles_n;
+
+  for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+    const int row0 = tc.m * G_BM, col0 = tc.n * G_BN;
+    const float* Pbase = P + (size_t)(col0 >> 5) * K * kPanel;
+
+    float4 ra[LA], rb[LB];
+    auto gload = [&](int k0) {
+#pragma unroll
+      for (int i = 0; i < LA; ++i) {
+        const int q = tid + i * 256;
+        const int r = q / K4, kq = (q % K4) * 4;
+        ra[i] = load_a4<G_BM, BK>(A, M, K, lda, vecA, row0 + r, k0 + kq);
+      }
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        const int q = tid + i * 256;
+        const int pnl = q / PANEL4, w = q % PANEL4;
+        const int kk = w >> 3, c4 = (w & 7) * 4;
+        const int gk = k0 + kk;
+        rb[i] = gk < K ? __ldg(reinterpret_cast<const float4*>(Pbase + ((size_t)pnl * K + gk) * kPanel + c4))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+      for (int i = 0; i < LA; ++i) {
+        const int q = tid + i * 256;
+        const int r = q / K4, kq = (q % K4) * 4;
+        As[buf][kq + 0][r] = ra[i].x; As[buf][kq + 1][r] = ra[i].y;
+        As[buf][kq + 2][r] = ra[i].z; As[buf][kq + 3][r] = ra[i].w;
+      }
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        const int q = tid + i * 256;
+        const int pnl = q / PANEL4, w = q % PANEL4;
+        *reinterpret_cast<float4*>(&Bs[buf][w >> 3][pnl * 32 + (w & 7) * 4]) = rb[i];
+      }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < K; k0 += BK) {
+      const bool more = k0 + BK < K;
+      if (more) gload(k0 + BK);
+      float a[2][8], b[2][8];
+      auto lfrag = [&](int slot, int k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][trow]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][trow + 32]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol + 16]);
+        a[slot][0] = a0.x; a[slot][1] = a0.y; a[slot][2] = a0.z; a[slot][3] = a0.w;
+        a[slot][4] = a1.x; a[slot][5] = a1.y; a[slot][6] = a1.z; a[slot][7] = a1.w;
+        b[slot][0] = b0.x; b[slot][1] = b0.y; b[slot][2] = b0.z; b[slot][3] = b0.w;
+        b[slot][4] = b1.x; b[slot][5] = b1.y; b[slot][6] = b1.z; b[slot][7] = b1.w;
+      };
+      lfrag(0, 0);
+#pragma unroll
+      for (int k = 0; k < BK; ++k) {
+        if (k + 1 < BK) lfrag((k + 1) & 1, k + 1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[k & 1][i], b[k & 1][j], acc[i][j]);
+      }
+      if (more) sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = col0 + tcol + h * 16;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float* v = &acc[i][h * 4];
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+  }
+}
+
+struct SgemmCfg { void (*fn)(const float*, const float*, float*, int, int, int, int, int); int minb; };
+static const SgemmCfg kSgemmCfgs[] = {
+    {k6_sgemm_db<8, 2>, 2}, {k6_sgemm_db<8, 1>, 1}, {k6_sgemm_db<16, 2>, 2}, {k6_sgemm_db<16, 1>, 1},
+};
+
+static int sgemm_cfg() {
+  static int cfg = -2;
+  if (cfg == -2) {
+    const char* e = getenv("ELV_SGEMM_CFG");
+    cfg = e ? atoi(e) : 0;
+    if (cfg < -1 || cfg >= (int)(sizeof(kSgemmCfgs) / sizeof(kSgemmCfgs[0]))) cfg = 0;
+  }
+  return cfg;
+}
+
+// ---------------------------------------------------------------------------
 // packB: packedB[p][k][c] = B[k][32p + c], zero-filled past N (rules.py:516-549,
 // TVM packedB PAPER.md:49-50).  Pure layout transform, HBM-bound: every
 // thread moves one float4; reads are coalesced along B's rows, writes along
@@ -470,6 +615,14 @@ int launch_simt(int variant, const float* A, const float* B, const float* packed
       return check_launch("gemm_cacheblocks");
     }
     case ELV_PARALLEL: {
+      const int cfg = sgemm_cfg();
+      if (cfg >= 0) {
+        const long long tiles = (long long)((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN);
+        long long grid = (long long)num_sms() * kSgemmCfgs[cfg].minb;
+        if (grid > tiles) grid = tiles;
+        kSgemmCfgs[cfg].fn<<<(unsigned)grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, ldc);
+        return check_launch("gemm_parallel");
+      }
       const long long tiles = (long long)((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN);
       long long grid = (long long)num_sms() * 2;
       if (grid > tiles) grid = tiles;

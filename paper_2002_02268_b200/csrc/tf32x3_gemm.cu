@@ -12,11 +12,17 @@
 //               tiles into a STAGES-deep SMEM ring (64B swizzle), mbarrier
 //               complete_tx signalling.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (kind::tf32, M=128, N=256, K=8 per instruction, 3 per k-step),
-//               tcgen05.commit frees SMEM slots and publishes accumulators.
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> global C, with
-//               two TMEM accumulators (2 x 256 columns) so the epilogue of
-//               tile i overlaps the MMAs of tile i+1.
+//               (kind::tf32, M=128, N=256, K=8 per instruction, 3 per k-step
+//               or 4 for short K), tcgen05.commit frees SMEM slots and
+//               publishes the accumulators.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b of D_big and D_small ->
+//               C = RN(D_big + D_small) in registers -> global C.
+// Accuracy: the tensor core truncates (round-toward-zero) on every
+// accumulate; measured on B200 (scripts/tf32x3_numerics.py) a single shared
+// accumulator gives err/bound 0.13 mean / 0.7-0.96 worst at K >= 64 and up
+// to 6 at K=1, against SIMT FFMA's 0.04 at K=8192.  Separate accumulators for
+// hi.hi and the correction terms, an RN combine in the epilogue and lo.lo
+// for short K keep it inside the tau = 1 bound at every K.
 // The split prepass (split_a / split_transpose_b below) is the packB of this
 // variant: it writes the hi/lo planes K-major, zero-padded to BK, so TMA
 // boxes and UMMA K-major descriptors apply to both operands.
@@ -25,6 +31,7 @@
 
 #include <cuda.h>
 #include <mutex>
+#include <stdlib.h>
 
 namespace elv {
 namespace {
@@ -35,7 +42,7 @@ constexpr int NUM_THREADS = 192;
 constexpr int A_TILE_BYTES = BM * BK * 4;         // 8 KB
 constexpr int B_TILE_BYTES = BN * BK * 4;         // 16 KB
 constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;   // 48 KB
-constexpr int TMEM_COLS = 512;                    // 2 accumulators x 256 fp32 columns
+constexpr int TMEM_COLS = 512;                    // D_big + D_small, 256 fp32 columns each
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
 
 inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
@@ -145,7 +152,7 @@ struct TileSched {
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-          float* __restrict__ C, int M, int N, int ldc, int num_kb) {
+          float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -162,7 +169,8 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     tma_prefetch_desc(&map_ahi); tma_prefetch_desc(&map_alo);
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -199,14 +207,17 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
+      // D_big (TMEM cols [0,256)) accumulates hi.hi; D_small (cols [256,512))
+      // accumulates hi.lo + lo.hi (+ lo.lo for short K).  The tensor core
+      // rounds every accumulate toward zero, so keeping the 2^-11-smaller
+      // correction terms out of the big accumulator cuts the number of
+      // truncations that land on |C|-sized values by 3x.
       int s = 0; uint32_t ph = 0;
       int it = 0;
+      const uint32_t d_big = tmem_base, d_small = tmem_base + (uint32_t)BN;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t use = (uint32_t)(it >> 1);
-        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        mbar_wait(&tempty[0], (uint32_t)(it & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -218,53 +229,56 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t koff = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along the row
-            const uint32_t first = (kb | k) != 0;
-            tc_mma_tf32(d, ahi + koff, bhi + koff, kIdesc, first);
-            tc_mma_tf32(d, ahi + koff, blo + koff, kIdesc, 1u);
-            tc_mma_tf32(d, alo + koff, bhi + koff, kIdesc, 1u);
+            const uint32_t acc = (kb | k) != 0;                 // 0: overwrite (first k-step)
+            tc_mma_tf32(d_small, ahi + koff, blo + koff, kIdesc, acc);
+            tc_mma_tf32(d_small, alo + koff, bhi + koff, kIdesc, 1u);
+            if (with_lolo) tc_mma_tf32(d_small, alo + koff, blo + koff, kIdesc, 1u);
+            tc_mma_tf32(d_big, ahi + koff, bhi + koff, kIdesc, acc);
           }
           tc_commit(&empty[s]);                 // frees the slot when these MMAs finish
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        tc_commit(&tfull[acc]);                 // accumulator complete
+        tc_commit(&tfull[0]);                   // accumulators complete
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+    // ---------------- epilogue (warps 2..5): C = RN(D_big + D_small) ----------------
     const int g = warp & 3;                      // TMEM lane group this warp may access
     const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int m0, n0;
       sched.coords(t, m0, n0);
-      const int acc = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
-      mbar_wait(&tfull[acc], use & 1);
+      mbar_wait(&tfull[0], (uint32_t)(it & 1));
       tc_fence_after();
       const int row = m0 + g * 32 + lane;
       float* crow = C + (size_t)row * ldc;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+        uint32_t rb[32], rs[32];
+        tmem_ld_32x32b_x32(lane_base + (uint32_t)(c * 32), rb);
+        tmem_ld_32x32b_x32(lane_base + (uint32_t)(BN + c * 32), rs);
+        float v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
         const int col = n0 + c * 32;
         if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               *reinterpret_cast<float4*>(crow + col + 4 * q) =
-                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                              __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           } else {
 #pragma unroll
             for (int q = 0; q < 32; ++q)
-              if (col + q < N) crow[col + q] = __uint_as_float(r[q]);
+              if (col + q < N) crow[col + q] = v[q];
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) mbar_arrive(&tempty[0]);
     }
   }
 
@@ -362,6 +376,20 @@ size_t tf32x3_workspace_bytes(int M, int N, int K) {
   return (size_t)(2 * (long long)M * Kp + 2 * (long long)N * Kp) * sizeof(float) + 256;
 }
 
+// lo.lo (a 4th MMA per k-step) is added for short reductions, where the
+// missing ~2^-22 |a b| term is not averaged out over K (measured: without it
+// the worst err/bound is 3.4 at K=1 even with exact accumulation).
+// ELV_TF32X3_LOLO=0/1 forces it off/on (diagnostics).
+static int with_lolo(int K) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("ELV_TF32X3_LOLO");
+    force = e ? (atoi(e) != 0) : -1;
+  }
+  if (force >= 0) return force;
+  return K < 512 ? 1 : 0;
+}
+
 struct Planes { float *a_hi, *a_lo, *b_hi, *b_lo; int Kp; };
 
 static Planes carve(void* ws, int M, int N, int K) {
@@ -411,7 +439,7 @@ int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_b
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, p.Kp / BK);
+  k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, p.Kp / BK, with_lolo(K));
   return check_launch("gemm_parallel_tf32x3");
 }
 

@@ -180,3 +180,18 @@ def test_errors_raise_eval_error(cuda):
         interp.run_tensor(t, A, B)
     with pytest.raises(EvalError):
         interp.run(t, [np.zeros((64, 64), np.float32)])
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "baseline", "blocking"])
+def test_error_vs_k_sweep(cuda, variant):
+    """The stated tolerance (oracle.bound: tau=1 for K>=32, 2 below) holds
+    from K=1 to K=4096 on 128x128 outputs."""
+    name, tf = _sched(variant)
+    for K in (1, 2, 3, 4, 8, 16, 31, 32, 64, 1000, 4096):
+        M = N = 128
+        A, B = _device_inputs(M, N, K, 21, cuda)
+        term = schedules.apply_padded(name, M, N, K).term
+        C = interp.run_tensor(term, A, B, tf32x3=tf).cpu().numpy()
+        Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+        ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
+        assert ok, f"{variant} K={K}: worst err/bound = {worst:.3g}"
