@@ -53,18 +53,46 @@ def load_peaks():
                 "sm_max_mhz": 1965.0}, "fallback"
 
 
-def roofline_peak(variant: str, peaks: dict, n_sms: int):
+def measure_cublas(dev, n=8192, reps=10):
+    """Library reference points for the denominators (not on our path):
+    cuBLAS TF32 (torch.matmul, allow_tf32) and cuBLAS SGEMM at n^3, best of
+    `reps` (burst), CUDA events."""
+    import torch
+    a = torch.randn(n, n, device=dev)
+    b = torch.randn(n, n, device=dev)
+    out = {}
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        for name, tf in (("cublas_tf32_tflops", True), ("cublas_sgemm_tflops", False)):
+            torch.backends.cuda.matmul.allow_tf32 = tf
+            for _ in range(2):
+                a @ b
+            best = float("inf")
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(); a @ b; e1.record(); torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            out[name] = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out
+
+
+def roofline_peak(variant: str, peaks: dict, n_sms: int, cublas: dict | None = None):
     """(peak TFLOP/s of useful fp32 flops, bound, note)."""
     if variant == "parallel_tf32x3":
-        # tf32 tensor rate = 1/2 the bf16 rate; 3 MMAs per useful MAC
-        tf32 = peaks["bf16_tflops_sustained"] / 2.0
+        if cublas and cublas.get("cublas_tf32_tflops"):
+            tf32, src = cublas["cublas_tf32_tflops"], "measured here: cuBLAS TF32 8192^3 (burst)"
+        else:
+            tf32, src = peaks["bf16_tflops"] / 2.0, "MEASURED_PEAKS bf16_tflops / 2"
         return tf32 / 3.0, "tensor", (
-            "tf32 tensor peak = MEASURED_PEAKS bf16_tflops_sustained/2; 3xTF32 issues 3 MMAs per "
-            "useful MAC, so the useful-fp32 ceiling is that /3")
+            f"tf32 tensor peak {tf32:.0f} TF ({src}); 3xTF32 issues 3 MMAs per useful MAC, so the "
+            "useful-fp32 ceiling is that / 3")
     fp32 = n_sms * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    extra = f"; cuBLAS SGEMM 8192^3 measured {cublas['cublas_sgemm_tflops']:.1f} TF" if cublas else ""
     return fp32, "fp32-simt", (
         f"fp32 FFMA peak = {n_sms} SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS); no "
-        "measured SIMT peak exists")
+        f"measured SIMT peak exists{extra}")
 
 
 class ClockSampler:
@@ -233,6 +261,7 @@ def main():
     ap.add_argument("--N", type=int, default=32768)
     ap.add_argument("--K", type=int, default=8192)
     ap.add_argument("--workload", default="rowshard", choices=["rowshard", "ladder"])
+    ap.add_argument("--chunks", type=int, default=4, help="packedB broadcast chunks (N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -269,31 +298,41 @@ def main():
 
     stream = torch.cuda.current_stream(dev)
     A = torch.empty((sh.rows, K), device=dev)
-    B = torch.empty((K, N), device=dev)
+    B = torch.empty((K, N), device=dev) if rank == 0 else None
     C = torch.empty((sh.rows, N), device=dev)
     synth.fill_device(A, 0, 0, offset=sh.row0 * K)
     if rank == 0:
         synth.fill_device(B, 0, 1)
+    if world == 1:
+        # one GPU: nothing to broadcast; prepass straight from row-major B
+        call = interp.GemmCall(plan, A, B, C, stream)
+        launches_per_step = call.launches
     else:
-        B.zero_()
-    call = interp.GemmCall(plan, A, B, C, stream)
-    rsg = D.RowShardGemm(plan, compute=lambda a, b, c: None)   # broadcast helper only
+        # N GPUs: packedB broadcast in column chunks overlapped with the GEMM
+        pipe = D.PipelinedRowShardGemm(plan, N, K, dev, chunks=args.chunks, stream=stream)
+        launches_per_step = pipe.launches
 
     ev = []
 
     def step(record=False):
-        rsg.broadcast_b(B)
         if record:
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            call.prepare()
-            e1.record(stream)
-            call.compute()
+            if world == 1:
+                call.prepare()
+                e1.record(stream)
+                call.compute()
+            else:
+                pipe.step(A, B, C)
+                e1.record(stream)
             e2.record(stream)
             ev.append((e0, e1, e2))
-        else:
+        elif world == 1:
             call.prepare()
             call.compute()
+        else:
+            pipe.step(A, B, C)
 
     def barrier():
         if world > 1:
@@ -312,8 +351,12 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = start.elapsed_time(end) / args.steps
-    prep_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
-    comp_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev)
+    if world == 1:
+        prep_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
+        comp_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev)
+    else:   # the pipelined step interleaves prepass, broadcast waits and GEMM chunks
+        prep_ms = 0.0
+        comp_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
     if world > 1:
         t = torch.tensor([ms, comp_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -341,8 +384,7 @@ def main():
                 if rank == 0:
                     B.copy_(B_h, non_blocking=True)
                 A.copy_(A_h, non_blocking=True)
-                rsg.broadcast_b(B)
-                interp.gemm(plan, A, B, out=C, stream=stream)
+                pipe.step(A, B, C)
                 C_h.copy_(C, non_blocking=True)
                 torch.cuda.current_stream(dev).synchronize()
 
@@ -363,7 +405,8 @@ def main():
         e2e = {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "api": "interp.run(term, [A_host_pinned, B_host_pinned], out=C_host_pinned)"
-               if world == 1 else "H2D A-shard (+B on rank 0), NCCL broadcast, interp.gemm, D2H C-shard"}
+               if world == 1 else ("H2D A-shard (+B on rank 0), PipelinedRowShardGemm.step "
+                                   "(chunked packedB NCCL broadcast + GEMM), D2H C-shard")}
 
     if rank != 0:
         if world > 1:
@@ -372,15 +415,19 @@ def main():
 
     peaks, peaks_src = load_peaks()
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak, bound, note = roofline_peak(args.variant, peaks, n_sms)
+    try:
+        cublas = measure_cublas(dev)
+    except RuntimeError:
+        cublas = None
+    peak, bound, note = roofline_peak(args.variant, peaks, n_sms, cublas)
     achieved = 2.0 * sh.rows * N * K / (comp_ms * 1e-3) / 1e12
-    kernel = {"parallel_tf32x3": "k7_tf32x3", "parallel": "k56_packed_8x8<true>"}.get(args.variant, args.variant)
+    kernel = {"parallel_tf32x3": "k7_tf32x3", "parallel": "k6_sgemm_db<8,2>"}.get(args.variant, args.variant)
     roof = {"bound": "tensor" if bound == "tensor" else "fp32-simt", "achieved": achieved,
             "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic_from_profiles(f"{kernel}@{sh.rows}x{N}x{K}"),
             "kernel": kernel, "kernel_ms": comp_ms, "prepass_ms": prep_ms,
             "kernel_share_of_step": comp_ms / ms, "peak_source": f"{peaks_src}: {note}",
-            "algorithmic_flops_per_launch": 2.0 * sh.rows * N * K}
+            "algorithmic_flops_per_launch": 2.0 * sh.rows * N * K, "library_reference": cublas}
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -388,7 +435,7 @@ def main():
         "config": workload_config(args, world),
         "roofline": roof,
         "clocks": clk.summary(),
-        "gpu_launches": args.steps * call.launches,
+        "gpu_launches": args.steps * launches_per_step,
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -404,6 +451,8 @@ def run_ladder(args, dev):
     from paper_2002_02268_b200 import dispatch, interp, schedules, synth
     peaks, src = load_peaks()
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cublas = measure_cublas(dev)
+    print(json.dumps({"workload": "library reference points (not our path)", **cublas}), flush=True)
     cases = [(v, 1024) for v in list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]]
     cases += [(v, 8192) for v in ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3")]
     stream = torch.cuda.current_stream(dev)
@@ -430,7 +479,7 @@ def run_ladder(args, dev):
             torch.cuda.synchronize()
             tot.append(e0.elapsed_time(e2)); comp.append(e1.elapsed_time(e2))
         ms = statistics.median(tot)
-        peak, bound, note = roofline_peak(v, peaks, n_sms)
+        peak, bound, note = roofline_peak(v, peaks, n_sms, cublas)
         ach = 2.0 * n ** 3 / (statistics.median(comp) * 1e-3) / 1e12
         print(json.dumps({"workload": f"{v} mm({n},{n},{n})", "variant": v, "M": n, "N": n, "K": n,
                           "gflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "ms": ms,

@@ -99,6 +99,20 @@ size_t elv_pack_b_bytes(int K, int N);
 int elv_split_tf32(const float* X, float* hi, float* lo, long long n,
                    void* stream);
 
+/* 3xTF32 building blocks (variant 7 split into its pieces, for pipelined and
+ * row-sharded callers).  Planes = [hi | lo], each rows x Kp fp32, K-major,
+ * Kp = K rounded up to 16, zero padded.  elv_gemm(7) == split_a ; split_b ;
+ * gemm_planes.  split_b_packed reads packedB panels (elv_pack_b layout), so
+ * a broadcast packedB chunk of Nc columns is split without unpacking. */
+size_t elv_tf32x3_a_planes_bytes(int M, int K);
+size_t elv_tf32x3_b_planes_bytes(int N, int K);
+int elv_tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, void* stream);
+int elv_tf32x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, void* stream);
+int elv_tf32x3_split_b_packed(const float* packedB, int K, int N, void* b_planes,
+                              void* stream);
+int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
+                           int M, int N, int K, int ldc, void* stream);
+
 /* Synthetic inputs: X[i] = U(-1,1) with 24-bit resolution from
  * splitmix64((seed << 48) ^ (tensor_id << 40) ^ (offset + i)); bit-identical
  * to paper_2002_02268_b200.synth.uniform() on the host. */

@@ -20,7 +20,9 @@ EXPORTS = (
     "elv_gemm", "elv_gemm_prepare", "elv_gemm_compute", "elv_gemm_workspace_bytes", "elv_gemm_prepacked", "elv_pack_b",
     "elv_pack_b_bytes", "elv_split_tf32", "elv_fill_uniform", "elv_nccl_init",
     "elv_nccl_destroy", "elv_gemm_rowshard", "elv_last_error", "elv_abi_version",
-    "elv_variant_name",
+    "elv_variant_name", "elv_tf32x3_a_planes_bytes", "elv_tf32x3_b_planes_bytes",
+    "elv_tf32x3_split_a", "elv_tf32x3_split_b", "elv_tf32x3_split_b_packed",
+    "elv_tf32x3_gemm_planes",
 )
 
 _lib = None
@@ -55,6 +57,12 @@ def load():
         "elv_gemm_rowshard": (c_int, [c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_vp),
                                       ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                       ctypes.POINTER(c_int), c_int, c_int, ctypes.POINTER(c_vp)]),
+        "elv_tf32x3_a_planes_bytes": (c_size, [c_int, c_int]),
+        "elv_tf32x3_b_planes_bytes": (c_size, [c_int, c_int]),
+        "elv_tf32x3_split_a": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
+        "elv_tf32x3_split_b": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
+        "elv_tf32x3_split_b_packed": (c_int, [c_vp, c_int, c_int, c_vp, c_vp]),
+        "elv_tf32x3_gemm_planes": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
         "elv_last_error": (ctypes.c_char_p, []),
         "elv_abi_version": (c_int, []),
         "elv_variant_name": (ctypes.c_char_p, [c_int]),

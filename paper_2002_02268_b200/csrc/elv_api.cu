@@ -259,6 +259,38 @@ int elv_gemm(int variant, const float* A, const float* B, float* C, int M, int N
   return elv_gemm_compute(variant, A, B, C, M, N, K, lda, ldb, ldc, workspace, workspace_bytes, stream);
 }
 
+size_t elv_tf32x3_a_planes_bytes(int M, int K) {
+  return (M < 1 || K < 1) ? 0 : tf32x3_a_planes_bytes(M, K);
+}
+size_t elv_tf32x3_b_planes_bytes(int N, int K) {
+  return (N < 1 || K < 1) ? 0 : tf32x3_b_planes_bytes(N, K);
+}
+
+int elv_tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, void* stream) {
+  if (bad_ptr(A) || bad_ptr(a_planes) || M < 1 || K < 1 || lda < K)
+    return set_error(ELV_EINVAL, "tf32x3_split_a: bad arguments");
+  return tf32x3_split_a(A, M, K, lda, a_planes, (cudaStream_t)stream);
+}
+
+int elv_tf32x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, void* stream) {
+  if (bad_ptr(B) || bad_ptr(b_planes) || N < 1 || K < 1 || ldb < N)
+    return set_error(ELV_EINVAL, "tf32x3_split_b: bad arguments");
+  return tf32x3_split_b(B, K, N, ldb, false, b_planes, (cudaStream_t)stream);
+}
+
+int elv_tf32x3_split_b_packed(const float* packedB, int K, int N, void* b_planes, void* stream) {
+  if (bad_ptr(packedB) || bad_ptr(b_planes) || N < 1 || K < 1)
+    return set_error(ELV_EINVAL, "tf32x3_split_b_packed: bad arguments");
+  return tf32x3_split_b(packedB, K, N, 0, true, b_planes, (cudaStream_t)stream);
+}
+
+int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K,
+                           int ldc, void* stream) {
+  if (bad_ptr(a_planes) || bad_ptr(b_planes) || bad_ptr(C) || M < 1 || N < 1 || K < 1 || ldc < N)
+    return set_error(ELV_EINVAL, "tf32x3_gemm_planes: bad arguments");
+  return tf32x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
+}
+
 int elv_nccl_init(int ndev, const int* devs) {
   std::lock_guard<std::mutex> lk(g_nccl_mu);
   if (ndev < 1 || devs == nullptr) return set_error(ELV_EINVAL, "nccl_init: bad device list");

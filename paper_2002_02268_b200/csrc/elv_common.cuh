@@ -40,6 +40,12 @@ size_t tf32x3_workspace_bytes(int M, int N, int K);
 int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb,
                    void* ws, size_t ws_bytes, cudaStream_t st);
 int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t tf32x3_a_planes_bytes(int M, int K);
+size_t tf32x3_b_planes_bytes(int N, int K);
+int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st);
+int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st);
+int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
+                       cudaStream_t st);
 int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st);
 
 }  // namespace elv

@@ -312,7 +312,10 @@ k_split_a(const float* __restrict__ A, float* __restrict__ hi, float* __restrict
   }
 }
 
-// 32x32 tiles through SMEM: reads of B rows and writes of Bt rows coalesce
+// 32x32 tiles through SMEM: reads of B rows and writes of Bt rows coalesce.
+// PACKED: the source is packedB panels [N/32][K][32] (the packB layout the
+// row-shard driver broadcasts) instead of row-major B.
+template <bool PACKED>
 __global__ void __launch_bounds__(256)
 k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* __restrict__ lo,
                     int K, int N, int ldb, int Kp) {
@@ -322,7 +325,10 @@ k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* 
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = k0 + ty + 8 * r, n = n0 + tx;
-    t[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
+    float v = 0.f;
+    if (k < K && n < N)
+      v = PACKED ? __ldg(B + ((size_t)(n >> 5) * K + k) * 32 + (n & 31)) : __ldg(B + (size_t)k * ldb + n);
+    t[ty + 8 * r][tx] = v;
   }
   __syncthreads();
 #pragma unroll
@@ -371,9 +377,19 @@ int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows
 
 }  // namespace
 
+static inline long long kpad(int K) { return round_up(K, BK); }
+static inline size_t planes_bytes(int rows, int K) {
+  return (size_t)(2 * (long long)rows * kpad(K)) * sizeof(float) + 128;
+}
+static inline float* align128(const void* p) {
+  return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+
+size_t tf32x3_a_planes_bytes(int M, int K) { return planes_bytes(M, K); }
+size_t tf32x3_b_planes_bytes(int N, int K) { return planes_bytes(N, K); }
+
 size_t tf32x3_workspace_bytes(int M, int N, int K) {
-  const long long Kp = round_up(K, BK);
-  return (size_t)(2 * (long long)M * Kp + 2 * (long long)N * Kp) * sizeof(float) + 256;
+  return tf32x3_a_planes_bytes(M, K) + tf32x3_b_planes_bytes(N, K);
 }
 
 // lo.lo (a 4th MMA per k-step) is added for short reductions, where the
@@ -390,44 +406,39 @@ static int with_lolo(int K) {
   return K < 512 ? 1 : 0;
 }
 
-struct Planes { float *a_hi, *a_lo, *b_hi, *b_lo; int Kp; };
-
-static Planes carve(void* ws, int M, int N, int K) {
-  Planes p;
-  p.Kp = (int)round_up(K, BK);
-  float* base = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127));
-  p.a_hi = base;
-  p.a_lo = p.a_hi + (size_t)M * p.Kp;
-  p.b_hi = p.a_lo + (size_t)M * p.Kp;
-  p.b_lo = p.b_hi + (size_t)N * p.Kp;
-  return p;
-}
-
-int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
-                   size_t ws_bytes, cudaStream_t st) {
-  if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
-    return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
-  const Planes p = carve(ws, M, N, K);
-  long long blocks = ((long long)M * p.Kp + 255) / 256;
+int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st) {
+  const int Kp = (int)kpad(K);
+  float* hi = align128(a_planes);
+  float* lo = hi + (size_t)M * Kp;
+  long long blocks = ((long long)M * Kp + 255) / 256;
   const long long cap = (long long)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  k_split_a<<<(unsigned)blocks, 256, 0, st>>>(A, p.a_hi, p.a_lo, M, K, lda, p.Kp);
-  int rc = check_launch("tf32x3_split_a");
-  if (rc) return rc;
-  dim3 grid((N + 31) / 32, (p.Kp + 31) / 32);
-  k_split_transpose_b<<<grid, 256, 0, st>>>(B, p.b_hi, p.b_lo, K, N, ldb, p.Kp);
+  k_split_a<<<(unsigned)blocks, 256, 0, st>>>(A, hi, lo, M, K, lda, Kp);
+  return check_launch("tf32x3_split_a");
+}
+
+int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st) {
+  const int Kp = (int)kpad(K);
+  float* hi = align128(b_planes);
+  float* lo = hi + (size_t)N * Kp;
+  dim3 grid((N + 31) / 32, (Kp + 31) / 32);
+  if (packed) k_split_transpose_b<true><<<grid, 256, 0, st>>>(B, hi, lo, K, N, 0, Kp);
+  else k_split_transpose_b<false><<<grid, 256, 0, st>>>(B, hi, lo, K, N, ldb, Kp);
   return check_launch("tf32x3_split_b");
 }
 
-int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
-    return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
-  const Planes p = carve(ws, M, N, K);
+int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
+                       cudaStream_t st) {
+  const int Kp = (int)kpad(K);
+  const float* a_hi = align128(a_planes);
+  const float* a_lo = a_hi + (size_t)M * Kp;
+  const float* b_hi = align128(b_planes);
+  const float* b_lo = b_hi + (size_t)N * Kp;
   CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
-  int rc = make_map(&m_ahi, p.a_hi, M, p.Kp, BM);
-  if (!rc) rc = make_map(&m_alo, p.a_lo, M, p.Kp, BM);
-  if (!rc) rc = make_map(&m_bhi, p.b_hi, N, p.Kp, BN);
-  if (!rc) rc = make_map(&m_blo, p.b_lo, N, p.Kp, BN);
+  int rc = make_map(&m_ahi, a_hi, M, Kp, BM);
+  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM);
+  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, BN);
+  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, BN);
   if (rc) return rc;
   static int attr_dev = -1;
   int dev = 0;
@@ -439,8 +450,25 @@ int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_b
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, p.Kp / BK, with_lolo(K));
+  k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / BK,
+                                                   with_lolo(K));
   return check_launch("gemm_parallel_tf32x3");
+}
+
+// elv_gemm workspace for variant 7 = [A planes | B planes]
+int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
+    return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
+  int rc = tf32x3_split_a(A, M, K, lda, ws, st);
+  if (rc) return rc;
+  return tf32x3_split_b(B, K, N, ldb, false, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), st);
+}
+
+int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
+    return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
+  return tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
 }
 
 }  // namespace elv

@@ -80,6 +80,109 @@ class RowShardGemm:
         return self.compute(A_shard, B, C_shard)
 
 
+def column_chunks(N: int, chunks: int, align: int = 256):
+    """Split [0, N) into <= `chunks` column blocks, each a multiple of `align`
+    (the 3xTF32 tile width; also a multiple of the 128-column packB unit)."""
+    units = (N + align - 1) // align
+    chunks = max(1, min(chunks, units))
+    base, extra = divmod(units, chunks)
+    out, u = [], 0
+    for c in range(chunks):
+        nu = base + (1 if c < extra else 0)
+        n0, n1 = u * align, min((u + nu) * align, N)
+        if n1 > n0:
+            out.append((n0, n1))
+        u += nu
+    return out
+
+
+class PipelinedRowShardGemm:
+    """The production multi-GPU step: packedB broadcast in column chunks,
+    overlapped with the GEMM on the chunks that already arrived.
+
+    configs[3] ("row-sharded ... with NCCL broadcast of packedB over NVLink"):
+      rank src : packB(B[:, chunk c]) -> P_c   (compute stream)
+      all      : broadcast(P_c) on NCCL's stream (async, issued in order)
+      all      : wait(P_c) -> C[:, chunk c] = A_shard . B[:, chunk c]
+                 SIMT (variant 6): elv_gemm_prepacked on the packed chunk
+                 3xTF32 (variant 7): split_b_packed(P_c) + gemm_planes, with
+                 A's hi/lo planes made once per step while chunk 0 is in flight
+    Column blocks of C are independent, so the result is bit-identical to
+    the unchunked kernel's for the same per-tile arithmetic.
+    """
+
+    def __init__(self, plan, N: int, K: int, device, group=None, src: int = 0, chunks: int = 4,
+                 stream=None):
+        from . import _lib
+        self.lib = _lib.load()
+        self._check = _lib.check
+        self.plan, self.N, self.K, self.group, self.src = plan, N, K, group, src
+        self.variant = plan.variant
+        if self.variant not in (4, 5, 6, 7):
+            raise ValueError("the pipelined row shard runs the packed variants (4..7)")
+        self.device = device
+        self.stream = stream or torch.cuda.current_stream(device)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.chunks = column_chunks(N, chunks)
+        self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
+        M = plan.M
+        if self.variant == 7:
+            self.a_planes = torch.empty(self.lib.elv_tf32x3_a_planes_bytes(max(M, 1), K),
+                                        device=device, dtype=torch.uint8)
+            self.b_planes = [torch.empty(self.lib.elv_tf32x3_b_planes_bytes(n1 - n0, K),
+                                         device=device, dtype=torch.uint8) for n0, n1 in self.chunks]
+        # launches per step on this rank: pack (src only) + split_a + per chunk (split_b + gemm | gemm)
+        per_chunk = 2 if self.variant == 7 else 1
+        self.launches = (len(self.chunks) if self.rank == src else 0) + \
+            (1 if self.variant == 7 else 0) + per_chunk * len(self.chunks)
+
+    def _panel(self, n0: int) -> torch.Tensor:
+        return self.P[(n0 // 32) * self.K * 32:]
+
+    def step(self, A_shard: torch.Tensor, B: torch.Tensor | None, C_shard: torch.Tensor):
+        lib, K, N, st = self.lib, self.K, self.N, self.stream.cuda_stream
+        M = A_shard.shape[0]
+        works = []
+        with torch.cuda.stream(self.stream):
+            for n0, n1 in self.chunks:
+                Pc = self._panel(n0)
+                count = ((n1 - n0 + 127) // 128) * 128 * K     # packB writes whole 128-col groups
+                if self.rank == self.src:
+                    self._check(lib.elv_pack_b(B.data_ptr() + 4 * n0, Pc.data_ptr(), K, n1 - n0, B.stride(0),
+                                               32, st), "elv_pack_b")
+                if self.world > 1:
+                    works.append(dist.broadcast(Pc[:count], src=self.src, group=self.group, async_op=True))
+                else:
+                    works.append(None)
+            if M == 0:
+                for w in works:
+                    if w is not None:
+                        w.wait()
+                return C_shard
+            if self.variant == 7:
+                self._check(lib.elv_tf32x3_split_a(A_shard.data_ptr(), M, K, A_shard.stride(0),
+                                                   self.a_planes.data_ptr(), st), "split_a")
+            for (n0, n1), w, bp in zip(self.chunks, works,
+                                      self.b_planes if self.variant == 7 else [None] * len(works)):
+                if w is not None:
+                    w.wait()                        # compute stream waits for chunk c only
+                Pc = self._panel(n0)
+                Cc = C_shard.data_ptr() + 4 * n0
+                if self.variant == 7:
+                    self._check(lib.elv_tf32x3_split_b_packed(Pc.data_ptr(), K, n1 - n0, bp.data_ptr(), st),
+                                "split_b_packed")
+                    self._check(lib.elv_tf32x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(), Cc, M,
+                                                           n1 - n0, K, C_shard.stride(0), st), "gemm_planes")
+                else:
+                    self._check(lib.elv_gemm_prepacked(self.variant, A_shard.data_ptr(), Pc.data_ptr(), Cc, M,
+                                                       n1 - n0, K, A_shard.stride(0), C_shard.stride(0), st),
+                                "elv_gemm_prepacked")
+        return C_shard
+
+
+
+
 def gather_rows(C_shard: torch.Tensor, M: int, group=None, align: int = ROW_ALIGN) -> torch.Tensor:
     """Optional: assemble the full C on every rank (not on the timed path).
     Shards are padded to the largest shard for the equal-size all_gather."""
