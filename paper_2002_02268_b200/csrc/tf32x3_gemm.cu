@@ -291,6 +291,223 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 }
 
 // ----------------------------------------------------------------------------
+// K7 on a CTA pair (cta_group::2): the same 3xTF32 math on 256x256 tiles.
+// Each CTA of a 2-CTA cluster stages its own 128 rows of A and its own 128
+// columns of B (as Bt rows); the leader CTA issues tcgen05.mma.cta_group::2
+// (M=256, N=256), which reads A halves from both CTAs' SMEM and B halves
+// from both, and writes each CTA's 128 accumulator rows into its own TMEM.
+// Per SM this halves the B operand's SMEM reads and L2->SMEM fills relative
+// to the 1-CTA kernel (the 1-CTA kernel measured L1/SMEM throughput 88 %,
+// its limiter), for the same MMA work.
+constexpr int P_BM = 128;                          // rows per CTA (pair: 256)
+constexpr int P_BN = 256;                          // columns per pair tile (128 per CTA staged)
+constexpr int P_STAGES = 6;
+constexpr int P_A_TILE = P_BM * BK * 4;            // 8 KB
+constexpr int P_B_TILE = (P_BN / 2) * BK * 4;      // 8 KB (this CTA's half of Bt)
+constexpr int P_STAGE_BYTES = 2 * P_A_TILE + 2 * P_B_TILE;   // 32 KB
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 256 + 1024;
+constexpr uint32_t kIdescPair = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
+                                ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+               const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+               float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int tiles_m = (M + 2 * P_BM - 1) / (2 * P_BM), tiles_n = (N + P_BN - 1) / P_BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_ahi); tma_prefetch_desc(&map_alo);
+    tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
+    for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 8);                       // 4 epilogue warps x 2 CTAs (leader's copy)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  // tile t: rows [mt*256, +256) (this CTA: + rank*128), cols [nt*256, +256) (this CTA stages + rank*128)
+  auto coords = [&](int t, int& m0, int& n0) {
+    constexpr int GROUP = 8;
+    const int per_group = GROUP * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * GROUP;
+    const int gm = min(tiles_m - first_m, GROUP);
+    const int in = t - g * per_group;
+    m0 = (first_m + in % gm) * 2 * P_BM;
+    n0 = (in / gm) * P_BN;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      const uint32_t full0 = mapa_rank(smem_u32(&full[0]), 0);
+      int s = 0; uint32_t ph = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int m0, n0;
+        coords(t, m0, n0);
+        const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (P_BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * P_STAGE_BYTES;
+          if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
+          const uint32_t bar = full0 + (uint32_t)(s * 8);
+          const int k0 = kb * BK;
+          tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
+          tma_load_2d_pair(&map_alo, bar, st + P_A_TILE, k0, ma);
+          tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
+          tma_load_2d_pair(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb);
+          if (++s == P_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader CTA only) ----------------
+      int s = 0; uint32_t ph = 0;
+      int it = 0;
+      const uint32_t d_big = tmem_base, d_small = tmem_base + (uint32_t)P_BN;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+        mbar_wait(&tempty[0], (uint32_t)(it & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * P_STAGE_BYTES);
+          const uint64_t ahi = umma_desc_sw64(st);
+          const uint64_t alo = umma_desc_sw64(st + P_A_TILE);
+          const uint64_t bhi = umma_desc_sw64(st + 2 * P_A_TILE);
+          const uint64_t blo = umma_desc_sw64(st + 2 * P_A_TILE + P_B_TILE);
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t koff = (uint64_t)((k * 32) >> 4);
+            const uint32_t acc = (kb | k) != 0;
+            tc_mma_tf32_pair(d_small, ahi + koff, blo + koff, kIdescPair, acc);
+            tc_mma_tf32_pair(d_small, alo + koff, bhi + koff, kIdescPair, 1u);
+            if (with_lolo) tc_mma_tf32_pair(d_small, alo + koff, blo + koff, kIdescPair, 1u);
+            tc_mma_tf32_pair(d_big, ahi + koff, bhi + koff, kIdescPair, acc);
+          }
+          tc_commit_pair(&empty[s]);            // frees slot s in both CTAs
+          if (++s == P_STAGES) { s = 0; ph ^= 1; }
+        }
+        tc_commit_pair(&tfull[0]);              // accumulators ready in both CTAs
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5, both CTAs) ----------------
+    const int g = warp & 3;
+    const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
+    const uint32_t tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
+    int it = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+      int m0, n0;
+      coords(t, m0, n0);
+      mbar_wait(&tfull[0], (uint32_t)(it & 1));
+      tc_fence_after();
+      const int row = m0 + (int)rank * P_BM + g * 32 + lane;
+      float* crow = C + (size_t)row * ldc;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < P_BN / 32; ++c) {
+        uint32_t rb[32], rs[32];
+        tmem_ld_32x32b_x32(lane_base + (uint32_t)(c * 32), rb);
+        tmem_ld_32x32b_x32(lane_base + (uint32_t)(P_BN + c * 32), rs);
+        float v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
+        const int col = n0 + c * 32;
+        if (row < M && col < N) {
+          if (vecC && col + 31 < N) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(crow + col + 4 * q) =
+                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (col + q < N) crow[col + q] = v[q];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ----------------------------------------------------------------------------
 // split prepass: A -> A_hi, A_lo (M x Kp, K-major);  B -> Bt_hi, Bt_lo (N x Kp)
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -378,6 +595,16 @@ int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows
 }  // namespace
 
 static inline long long kpad(int K) { return round_up(K, BK); }
+
+// ELV_TF32X3_PAIR=1 selects the cta_group::2 kernel (default off until measured)
+static bool use_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ELV_TF32X3_PAIR");
+    v = e ? (atoi(e) != 0) : 0;
+  }
+  return v != 0;
+}
 static inline size_t planes_bytes(int rows, int K) {
   return (size_t)(2 * (long long)rows * kpad(K)) * sizeof(float) + 128;
 }
@@ -447,6 +674,25 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
     cudaError_t e = cudaFuncSetAttribute(k7_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
     attr_dev = dev;
+  }
+  if (use_pair()) {
+    CUtensorMap p_bhi, p_blo;
+    rc = make_map(&p_bhi, b_hi, N, Kp, P_BN / 2);
+    if (!rc) rc = make_map(&p_blo, b_lo, N, Kp, P_BN / 2);
+    if (rc) return rc;
+    static int pair_attr_dev = -1;
+    if (pair_attr_dev != dev) {
+      cudaError_t e = cudaFuncSetAttribute(k7_tf32x3_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           P_SMEM_BYTES);
+      if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 pair smem attribute: %s", cudaGetErrorString(e));
+      pair_attr_dev = dev;
+    }
+    const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
+    int clusters = num_sms() / 2;
+    if (clusters > tiles) clusters = tiles;
+    k7_tf32x3_pair<<<2 * clusters, NUM_THREADS, P_SMEM_BYTES, st>>>(m_ahi, m_alo, p_bhi, p_blo, C, M, N, ldc,
+                                                                     Kp / BK, with_lolo(K));
+    return check_launch("gemm_parallel_tf32x3_pair");
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();

@@ -152,6 +152,79 @@ def _as_host_f32(x):
     raise EvalError(f"map expects an array, got {type(x).__name__}")
 
 
+class HostPipeline:
+    """Host-resident A, B -> host C with the transfers overlapped.
+
+    B goes to the device first (every row block needs all of it) and is
+    prepared once (packB / tf32 split).  A and C move in row blocks: block i+1
+    is copied in on one stream while block i is multiplied on the compute
+    stream and block i-1 is copied out on a third stream (PCIe is full
+    duplex).  Row blocks of C are independent (the mapPar axis), and the
+    per-row arithmetic is the single-launch kernel's, so the result is
+    bit-identical to `gemm`."""
+
+    def __init__(self, p: dispatch.KernelPlan, device, chunk_rows: int | None = None):
+        self.lib = _lib.load()
+        self.p, self.device = p, device
+        M = p.M
+        if chunk_rows is None:
+            chunk_rows = max(128, -(-M // 8))
+        self.R = -(-chunk_rows // 128) * 128        # multiple of the kernels' row tile
+        self.blocks = [(r0, min(r0 + self.R, M)) for r0 in range(0, M, self.R)]
+
+    def __call__(self, A_h: torch.Tensor, B_h: torch.Tensor, out_h: torch.Tensor) -> torch.Tensor:
+        p, lib, dev = self.p, self.lib, self.device
+        M, N, K, v = p.M, p.N, p.K, p.variant
+        comp = torch.cuda.current_stream(dev)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        A_d = torch.empty((M, K), device=dev)
+        B_d = torch.empty((K, N), device=dev)
+        C_d = torch.empty((M, N), device=dev)
+        ev_b = torch.cuda.Event()
+        ev_a = [torch.cuda.Event() for _ in self.blocks]
+        ev_c = [torch.cuda.Event() for _ in self.blocks]
+        with torch.cuda.stream(s_in):
+            B_d.copy_(B_h, non_blocking=True)
+            ev_b.record(s_in)
+            for (r0, r1), ev in zip(self.blocks, ev_a):
+                A_d[r0:r1].copy_(A_h[r0:r1], non_blocking=True)
+                ev.record(s_in)
+        st = comp.cuda_stream
+        comp.wait_event(ev_b)
+        ws = None
+        if v in (4, 5, 6):
+            ws = torch.empty(lib.elv_pack_b_bytes(K, N), device=dev, dtype=torch.uint8)
+            _lib.check(lib.elv_pack_b(B_d.data_ptr(), ws.data_ptr(), K, N, N, 32, st), "elv_pack_b")
+        elif v == 7:
+            ws = torch.empty(lib.elv_tf32x3_b_planes_bytes(N, K), device=dev, dtype=torch.uint8)
+            a_pl = torch.empty(lib.elv_tf32x3_a_planes_bytes(self.R, K), device=dev, dtype=torch.uint8)
+            _lib.check(lib.elv_tf32x3_split_b(B_d.data_ptr(), K, N, N, ws.data_ptr(), st), "split_b")
+        for (r0, r1), ea, ec in zip(self.blocks, ev_a, ev_c):
+            comp.wait_event(ea)
+            rows = r1 - r0
+            a_ptr = A_d.data_ptr() + 4 * r0 * K
+            c_ptr = C_d.data_ptr() + 4 * r0 * N
+            if v in (4, 5, 6):
+                rc = lib.elv_gemm_prepacked(v, a_ptr, ws.data_ptr(), c_ptr, rows, N, K, K, N, st)
+            elif v == 7:
+                _lib.check(lib.elv_tf32x3_split_a(a_ptr, rows, K, K, a_pl.data_ptr(), st), "split_a")
+                rc = lib.elv_tf32x3_gemm_planes(a_pl.data_ptr(), ws.data_ptr(), c_ptr, rows, N, K, N, st)
+            else:
+                rc = lib.elv_gemm_compute(v, a_ptr, B_d.data_ptr(), c_ptr, rows, N, K, K, N, N, None, 0, st)
+            _lib.check(rc, f"row block {r0}:{r1}")
+            ec.record(comp)
+        with torch.cuda.stream(s_out):
+            for (r0, r1), ec in zip(self.blocks, ev_c):
+                s_out.wait_event(ec)
+                out_h[r0:r1].copy_(C_d[r0:r1], non_blocking=True)
+        s_out.synchronize()
+        comp.synchronize()
+        return out_h
+
+
+_PIPELINE_MIN_BYTES = 64 << 20
+
+
 def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     """Evaluate the scheduled mm program `e` applied to `[A, B]` on a B200.
 
@@ -159,7 +232,9 @@ def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     the GPU, the kernel runs, and the result comes back in the caller's
     representation (nested lists for lists, numpy for numpy, tensors for
     tensors).  `out` (optional) is a preallocated M x N fp32 tensor -- e.g.
-    pinned host memory -- the result is written into and returned."""
+    pinned host memory -- the result is written into and returned.  Large
+    host-resident problems go through `HostPipeline` (transfers overlapped
+    with the kernel)."""
     if len(args) != 2:
         raise EvalError(f"the mm program takes 2 arguments, got {len(args)}")
     kinds = [type(a) for a in args]
@@ -171,6 +246,20 @@ def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     if device is None:
         device = ts[0].device if ts[0].is_cuda else torch.device("cuda", torch.cuda.current_device())
     on_host = not ts[0].is_cuda
+    if (on_host and not ts[1].is_cuda and p.M >= 256
+            and 4 * (p.M * p.K + p.M * p.N) >= _PIPELINE_MIN_BYTES
+            and (out is None or not out.is_cuda)):
+        A_h = ts[0].contiguous().float()
+        B_h = ts[1].contiguous().float()
+        dst = out if out is not None else torch.empty((p.M, p.N), dtype=torch.float32,
+                                                      pin_memory=A_h.is_pinned())
+        with torch.cuda.device(device):
+            HostPipeline(p, device)(A_h, B_h, dst)
+        if kinds[0] is list:
+            return dst.double().tolist()
+        if kinds[0] is np.ndarray:
+            return dst.numpy()
+        return dst
     A = ts[0].to(device, torch.float32, non_blocking=True)
     B = ts[1].to(device, torch.float32, non_blocking=True)
     if out is not None and out.is_cuda:

@@ -94,3 +94,27 @@ def test_two_ranks_share_one_gpu_over_gloo(cuda, variant):
     B = torch.empty((K, N), device=cuda); synth.fill_device(B, 0, 1)
     ref = interp.gemm(p, A, B).cpu().numpy()
     assert np.array_equal(C, ref)
+
+
+@pytest.mark.parametrize("variant", ["baseline", "loopPerm", "parallel", "parallel_tf32x3"])
+def test_host_pipeline_bitwise_equals_device_path(cuda, variant):
+    """interp.run on host tensors large enough for HostPipeline (row blocks with
+    overlapped H2D / GEMM / D2H) returns exactly the single-launch result."""
+    sched, tf = ("parallel", True) if variant == "parallel_tf32x3" else (variant, False)
+    M, N, K = 1100, 4096, 2048          # 52 MiB of A+C... plus tails in M
+    if variant == "baseline":
+        M, N, K = 1100, 4096, 512
+    from paper_2002_02268_b200 import interp as I
+    old = I._PIPELINE_MIN_BYTES
+    I._PIPELINE_MIN_BYTES = 1 << 20
+    try:
+        term = schedules.apply_padded(sched, M, N, K).term
+        A = torch.from_numpy(synth.matrix(M, K, 8, 0)).pin_memory()
+        B = torch.from_numpy(synth.matrix(K, N, 8, 1)).pin_memory()
+        C_host = I.run(term, [A, B], tf32x3=tf)
+        assert not C_host.is_cuda
+        p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf)
+        C_dev = I.gemm(p, A.to(cuda), B.to(cuda)).cpu()
+        assert torch.equal(C_host, C_dev)
+    finally:
+        I._PIPELINE_MIN_BYTES = old
