@@ -88,7 +88,7 @@ int elv_gemm_prepacked(int variant, const float* A, const float* packedB,
                        float* C, int M, int N, int K, int lda, int ldc,
                        void* stream);
 
-/* packedB[p][k][c] = B[k][p*blk + c] (0 past N); p < ceil(N/128)*128/blk.
+/* packedB[p][k][c] = B[k][p*blk + c] (0 past N); p < ceil(N/256)*256/blk.
  * The toMem of the packB rule (reference rules.py:516-549; TVM packedB,
  * PAPER.md:49-50).  blk must be 32. */
 int elv_pack_b(const float* B, float* packedB, int K, int N, int ldb, int blk,

@@ -15,7 +15,7 @@ int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 
 constexpr int kPanel = 32;          // packB block (rules.py:516 default 32)
-constexpr int kPackAlign = 128;     // packed column count padded to 4 panels
+constexpr int kPackAlign = 256;     // packed column count padded to 8 panels (widest SIMT tile)
 
 inline size_t packed_cols(int N) { return (size_t)((N + kPackAlign - 1) / kPackAlign) * kPackAlign; }
 

@@ -522,17 +522,129 @@ k6_sgemm_db(const float* __restrict__ A, const float* __restrict__ P, float* __r
   }
 }
 
-struct SgemmCfg { void (*fn)(const float*, const float*, float*, int, int, int, int, int); int minb; };
+// 128x256 CTA tile, 8x16 per thread (128 accumulators, 1 CTA of 8 warps per
+// SM): 128 FFMA per 6 LDS.128 per k-step instead of 64 per 4.
+template <int BK>
+__global__ void __launch_bounds__(256, 1)
+k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* __restrict__ C,
+              int M, int N, int K, int lda, int ldc) {
+  constexpr int BM = 128, BN = 256;
+  constexpr int LA = BM * BK / 4 / 256;           // float4 of A per thread per k-block
+  constexpr int LB = BN * BK / 4 / 256;           // float4 of B per thread per k-block
+  constexpr int K4 = BK / 4;
+  constexpr int PANEL4 = BK * 8;
+  __shared__ __align__(16) float As[2][BK][BM + G_APAD];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;         // 2 x 4 warps, warp tile 64 x 64
+  const int lm = lane >> 2, ln = lane & 3;         // 8 x 4 lanes
+  const int trow = wm * 64 + lm * 4;               // rows +{0..3}, +32+{0..3}
+  const int tcol = wn * 64 + ln * 4;               // cols +{0..3} +16h
+  const bool vecA = aligned16(A) && (lda & 3) == 0;
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+
+  for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+    const int row0 = tc.m * BM, col0 = tc.n * BN;
+    const float* Pbase = P + (size_t)(col0 >> 5) * K * kPanel;
+    float4 ra[LA], rb[LB];
+    auto gload = [&](int k0) {
+#pragma unroll
+      for (int i = 0; i < LA; ++i) {
+        const int q = tid + i * 256;
+        ra[i] = load_a4<BM, BK>(A, M, K, lda, vecA, row0 + q / K4, k0 + (q % K4) * 4);
+      }
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        const int q = tid + i * 256;
+        const int pnl = q / PANEL4, w = q % PANEL4;
+        const int gk = k0 + (w >> 3);
+        rb[i] = gk < K ? __ldg(reinterpret_cast<const float4*>(Pbase + ((size_t)pnl * K + gk) * kPanel + (w & 7) * 4))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+      for (int i = 0; i < LA; ++i) {
+        const int q = tid + i * 256;
+        const int r = q / K4, kq = (q % K4) * 4;
+        As[buf][kq + 0][r] = ra[i].x; As[buf][kq + 1][r] = ra[i].y;
+        As[buf][kq + 2][r] = ra[i].z; As[buf][kq + 3][r] = ra[i].w;
+      }
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        const int q = tid + i * 256;
+        const int pnl = q / PANEL4, w = q % PANEL4;
+        *reinterpret_cast<float4*>(&Bs[buf][w >> 3][pnl * 32 + (w & 7) * 4]) = rb[i];
+      }
+    };
+    float acc[8][16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[i][j] = 0.f;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < K; k0 += BK) {
+      const bool more = k0 + BK < K;
+      if (more) gload(k0 + BK);
+#pragma unroll
+      for (int k = 0; k < BK; ++k) {
+        float a[8], b[16];
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][trow]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][trow + 32]);
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+        a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float4 bv = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol + 16 * h]);
+          b[4 * h] = bv.x; b[4 * h + 1] = bv.y; b[4 * h + 2] = bv.z; b[4 * h + 3] = bv.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      if (more) sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int gj = col0 + tcol + h * 16;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float* v = &acc[i][h * 4];
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+  }
+}
+
+struct SgemmCfg { void (*fn)(const float*, const float*, float*, int, int, int, int, int); int minb, bm, bn; };
 static const SgemmCfg kSgemmCfgs[] = {
-    {k6_sgemm_db<8, 2>, 2}, {k6_sgemm_db<8, 1>, 1}, {k6_sgemm_db<16, 2>, 2}, {k6_sgemm_db<16, 1>, 1},
+    {k6_sgemm_db<8, 2>, 2, 128, 128}, {k6_sgemm_db<8, 1>, 1, 128, 128}, {k6_sgemm_db<16, 2>, 2, 128, 128},
+    {k6_sgemm_db<16, 1>, 1, 128, 128}, {k6_sgemm_8x16<8>, 1, 128, 256},
 };
 
 static int sgemm_cfg() {
   static int cfg = -2;
   if (cfg == -2) {
     const char* e = getenv("ELV_SGEMM_CFG");
-    cfg = e ? atoi(e) : 0;
-    if (cfg < -1 || cfg >= (int)(sizeof(kSgemmCfgs) / sizeof(kSgemmCfgs[0]))) cfg = 0;
+    cfg = e ? atoi(e) : -2;   // -2: choose by problem size (below)
+    if (cfg < -3 || cfg >= (int)(sizeof(kSgemmCfgs) / sizeof(kSgemmCfgs[0]))) cfg = -2;
   }
   return cfg;
 }
@@ -615,9 +727,26 @@ int launch_simt(int variant, const float* A, const float* B, const float* packed
       return check_launch("gemm_cacheblocks");
     }
     case ELV_PARALLEL: {
-      const int cfg = sgemm_cfg();
+      // mapPar -> a grid covering all SMs.  Large problems: the 8x16-per-thread
+      // 128x256 persistent kernel (measured best, 51.9 TF at 32768x32768x8192);
+      // mid-size: 128x128 tiles at 2 CTAs/SM; small (fewer 128x128 tiles than
+      // SMs, e.g. 1024^3): 64x64 tiles so every SM gets work.
+      auto tiles_of = [&](int bm, int bn) {
+        return (long long)((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+      };
+      int cfg = sgemm_cfg();
+      if (cfg == -2) {
+        if (tiles_of(128, 256) >= 2LL * num_sms()) cfg = 4;
+        else if (tiles_of(128, 128) >= num_sms()) cfg = 0;
+        else cfg = -3;
+      }
+      if (cfg == -3) {
+        dim3 grid((N + 63) / 64, (M + 63) / 64);
+        k34_outer4x4<true><<<grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, 0, ldc);
+        return check_launch("gemm_parallel");
+      }
       if (cfg >= 0) {
-        const long long tiles = (long long)((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN);
+        const long long tiles = tiles_of(kSgemmCfgs[cfg].bm, kSgemmCfgs[cfg].bn);
         long long grid = (long long)num_sms() * kSgemmCfgs[cfg].minb;
         if (grid > tiles) grid = tiles;
         kSgemmCfgs[cfg].fn<<<(unsigned)grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, ldc);

@@ -131,14 +131,29 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   return d;
 }
 
+// K-major descriptor for 128B swizzle: 8-row atoms of 1024 B.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
+  return d;
+}
+template <int BKT>
+__device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr) {
+  return BKT == 32 ? umma_desc_sw128(saddr) : umma_desc_sw64(saddr);
+}
+
 // instruction descriptor: D=f32, A=B=tf32, both K-major, N=256, M=128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
 struct TileSched {
-  int tiles_m, tiles_n;
+  int tiles_m, tiles_n, group;
   __device__ void coords(int t, int& m0, int& n0) const {
-    constexpr int GROUP = 16;                       // row-tiles per L2 group
+    const int GROUP = group;                        // row-tiles per L2 group
     const int per_group = GROUP * tiles_n;
     const int g = t / per_group;
     const int first_m = g * GROUP;
@@ -152,7 +167,7 @@ struct TileSched {
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-          float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo) {
+          float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -162,7 +177,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN};
+  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN, group};
   const int num_tiles = sched.tiles_m * sched.tiles_n;
 
   if (warp == 0 && lane == 0) {
@@ -301,11 +316,13 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 // its limiter), for the same MMA work.
 constexpr int P_BM = 128;                          // rows per CTA (pair: 256)
 constexpr int P_BN = 256;                          // columns per pair tile (128 per CTA staged)
-constexpr int P_STAGES = 6;
-constexpr int P_A_TILE = P_BM * BK * 4;            // 8 KB
-constexpr int P_B_TILE = (P_BN / 2) * BK * 4;      // 8 KB (this CTA's half of Bt)
-constexpr int P_STAGE_BYTES = 2 * P_A_TILE + 2 * P_B_TILE;   // 32 KB
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 256 + 1024;
+template <int BKT> struct PairCfg {
+  static constexpr int STAGES = BKT == 32 ? 3 : 6;
+  static constexpr int A_TILE = P_BM * BKT * 4;            // 8 / 16 KB
+  static constexpr int B_TILE = (P_BN / 2) * BKT * 4;      // this CTA's half of Bt
+  static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+};
 constexpr uint32_t kIdescPair = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
                                 ((uint32_t)(256 >> 4) << 24);
 
@@ -351,10 +368,15 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+template <int BKT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-               float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo) {
+               float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group) {
+  constexpr int P_STAGES = PairCfg<BKT>::STAGES;
+  constexpr int P_A_TILE = PairCfg<BKT>::A_TILE;
+  constexpr int P_B_TILE = PairCfg<BKT>::B_TILE;
+  constexpr int P_STAGE_BYTES = PairCfg<BKT>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
@@ -391,7 +413,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
 
   // tile t: rows [mt*256, +256) (this CTA: + rank*128), cols [nt*256, +256) (this CTA stages + rank*128)
   auto coords = [&](int t, int& m0, int& n0) {
-    constexpr int GROUP = 8;
+    const int GROUP = group;
     const int per_group = GROUP * tiles_n;
     const int g = t / per_group;
     const int first_m = g * GROUP;
@@ -415,7 +437,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           uint8_t* st = smem + s * P_STAGE_BYTES;
           if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
           const uint32_t bar = full0 + (uint32_t)(s * 8);
-          const int k0 = kb * BK;
+          const int k0 = kb * BKT;
           tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
           tma_load_2d_pair(&map_alo, bar, st + P_A_TILE, k0, ma);
           tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
@@ -437,12 +459,12 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * P_STAGE_BYTES);
-          const uint64_t ahi = umma_desc_sw64(st);
-          const uint64_t alo = umma_desc_sw64(st + P_A_TILE);
-          const uint64_t bhi = umma_desc_sw64(st + 2 * P_A_TILE);
-          const uint64_t blo = umma_desc_sw64(st + 2 * P_A_TILE + P_B_TILE);
+          const uint64_t ahi = umma_desc_k<BKT>(st);
+          const uint64_t alo = umma_desc_k<BKT>(st + P_A_TILE);
+          const uint64_t bhi = umma_desc_k<BKT>(st + 2 * P_A_TILE);
+          const uint64_t blo = umma_desc_k<BKT>(st + 2 * P_A_TILE + P_B_TILE);
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
+          for (int k = 0; k < BKT / 8; ++k) {
             const uint64_t koff = (uint64_t)((k * 32) >> 4);
             const uint32_t acc = (kb | k) != 0;
             tc_mma_tf32_pair(d_small, ahi + koff, blo + koff, kIdescPair, acc);
@@ -578,15 +600,16 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows) {
+int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows, int box_k = BK) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
-  const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return ELV_OK;
@@ -594,16 +617,65 @@ int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows
 
 }  // namespace
 
-static inline long long kpad(int K) { return round_up(K, BK); }
+static inline long long kpad(int K) { return round_up(K, 32); }   // both BK=16 and BK=32 kernels
 
-// ELV_TF32X3_PAIR=1 selects the cta_group::2 kernel (default off until measured)
-static bool use_pair() {
+// lo.lo (a 4th MMA per k-step) is added for short reductions, where the
+// missing ~2^-22 |a b| term is not averaged out over K (measured: without it
+// the worst err/bound is 3.4 at K=1 even with exact accumulation).
+// ELV_TF32X3_LOLO=0/1 forces it off/on (diagnostics).
+static int with_lolo(int K) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("ELV_TF32X3_LOLO");
+    force = e ? (atoi(e) != 0) : -1;
+  }
+  if (force >= 0) return force;
+  return K < 512 ? 1 : 0;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+// ELV_TF32X3_PAIR: 0 = 1-CTA kernel, 16 / 32 = cta_group::2 kernel with that BK
+static int pair_mode() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("ELV_TF32X3_PAIR");
-    v = e ? (atoi(e) != 0) : 0;
+    v = env_int("ELV_TF32X3_PAIR", 0);
+    if (v == 1) v = 16;
+    if (v != 0 && v != 16 && v != 32) v = 0;
   }
-  return v != 0;
+  return v;
+}
+static int tile_group(int dflt) {
+  static int v = -2;
+  if (v == -2) v = env_int("ELV_TILE_GROUP", -1);
+  return v > 0 ? v : dflt;
+}
+
+template <int BKT>
+static int launch_pair(const CUtensorMap& m_ahi_unused, const float* a_hi, const float* a_lo, const float* b_hi,
+                       const float* b_lo, float* C, int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st) {
+  (void)m_ahi_unused;
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  int rc = make_map(&ma_hi, a_hi, M, Kp, P_BM, BKT);
+  if (!rc) rc = make_map(&ma_lo, a_lo, M, Kp, P_BM, BKT);
+  if (!rc) rc = make_map(&mb_hi, b_hi, N, Kp, P_BN / 2, BKT);
+  if (!rc) rc = make_map(&mb_lo, b_lo, N, Kp, P_BN / 2, BKT);
+  if (rc) return rc;
+  static int attr_dev = -1;
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3_pair<BKT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PairCfg<BKT>::SMEM_BYTES);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 pair smem attribute: %s", cudaGetErrorString(e));
+    attr_dev = dev;
+  }
+  const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
+  int clusters = num_sms() / 2;
+  if (clusters > tiles) clusters = tiles;
+  k7_tf32x3_pair<BKT><<<2 * clusters, NUM_THREADS, PairCfg<BKT>::SMEM_BYTES, st>>>(
+      ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT, with_lolo(K), tile_group(8));
+  return check_launch("gemm_parallel_tf32x3_pair");
 }
 static inline size_t planes_bytes(int rows, int K) {
   return (size_t)(2 * (long long)rows * kpad(K)) * sizeof(float) + 128;
@@ -619,19 +691,6 @@ size_t tf32x3_workspace_bytes(int M, int N, int K) {
   return tf32x3_a_planes_bytes(M, K) + tf32x3_b_planes_bytes(N, K);
 }
 
-// lo.lo (a 4th MMA per k-step) is added for short reductions, where the
-// missing ~2^-22 |a b| term is not averaged out over K (measured: without it
-// the worst err/bound is 3.4 at K=1 even with exact accumulation).
-// ELV_TF32X3_LOLO=0/1 forces it off/on (diagnostics).
-static int with_lolo(int K) {
-  static int force = -2;
-  if (force == -2) {
-    const char* e = getenv("ELV_TF32X3_LOLO");
-    force = e ? (atoi(e) != 0) : -1;
-  }
-  if (force >= 0) return force;
-  return K < 512 ? 1 : 0;
-}
 
 int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st) {
   const int Kp = (int)kpad(K);
@@ -675,29 +734,12 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
     attr_dev = dev;
   }
-  if (use_pair()) {
-    CUtensorMap p_bhi, p_blo;
-    rc = make_map(&p_bhi, b_hi, N, Kp, P_BN / 2);
-    if (!rc) rc = make_map(&p_blo, b_lo, N, Kp, P_BN / 2);
-    if (rc) return rc;
-    static int pair_attr_dev = -1;
-    if (pair_attr_dev != dev) {
-      cudaError_t e = cudaFuncSetAttribute(k7_tf32x3_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           P_SMEM_BYTES);
-      if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 pair smem attribute: %s", cudaGetErrorString(e));
-      pair_attr_dev = dev;
-    }
-    const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
-    int clusters = num_sms() / 2;
-    if (clusters > tiles) clusters = tiles;
-    k7_tf32x3_pair<<<2 * clusters, NUM_THREADS, P_SMEM_BYTES, st>>>(m_ahi, m_alo, p_bhi, p_blo, C, M, N, ldc,
-                                                                     Kp / BK, with_lolo(K));
-    return check_launch("gemm_parallel_tf32x3_pair");
-  }
+  if (pair_mode() == 16) return launch_pair<16>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (pair_mode() == 32) return launch_pair<32>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / BK,
-                                                   with_lolo(K));
+                                                   with_lolo(K), tile_group(8));
   return check_launch("gemm_parallel_tf32x3");
 }
 

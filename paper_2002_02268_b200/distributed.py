@@ -82,7 +82,7 @@ class RowShardGemm:
 
 def column_chunks(N: int, chunks: int, align: int = 256):
     """Split [0, N) into <= `chunks` column blocks, each a multiple of `align`
-    (the 3xTF32 tile width; also a multiple of the 128-column packB unit)."""
+    (the 3xTF32 tile width and the 256-column packB padding unit)."""
     units = (N + align - 1) // align
     chunks = max(1, min(chunks, units))
     base, extra = divmod(units, chunks)
@@ -147,7 +147,7 @@ class PipelinedRowShardGemm:
         with torch.cuda.stream(self.stream):
             for n0, n1 in self.chunks:
                 Pc = self._panel(n0)
-                count = ((n1 - n0 + 127) // 128) * 128 * K     # packB writes whole 128-col groups
+                count = ((n1 - n0 + 255) // 256) * 256 * K     # packB writes whole 256-col groups
                 if self.rank == self.src:
                     self._check(lib.elv_pack_b(B.data_ptr() + 4 * n0, Pc.data_ptr(), K, n1 - n0, B.stride(0),
                                                32, st), "elv_pack_b")

@@ -42,7 +42,7 @@ def test_workspace_sizes():
     lib = _lib.load()
     for v in range(4):
         assert lib.elv_gemm_workspace_bytes(v, 1024, 1024, 1024) == 0
-    # packedB: ceil(N/128)*128 columns x K rows of fp32
+    # packedB: ceil(N/256)*256 columns x K rows of fp32
     for v in (4, 5, 6):
         assert lib.elv_gemm_workspace_bytes(v, 100, 1000, 33) == 1024 * 33 * 4
     assert lib.elv_pack_b_bytes(33, 1000) == 1024 * 33 * 4

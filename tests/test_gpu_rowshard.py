@@ -118,3 +118,32 @@ def test_host_pipeline_bitwise_equals_device_path(cuda, variant):
         assert torch.equal(C_host, C_dev)
     finally:
         I._PIPELINE_MIN_BYTES = old
+
+
+def test_c_abi_rowshard_single_process(cuda):
+    """elv_gemm_rowshard (one process, ncclCommInitAll) over the devices we
+    have (1 here): NCCL broadcast of B + pack + GEMM on each shard."""
+    import ctypes
+    from paper_2002_02268_b200 import _lib
+    lib = _lib.load()
+    ndev = 1
+    devs = (ctypes.c_int * ndev)(*range(ndev))
+    _lib.check(lib.elv_nccl_init(ndev, devs), "elv_nccl_init")
+    try:
+        M, N, K = 384, 640, 200
+        A = torch.empty((M, K), device=cuda); synth.fill_device(A, 6, 0)
+        B = torch.empty((K, N), device=cuda); synth.fill_device(B, 6, 1)
+        P = torch.empty(lib.elv_pack_b_bytes(K, N) // 4, device=cuda)
+        C = torch.empty((M, N), device=cuda)
+        vp = ctypes.c_void_p
+        arr = lambda *xs: (vp * ndev)(*xs)
+        rows = (ctypes.c_int * ndev)(M)
+        stream = torch.cuda.current_stream().cuda_stream
+        rc = lib.elv_gemm_rowshard(6, ndev, devs, arr(A.data_ptr()), arr(B.data_ptr()), arr(P.data_ptr()),
+                                   arr(C.data_ptr()), rows, N, K, arr(stream))
+        _lib.check(rc, "elv_gemm_rowshard")
+        torch.cuda.synchronize()
+        ref = interp.gemm(_plan(6, M, N, K), A, B)
+        assert torch.equal(C, ref)
+    finally:
+        lib.elv_nccl_destroy()
