@@ -150,6 +150,29 @@ __device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr) {
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
+// Wave synchronisation of the persistent CTAs' producers: before loading its
+// (w+1)-th tile a producer waits until every CTA has issued the loads of its
+// w-th tile.  Tiles that run concurrently share A rows / B columns through L2
+// only while their k positions stay close; unsynchronised, per-tile timing
+// noise lets the CTAs drift apart over hundreds of tiles and the operands
+// are re-read from HBM (measured: 222-260 GB of DRAM reads per 32768^2 x 8192
+// launch against ~64-83 GB for lock-step waves).  The wait is bounded
+// (~20 us) so a CTA that is not resident (e.g. SMs busy with an NCCL kernel)
+// never stalls the others for long.
+__device__ __forceinline__ void wave_sync_wait(unsigned int* ctr, unsigned int target) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 20000) break;
+    __nanosleep(64);
+  }
+}
+
 struct TileSched {
   int tiles_m, tiles_n, group;
   __device__ void coords(int t, int& m0, int& n0) const {
@@ -167,7 +190,8 @@ struct TileSched {
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-          float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group) {
+          float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
+          unsigned int* __restrict__ wave_ctr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -203,9 +227,11 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       int s = 0; uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int wave = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++wave) {
         int m0, n0;
         sched.coords(t, m0, n0);
+        if (wave_ctr != nullptr && wave > 0) wave_sync_wait(wave_ctr, (unsigned)(wave * gridDim.x));
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * STAGE_BYTES;
@@ -217,6 +243,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           tma_load_2d(&map_blo, &full[s], st + 2 * A_TILE_BYTES + B_TILE_BYTES, k0, n0);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        if (wave_ctr != nullptr) atomicAdd(wave_ctr, 1u);
       }
     }
   } else if (warp == 1) {
@@ -647,6 +674,29 @@ static int pair_mode() {
   }
   return v;
 }
+// per-device wave counter (library-internal scratch, 4 bytes), zeroed on the
+// launch stream before every launch; ELV_WAVE_SYNC=0 disables the sync.
+static unsigned int* wave_counter(int dev, cudaStream_t st) {
+  static int enabled = -1;
+  if (enabled < 0) enabled = env_int("ELV_WAVE_SYNC", 1) != 0;
+  if (!enabled) return nullptr;
+  static std::mutex mu;
+  static unsigned int* ctrs[64] = {nullptr};
+  if (dev < 0 || dev >= 64) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (ctrs[dev] == nullptr && cudaMalloc(&ctrs[dev], 256) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  if (cudaMemsetAsync(ctrs[dev], 0, sizeof(unsigned int), st) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return ctrs[dev];
+}
+
 static int tile_group(int dflt) {
   static int v = -2;
   if (v == -2) v = env_int("ELV_TILE_GROUP", -1);
@@ -738,8 +788,9 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   if (pair_mode() == 32) return launch_pair<32>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  unsigned int* ctr = wave_counter(dev, st);
   k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / BK,
-                                                   with_lolo(K), tile_group(8));
+                                                   with_lolo(K), tile_group(16), ctr);
   return check_launch("gemm_parallel_tf32x3");
 }
 
