@@ -146,8 +146,9 @@ size_t elv_gemm_workspace_bytes(int variant, int M, int N, int K) {
   if (M < 1 || N < 1 || K < 1) return 0;
   switch (variant) {
     case ELV_ARRAYPACKING:
-    case ELV_CACHEBLOCKS:
-    case ELV_PARALLEL: return elv_pack_b_bytes(K, N);
+    case ELV_CACHEBLOCKS: return elv_pack_b_bytes(K, N);
+    case ELV_PARALLEL:
+      return elv_pack_b_bytes(K, N) + (parallel_uses_packed_a(M, N) ? pack_a_bytes(M, K) : 0);
     case ELV_PARALLEL_TF32X3: return tf32x3_workspace_bytes(M, N, K);
     default: return 0;
   }
@@ -218,8 +219,13 @@ int elv_gemm_prepare(int variant, const float* A, const float* B, int M, int N, 
   switch (variant) {
     case ELV_ARRAYPACKING:
     case ELV_CACHEBLOCKS:
-    case ELV_PARALLEL:
       return launch_pack_b(B, static_cast<float*>(workspace), K, N, ldb, st);
+    case ELV_PARALLEL: {
+      int rc2 = launch_pack_b(B, static_cast<float*>(workspace), K, N, ldb, st);
+      if (rc2 || !parallel_uses_packed_a(M, N)) return rc2;
+      return launch_pack_a(A, reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + elv_pack_b_bytes(K, N)),
+                           M, K, lda, st);
+    }
     case ELV_PARALLEL_TF32X3:
       return tf32x3_prepare(A, B, M, N, K, lda, ldb, workspace, workspace_bytes, st);
     default:
@@ -239,9 +245,15 @@ int elv_gemm_compute(int variant, const float* A, const float* B, float* C, int 
     case ELV_VECTORIZED:
     case ELV_LOOPPERM:
       return launch_simt(variant, A, B, nullptr, C, M, N, K, lda, ldb, ldc, st);
+    case ELV_PARALLEL:
+      if (parallel_uses_packed_a(M, N))
+        return launch_parallel_packed(
+            reinterpret_cast<const float*>(static_cast<const uint8_t*>(workspace) + elv_pack_b_bytes(K, N)),
+            static_cast<const float*>(workspace), C, M, N, K, ldc, st);
+      return launch_simt(variant, A, nullptr, static_cast<const float*>(workspace), C, M, N, K, lda, 0,
+                         ldc, st);
     case ELV_ARRAYPACKING:
     case ELV_CACHEBLOCKS:
-    case ELV_PARALLEL:
       return launch_simt(variant, A, nullptr, static_cast<const float*>(workspace), C, M, N, K, lda, 0,
                          ldc, st);
     case ELV_PARALLEL_TF32X3:

@@ -34,6 +34,11 @@ inline int num_sms() {
 int launch_simt(int variant, const float* A, const float* B, const float* packedB,
                 float* C, int M, int N, int K, int lda, int ldb, int ldc, cudaStream_t st);
 int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStream_t st);
+size_t pack_a_bytes(int M, int K);
+int launch_pack_a(const float* A, float* packedA, int M, int K, int lda, cudaStream_t st);
+int launch_parallel_packed(const float* packedA, const float* packedB, float* C, int M, int N, int K, int ldc,
+                           cudaStream_t st);
+bool parallel_uses_packed_a(int M, int N);
 
 // tcgen05 3xTF32 (tf32x3_gemm.cu)
 size_t tf32x3_workspace_bytes(int M, int N, int K);

@@ -633,6 +633,171 @@ k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* _
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6 on packed operands (the default `parallel` path of elv_gemm): A is
+// packed by the prepass like B (packedA[M/128][K][128], the "packB" treatment
+// applied to the other operand), so every k-block of both tiles is a
+// contiguous run of 16-byte chunks.  The main loop is then a 4-stage
+// cp.async (LDGSTS) pipeline with no register staging and no transposing
+// stores, and the registers that frees hold a second A/B fragment set so the
+// next k-step's LDS overlap the current 128 FFMAs.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int CP_BK = 16, CP_STAGES = 4;
+constexpr int CP_SMEM = CP_STAGES * CP_BK * (128 + 256) * 4;    // 96 KB
+
+template <int ORDER>
+__global__ void __launch_bounds__(256, 1)
+k6_sgemm_cp(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
+            int M, int N, int K, int ldc) {
+  extern __shared__ __align__(16) float smem_f[];
+  float* As = smem_f;                               // [STAGES][BK][128]
+  float* Bs = smem_f + CP_STAGES * CP_BK * 128;     // [STAGES][BK][256]
+  constexpr int BM = 128, BN = 256;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lm = lane >> 2, ln = lane & 3;
+  const int trow = wm * 64 + lm * 4;
+  const int tcol = wn * 64 + ln * 4;
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nkb = (K + CP_BK - 1) / CP_BK;
+
+  for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+    const int row0 = tc.m * BM, col0 = tc.n * BN;
+    const float* pa = PA + (size_t)tc.m * K * BM;
+    const float* pb = PB + (size_t)(col0 >> 5) * K * kPanel;
+    auto issue = [&](int kb, int slot) {
+      const int k0 = kb * CP_BK;
+#pragma unroll
+      for (int i = 0; i < CP_BK * 32 / 256; ++i) {          // A: BK rows of 128 floats
+        const int q = tid + i * 256;
+        const int kk = q >> 5, c4 = (q & 31) * 4;
+        const int gk = k0 + kk;
+        cp_async16(&As[(slot * CP_BK + kk) * BM + c4], pa + (size_t)min(gk, K - 1) * BM + c4, gk < K ? 16 : 0);
+      }
+#pragma unroll
+      for (int i = 0; i < CP_BK * 64 / 256; ++i) {          // B: 8 panels x BK rows x 32 floats
+        const int q = tid + i * 256;
+        const int pnl = q / (CP_BK * 8), w = q % (CP_BK * 8);
+        const int kk = w >> 3, c4 = (w & 7) * 4;
+        const int gk = k0 + kk;
+        cp_async16(&Bs[(slot * CP_BK + kk) * BN + pnl * 32 + c4],
+                   pb + ((size_t)pnl * K + min(gk, K - 1)) * kPanel + c4, gk < K ? 16 : 0);
+      }
+    };
+
+    float acc[8][16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[i][j] = 0.f;
+
+#pragma unroll
+    for (int st = 0; st < CP_STAGES - 1; ++st) {
+      if (st < nkb) issue(st, st);
+      cp_async_commit();
+    }
+    for (int kb = 0; kb < nkb; ++kb) {
+      cp_async_wait<CP_STAGES - 2>();
+      __syncthreads();
+      const int nk = kb + CP_STAGES - 1;
+      if (nk < nkb) issue(nk, nk % CP_STAGES);
+      cp_async_commit();
+      const float* as = As + (kb % CP_STAGES) * CP_BK * BM;
+      const float* bs = Bs + (kb % CP_STAGES) * CP_BK * BN;
+      float a[2][8], b[2][16];
+      auto lfrag = [&](int slot, int k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * BM + trow);
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * BM + trow + 32);
+        a[slot][0] = a0.x; a[slot][1] = a0.y; a[slot][2] = a0.z; a[slot][3] = a0.w;
+        a[slot][4] = a1.x; a[slot][5] = a1.y; a[slot][6] = a1.z; a[slot][7] = a1.w;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float4 bv = *reinterpret_cast<const float4*>(bs + k * BN + tcol + 16 * h);
+          b[slot][4 * h] = bv.x; b[slot][4 * h + 1] = bv.y; b[slot][4 * h + 2] = bv.z; b[slot][4 * h + 3] = bv.w;
+        }
+      };
+      lfrag(0, 0);
+#pragma unroll
+      for (int k = 0; k < CP_BK; ++k) {
+        if (k + 1 < CP_BK) lfrag((k + 1) & 1, k + 1);
+        if (ORDER == 0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[i][j] = fmaf(a[k & 1][i], b[k & 1][j], acc[i][j]);
+        } else if (ORDER == 1) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i][j] = fmaf(a[k & 1][i], b[k & 1][j], acc[i][j]);
+        } else {                                   // 2x2 blocks: both operands reused in pairs
+#pragma unroll
+          for (int i = 0; i < 8; i += 2)
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+              acc[i][j] = fmaf(a[k & 1][i], b[k & 1][j], acc[i][j]);
+              acc[i][j + 1] = fmaf(a[k & 1][i], b[k & 1][j + 1], acc[i][j + 1]);
+              acc[i + 1][j + 1] = fmaf(a[k & 1][i + 1], b[k & 1][j + 1], acc[i + 1][j + 1]);
+              acc[i + 1][j] = fmaf(a[k & 1][i + 1], b[k & 1][j], acc[i + 1][j]);
+            }
+        }
+      }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int gj = col0 + tcol + h * 16;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float* v = &acc[i][h * 4];
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+    __syncthreads();                               // smem slots are reused by the next tile
+  }
+}
+
+// packA: packedA[p][k][r] = A[128p + r][k], zero past M.  32x32 tiles through
+// SMEM so both the row reads of A and the panel-row writes coalesce.
+__global__ void __launch_bounds__(256)
+k_pack_a(const float* __restrict__ A, float* __restrict__ PA, int M, int K, int lda) {
+  __shared__ float tt[32][33];
+  const int k0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty + 8 * i, k = k0 + tx;
+    tt[ty + 8 * i][tx] = (r < M && k < K) ? __ldg(A + (size_t)r * lda + k) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + ty + 8 * i, r = r0 + tx;
+    if (k < K) PA[((size_t)(r >> 7) * K + k) * 128 + (r & 127)] = tt[tx][ty + 8 * i];
+  }
+}
+
 struct SgemmCfg { void (*fn)(const float*, const float*, float*, int, int, int, int, int); int minb, bm, bn; };
 static const SgemmCfg kSgemmCfgs[] = {
     {k6_sgemm_db<8, 2>, 2, 128, 128}, {k6_sgemm_db<8, 1>, 1, 128, 128}, {k6_sgemm_db<16, 2>, 2, 128, 128},
@@ -691,6 +856,52 @@ int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStr
   if (blocks < 1) blocks = 1;
   k_pack_b<<<(unsigned)blocks, 256, 0, st>>>(B, packedB, K, N, ldb, panels, vecB);
   return check_launch("pack_b");
+}
+
+// the packed-A cp.async kernel serves the large-problem regime of the
+// parallel schedule (the same regime as the 8x16 kernel); ELV_SGEMM_CP=0
+// falls back to the raw-A kernels for tuning comparisons.
+bool parallel_uses_packed_a(int M, int N) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("ELV_SGEMM_CP");
+    enabled = e ? (atoi(e) != 0) : 1;
+  }
+  if (!enabled) return false;
+  const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
+  return tiles >= 2LL * num_sms();
+}
+
+size_t pack_a_bytes(int M, int K) { return (size_t)((M + 127) / 128) * 128 * (size_t)K * sizeof(float); }
+
+int launch_pack_a(const float* A, float* packedA, int M, int K, int lda, cudaStream_t st) {
+  dim3 grid((K + 31) / 32, (M + 127) / 128 * 4);
+  k_pack_a<<<grid, 256, 0, st>>>(A, packedA, M, K, lda);
+  return check_launch("pack_a");
+}
+
+int launch_parallel_packed(const float* packedA, const float* packedB, float* C, int M, int N, int K, int ldc,
+                           cudaStream_t st) {
+  static int order = -1;
+  if (order < 0) {
+    const char* e = getenv("ELV_SGEMM_ORDER");
+    order = e ? atoi(e) : 2;              // measured: 2x2 FFMA blocks 51.97 TF vs 51.0 / 48.6
+    if (order < 0 || order > 2) order = 2;
+  }
+  auto fn = order == 0 ? k6_sgemm_cp<0> : order == 1 ? k6_sgemm_cp<1> : k6_sgemm_cp<2>;
+  static int attr_dev[3] = {-1, -1, -1};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev[order] != dev) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, CP_SMEM);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "sgemm_cp smem attribute: %s", cudaGetErrorString(e));
+    attr_dev[order] = dev;
+  }
+  const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
+  long long grid = num_sms();
+  if (grid > tiles) grid = tiles;
+  fn<<<(unsigned)grid, 256, CP_SMEM, st>>>(packedA, packedB, C, M, N, K, ldc);
+  return check_launch("gemm_parallel");
 }
 
 int launch_simt(int variant, const float* A, const float* B, const float* packedB,
