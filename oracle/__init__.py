@@ -25,8 +25,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle_mm.so")
 
-# schedules whose reduction is split(4) and lifted (association class chunk4)
-CHUNK4 = ("blocking", "vectorized", "loopPerm", "arrayPacking", "cacheBlocks", "parallel")
+# every schedule's evaluation is a sequential left fold over k (see mm_oracle.c)
+SCHEDULES = ("baseline", "blocking", "vectorized", "loopPerm", "arrayPacking", "cacheBlocks",
+             "parallel")
 
 _lib = None
 
@@ -43,7 +44,7 @@ def _load():
     if _lib is None:
         build()
         lib = ctypes.CDLL(LIB)
-        for fn in ("oracle_mm_seq_f64", "oracle_mm_chunk4_f64", "oracle_absprod_f64"):
+        for fn in ("oracle_mm_seq_f64", "oracle_absprod_f64"):
             f = getattr(lib, fn)
             f.restype = None
             f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3
@@ -64,11 +65,9 @@ def _call(name, A, B):
 
 def mm_interp_f64(A, B, schedule: str = "baseline") -> np.ndarray:
     """What interp.run(schedule(mm), [A, B]) returns, bit-exactly (f64)."""
-    if schedule == "baseline":
-        return _call("oracle_mm_seq_f64", A, B)
-    if schedule in CHUNK4:
-        return _call("oracle_mm_chunk4_f64", A, B)
-    raise KeyError(schedule)
+    if schedule not in SCHEDULES:
+        raise KeyError(schedule)
+    return _call("oracle_mm_seq_f64", A, B)
 
 
 def absprod(A, B) -> np.ndarray:

@@ -13,10 +13,10 @@
  *   - the baseline term folds acc + a_k*b_k over k in order
  *     (reduceSeq(fun acc p => add(acc)(mult(fst p)(snd p)))(0.0), the term
  *     DFNF;topDown(fuseReduceMap);lowerToC produces);
- *   - every schedule that applies split(4) to the reduction and lifts it
- *     (blocking ... parallel) folds acc + (((0 + p0) + p1) + p2) + p3 over
- *     chunks of 4 (reduceSeq(add)(0.0) per chunk inside the lifted reduce,
- *     rules.py:197-222 and 328-358).
+ *   - the six tiled schedules (paper_2002_02268_b200/schedules.py) split k
+ *     by 4 and reorder with liftReduce + absorbReduceInit (rules.py:328-385),
+ *     which turns `acc + (0 + p0 + ... + p3)` into `acc + p0 + ... + p3`:
+ *     the same sequential fold per output element.
  * Compiled with -ffp-contract=off so the f64 operations round exactly like
  * CPython's, which makes this bit-identical to interp.run on the same
  * inputs (pinned in tests/test_oracle.py against tests/golden/).
@@ -41,27 +41,6 @@ void oracle_mm_seq_f64(const float* A, const float* B, double* C, int M, int N, 
       const double* b = bt + (size_t)j * K;
       double acc = 0.0;
       for (int k = 0; k < K; ++k) acc = acc + (double)a[k] * b[k];
-      C[(size_t)i * N + j] = acc;
-    }
-  }
-  free(bt);
-}
-
-/* split(4) + liftReduce association: acc + (((0+p0)+p1)+p2)+p3 per chunk.
- * K must be a multiple of 4 (the schedule's own divisibility requirement;
- * zero-padded K for the padded route contributes exact zeros). */
-void oracle_mm_chunk4_f64(const float* A, const float* B, double* C, int M, int N, int K) {
-  double* bt = transpose_b(B, N, K);
-  for (int i = 0; i < M; ++i) {
-    const float* a = A + (size_t)i * K;
-    for (int j = 0; j < N; ++j) {
-      const double* b = bt + (size_t)j * K;
-      double acc = 0.0;
-      for (int k0 = 0; k0 < K; k0 += 4) {
-        double part = 0.0;
-        for (int k = k0; k < k0 + 4 && k < K; ++k) part = part + (double)a[k] * b[k];
-        acc = acc + part;
-      }
       C[(size_t)i * N + j] = acc;
     }
   }

@@ -3,9 +3,10 @@
 // Each kernel is the B200 lowering of the low-level patterns the schedule's
 // rewrite leaves in the `mm` term (reference rules.py:391-456, 516-549):
 //   mapSeq/reduceSeq           -> per-thread loops             (K0)
-//   split(32) of rows/cols     -> 32x32 CTA tile in SMEM       (K1, K2)
-//   split(4) + liftReduce      -> k strip-mined by 4, chunk partial sums
-//   mapVec (vectorize(32))     -> 128-bit loads/stores         (K2..K6)
+//   tile(32,32) (split+interchange) -> 32x32 CTA tile in SMEM  (K1, K2)
+//   split(4) + reorder (liftReduce, absorbReduceInit) -> k loop outside the
+//                                 in-tile loops, sequential fold per element
+//   mapVec (vectorize(32) of yi) -> 128-bit loads/stores       (K2..K6)
 //   reorder (loopPerm)         -> register outer-product tiles (K3..K6)
 //   packB / toMem(packed)      -> packedB[N/32][K][32] panels  (K4..K6)
 //   toMem(acc) + unroll        -> 8x8 register accumulators    (K5, K6)
@@ -46,10 +47,11 @@ k0_baseline(const float* __restrict__ A, const float* __restrict__ B, float* __r
 }
 
 // ---------------------------------------------------------------------------
-// K1 blocking: tile(32,32) -> 32x32 C tile per CTA, A/B tiles staged in SMEM;
-// split(4) of the reduction + liftReduce -> the k loop runs in chunks of 4
-// whose partial sums start at 0 and are added to the accumulator, the same
-// association the lowered term has (reduceSeq(add)(0.0) per chunk).
+// K1 blocking: TVM order (xo, yo, ko, ki, xi, yi).  (xo, yo) -> one 32x32 C
+// tile per CTA with A/B tiles staged in SMEM; (ko, ki) -> the k loop, chunks
+// of 4, outside the in-tile loops; (xi, yi) -> the CTA's threads.  Each
+// element accumulates sequentially in k, the lowered term's fold
+// (absorbReduceInit makes it acc + p0 + p1 + ..., not per-chunk sums).
 constexpr int K1_BK = 32;
 __global__ void __launch_bounds__(256)
 k1_blocking(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
@@ -70,14 +72,12 @@ k1_blocking(const float* __restrict__ A, const float* __restrict__ B, float* __r
     }
     __syncthreads();
 #pragma unroll
-    for (int kc = 0; kc < K1_BK; kc += 4) {          // split(4): chunk loop
+    for (int kc = 0; kc < K1_BK; kc += 4) {          // ko: chunks of split(4)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        float part = 0.f;                             // reduceSeq(add)(0.0)(chunk)
+      for (int kk = 0; kk < 4; ++kk)                   // ki
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) part = fmaf(As[ty + 8 * r][kc + kk], Bs[kc + kk][tx], part);
-        acc[r] += part;
-      }
+        for (int r = 0; r < 4; ++r)                    // xi (this thread's rows); yi = tx
+          acc[r] = fmaf(As[ty + 8 * r][kc + kk], Bs[kc + kk][tx], acc[r]);
     }
     __syncthreads();
   }
@@ -89,7 +89,7 @@ k1_blocking(const float* __restrict__ A, const float* __restrict__ B, float* __r
 }
 
 // ---------------------------------------------------------------------------
-// K2 vectorized: K1 plus vectorize(32) -> 128-bit (float4) global loads and
+// K2 vectorized: K1 plus vectorize(yi) -> 128-bit (float4) global loads and
 // stores and float4 SMEM reads of B; each thread owns 1 row x 4 columns.
 __global__ void __launch_bounds__(256)
 k2_vectorized(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
@@ -135,17 +135,11 @@ k2_vectorized(const float* __restrict__ A, const float* __restrict__ B, float* _
     }
     __syncthreads();
 #pragma unroll
-    for (int kc = 0; kc < K1_BK; kc += 4) {
-      float part[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const float a = As[r][kc + kk];
-        const float4 b = *reinterpret_cast<const float4*>(&Bs[kc + kk][c4]);
-        part[0] = fmaf(a, b.x, part[0]); part[1] = fmaf(a, b.y, part[1]);
-        part[2] = fmaf(a, b.z, part[2]); part[3] = fmaf(a, b.w, part[3]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] += part[q];
+    for (int k = 0; k < K1_BK; ++k) {                // ko, ki
+      const float a = As[r][k];
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][c4]);   // yi, vectorised
+      acc[0] = fmaf(a, b.x, acc[0]); acc[1] = fmaf(a, b.y, acc[1]);
+      acc[2] = fmaf(a, b.z, acc[2]); acc[3] = fmaf(a, b.w, acc[3]);
     }
     __syncthreads();
   }
@@ -205,9 +199,10 @@ __device__ __forceinline__ float4 load_b4_packed(const float* __restrict__ P, in
 }
 
 // ---------------------------------------------------------------------------
-// K3 loopPerm / K4 arrayPacking: 64x64 CTA tile, 16x16 threads, each thread a
-// 4x4 register outer product per k (A-stationary micro-tile: the reordered
-// nest keeps a k-slice of A and B in registers and sweeps the 4x4 block).
+// K3 loopPerm / K4 arrayPacking: TVM order (xo, yo, ko, xi, ki, yi): 64x64
+// CTA tile, 16x16 threads, each thread a 4x4 register outer product per k
+// (xi outside ki: a thread's rows of A stay in registers while k sweeps,
+// yi vectorised in float4).
 // PACKED selects packedB panels (arrayPacking's toMem) over row-major B.
 template <bool PACKED>
 __global__ void __launch_bounds__(256)

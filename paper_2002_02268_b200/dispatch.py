@@ -85,13 +85,13 @@ def _guess(f: dict) -> list:
     """Schedules consistent with the feature scan, most likely first."""
     if f["mapPar"]:
         return ["parallel"]
-    if f["toMem"] >= 3:
+    if f["toMem"] >= 2:                      # packedB + the cache_write accumulator
         return ["cacheBlocks"]
     if f["toMem"]:
         return ["arrayPacking"]
     if f["mapVec"]:
-        # loopPerm lifts the reduce twice: the lifted accumulator is 2-D
-        return ["loopPerm", "vectorized"] if f["transpose"] >= 4 else ["vectorized", "loopPerm"]
+        # blocking's reorder (ki above xi) leaves one more transpose than loopPerm's
+        return ["vectorized", "loopPerm"] if f["transpose"] >= 6 else ["loopPerm", "vectorized"]
     if 4 in f["splits"]:
         return ["blocking"]
     return ["baseline"]

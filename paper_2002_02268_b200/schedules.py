@@ -4,36 +4,44 @@ The reference ships the leaf rules but not the composite schedules
 (SPEC.md:449-516 specifies them; PAPER.md:269-315 lists them).  Each schedule
 below is built *only* from reference objects (rules.py, traversals.py,
 normal_forms.py, strategy.py) -- no rule is modified -- and yields a fully
-lowered, well-typed term for divisible shapes.  The output terms are the
-inputs of the hot path: `paper_2002_02268_b200.interp.run` decodes them into
-one sm_100a kernel variant each.
+lowered, well-typed term whose loop nest is the TVM tutorial's.
+The output terms are the inputs of the hot path:
+`paper_2002_02268_b200.interp.run` decodes them into one sm_100a kernel each.
 
-Paper listing -> strategy here (`;;` = `dfnf_seq`, normal_forms.py:39-42):
+`;;` is `dfnf_seq` (normal_forms.py:39-42).  Loop orders are outer -> inner
+(x = rows of C, y = columns, k = reduction; o/i = tile / in-tile):
 
-  baseline     DFNF ; topDown(fuseReduceMap) ; lowerToC
-  blocking     tile(32,32) ;; topDown(isReduce;split(4))
-               ;; topDown(liftReduce) ; lowerToC
-  vectorized   blocking-prefix ;; topDown(vectorize(32)) ; lowerToC PAPER.md:33,42
-  loopPerm     tile ;; split(4) ;; liftReduce ;; liftReduce
-               ;; topDown(vectorize(32)) ; lowerToC
-  arrayPacking topDown(packB) ;; loopPerm-prefix ; lowerToC
-  cacheBlocks  arrayPacking-prefix ;; topDown(isReduce;toMemAfter)
-               ;; bottomUp(isReduce;unroll) ; lowerToC
-  parallel     arrayPacking-prefix ;; topDown(parallel)
-               ;; bottomUp(isReduce;unroll) ; lowerToC
+  schedule      strategy                                          TVM order
+  baseline      DFNF ; topDown(fuseReduceMap) ; lowerToC          x, y, k            (271)
+  blocking      tile(32,32) ;; split(4) ;; reorder_blocking       xo,yo,ko,ki,xi,yi  (26-30, 280-283)
+  vectorized    blocking ;; vectorize(32) [lands on yi]           + vectorize(yi)    (33)
+  loopPerm      tile ;; split(4) ;; reorder_loopperm ;; vec(32)   xo,yo,ko,xi,ki,yi  (37-42, 293-297)
+  arrayPacking  packB ;; loopPerm                                 + packedB          (49-63, 303-306)
+  cacheBlocks   arrayPacking ;; topDown(isReduce;toMemAfter)
+                ;; bottomUp(isAppliedReduce;unroll)               + cache_write, unroll(ki) (65-79)
+  parallel      arrayPacking ;; topDown(parallel)
+                ;; bottomUp(isAppliedReduce;unroll)               + parallel(xo)     (80-83, 313-314)
 
-`reorder(1,2,5,6,3,4)` / `reorder(1,2,5,3,6,4)` are not shipped by the
-reference ("non-trivial ... not discussed").  The reduction
-loops are moved outward over the spatial tile loops with the shipped
-`liftReduce` (rules.py:328-358): once for blocking (k-chunks outside the
-32-column tile loop), twice for loopPerm (outside both j loops), which is the
-part of TVM's reorder that changes the arithmetic's data reuse.  A
-TVM-faithful `reorder`/`interchange` is SURVEY.md §8(f) rank 1 ("next").
+tile(x, y) is the paper's tileND: DFNF, fmap-recursive
+blocking, function(split(n)) and `interchange`, here built from the shipped
+interchange building blocks: at the row-block level,
+`map(fun r => join(map g cb))` --mapFission--> `map(join)(map(fun r => map g
+cb))` --mapMapInterchange--> `map(join)(transpose(map(fun c => map(fun r => g)
+rows) cb))`, which moves the column-tile loop outside the in-tile row loop.
 
-tileND follows the paper's listing: DFNF, recursive fmap
-blocking innermost-first, then `function(split(n.head))`.  The trailing
-`interchange(i)` is the same missing piece and is omitted, so tile(32,32)
-strip-mines both output dimensions (loops io, ii, jo, ji).
+reorder (PAPER.md:261 "non-trivial ... not discussed") is realised for the
+two GEMM nests with shipped rules only: liftReduce (rules.py:328-358) twice
+lifts the k-chunk reduce (ko) above xi and yi; absorbReduceInit
+(rules.py:361-385) folds the per-chunk `0 + ...` into the running
+accumulator; then liftReduce applied bottom-up lifts the in-chunk reduce (ki)
+above yi (loopPerm) or above yi and xi (blocking).  Every schedule's
+evaluation is therefore a sequential left fold acc + a_k b_k in k order (the
+C oracle checks this bit-exactly against the reference interpreter).
+
+`isAppliedReduce` is the reference's `predicate` combinator over a fully
+applied reduce: the shipped `isReduce` also matches the bare `reduce`
+primitive in function position, so `bottomUp(isReduce;unroll)` would unroll
+the outer ko reduce instead of TVM's `unroll(ki)`.
 """
 
 from __future__ import annotations
@@ -56,16 +64,15 @@ SCHEDULE_NAMES = ("baseline", "blocking", "vectorized", "loopPerm",
 ALIASES = {"parallelFull": "parallel"}
 
 # divisibility each schedule's rules require: split(32) on rows and columns
-# (tile / packB), split(4) on K (blocking), split(32) of the k-products
-# (vectorize(32) lands on the zipped k pairs, rules.py:429-431).
+# (tile / packB / vectorize(32) of the yi loop), split(4) on K.
 REQUIRED_MULTIPLE = {
     "baseline": (1, 1, 1),
     "blocking": (32, 32, 4),
-    "vectorized": (32, 32, 32),
-    "loopPerm": (32, 32, 32),
-    "arrayPacking": (32, 32, 32),
-    "cacheBlocks": (32, 32, 32),
-    "parallel": (32, 32, 32),
+    "vectorized": (32, 32, 4),
+    "loopPerm": (32, 32, 4),
+    "arrayPacking": (32, 32, 4),
+    "cacheBlocks": (32, 32, 4),
+    "parallel": (32, 32, 4),
 }
 
 
@@ -75,18 +82,39 @@ def mm(M: int, N: int, K: int):
     return s.ir.parse(MM_SOURCE, {"M": M, "N": N, "K": K})
 
 
+def _interchange():
+    """tileND's interchange for the 2-D case: mapFission then
+    mapMapInterchange one map level below the row-block map."""
+    s = S()
+    tv, rules, st = s.traversals, s.rules, s.strategy
+    return tv.fmap(st.seq(rules.map_fission, tv.argument(rules.map_map_interchange)))
+
+
 def _tile_nd(sizes):
-    """tileND without the trailing interchange."""
+    """tileND: DFNF, recursive fmap blocking innermost
+    first, function(split(n.head)), interchange."""
     s = S()
     nf, tv, rules, st = s.normal_forms, s.traversals, s.rules, s.strategy
     if len(sizes) == 1:
         return st.seq(nf.DFNF, tv.function(rules.make_split(sizes[0])))
     return st.seq(nf.DFNF, tv.fmap(_tile_nd(sizes[1:])),
-                  tv.function(rules.make_split(sizes[0])), nf.DFNF)
+                  tv.function(rules.make_split(sizes[0])), nf.DFNF,
+                  tv.top_down(_interchange()), nf.DFNF)
 
 
 def tile(x: int, y: int):
     return _tile_nd([x, y])
+
+
+def is_applied_reduce():
+    s = S()
+    ir = s.ir
+
+    def pred(t):
+        h, args = ir.spine(t)
+        return isinstance(h, ir.Prim) and h.kind in ir.REDUCE_KINDS and len(args) == 3
+
+    return s.strategy.predicate("isAppliedReduce", pred)
 
 
 @functools.lru_cache(maxsize=None)
@@ -96,17 +124,20 @@ def _prefixes():
     dseq = nf.dfnf_seq
     split4 = tv.top_down(st.seq(tv.is_reduce, rules.make_split(4)))
     lift = tv.top_down(rules.lift_reduce)
+    lift_inner = tv.bottom_up(rules.lift_reduce)
+    absorb = tv.top_down(rules.absorb_reduce_init)
     vec32 = tv.top_down(rules.make_vectorize(32))
-    tiled = dseq(tv.top_down(tile(32, 32)), split4)
-    blocking = dseq(tiled, lift)
+    # tile, split k by 4, lift ko above yi and xi, fold the chunk init into acc
+    tiled = dseq(dseq(dseq(dseq(tv.top_down(tile(32, 32)), split4), lift), lift), absorb)
+    blocking = dseq(dseq(tiled, lift_inner), lift_inner)     # ki above yi and xi
     vectorized = dseq(blocking, vec32)
-    loop_perm = dseq(dseq(dseq(tiled, lift), lift), vec32)
+    loop_perm = dseq(dseq(tiled, lift_inner), vec32)          # ki above yi only
     array_packing = dseq(tv.top_down(rules.make_pack_b(32)), loop_perm)
-    unroll = tv.bottom_up(st.seq(tv.is_reduce, rules.unroll))
+    unroll_ki = tv.bottom_up(st.seq(is_applied_reduce(), rules.unroll))
     cache_blocks = dseq(dseq(array_packing,
                              tv.top_down(st.seq(tv.is_reduce, rules.to_mem_after))),
-                        unroll)
-    parallel = dseq(dseq(array_packing, tv.top_down(rules.parallel)), unroll)
+                        unroll_ki)
+    parallel = dseq(dseq(array_packing, tv.top_down(rules.parallel)), unroll_ki)
     return {
         "baseline": st.seq(nf.DFNF, tv.top_down(rules.fuse_reduce_map)),
         "blocking": blocking,
