@@ -274,7 +274,7 @@ def main():
     ap.add_argument("--M", type=int, default=32768)
     ap.add_argument("--N", type=int, default=32768)
     ap.add_argument("--K", type=int, default=8192)
-    ap.add_argument("--workload", default="rowshard", choices=["rowshard", "ladder"])
+    ap.add_argument("--workload", default="rowshard", choices=["rowshard", "ladder", "binomial"])
     ap.add_argument("--chunks", type=int, default=4, help="packedB broadcast chunks (N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -300,6 +300,9 @@ def main():
 
     if args.workload == "ladder":
         run_ladder(args, dev)
+        return
+    if args.workload == "binomial":
+        run_binomial(args, dev)
         return
 
     M, N, K = args.M, args.N, args.K
@@ -503,6 +506,38 @@ def run_ladder(args, dev):
                           "l2": "flushed (256 MB write) before every rep"}), flush=True)
         del A, B, C, call, flush
         torch.cuda.empty_cache()
+
+
+def run_binomial(args, dev, H=16384, W=16384):
+    """The paper's binomial-filter case study on B200:
+    one line per schedule.  HBM-bound: algorithmic bytes = 8 per pixel
+    (read the image once, write the result once)."""
+    import torch
+    from paper_2002_02268_b200 import binomial, synth
+    peaks, src = load_peaks()
+    img = torch.empty((H, W), device=dev)
+    synth.fill_device(img, 0, 2)
+    out = torch.empty_like(img)
+    stream = torch.cuda.current_stream(dev)
+    for name in binomial.SCHEDULE_NAMES:
+        term = binomial.apply(name, 64, 64)      # the schedule's kernel; decode is size-independent
+        v = binomial.decode(term)[0]
+        for _ in range(3):
+            binomial.launch(v, img, out)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(max(args.steps, 5)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream); binomial.launch(v, img, out); e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        gbs = 8.0 * H * W / (ms * 1e-3) / 1e9
+        print(json.dumps({"workload": f"binomial {name} {H}x{W}", "schedule": name, "H": H, "W": W,
+                          "ms": ms, "mpix_per_s": H * W / (ms * 1e-3) / 1e6, "gflops": 18.0 * H * W / (ms * 1e-3) / 1e9,
+                          "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                       "frac": gbs / peaks["hbm_gbs"], "peak_source": src},
+                          "l2": "image 1 GiB > L2"}), flush=True)
 
 
 if __name__ == "__main__":

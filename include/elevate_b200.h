@@ -119,6 +119,23 @@ int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
 int elv_fill_uniform(float* X, long long n, unsigned long long seed,
                      unsigned int tensor_id, long long offset, void* stream);
 
+/* Binomial filter, the paper's second data-parallel workload (reference
+ * PAPER.md:1618-1770; separateDot rule, reference rules.py:462-513):
+ * out = [1 2 1; 2 4 2; 1 2 1]/16 (*) clamp-padded img (pad2D(1) = padClamp,
+ * interp.py:127-132; slide2D(3,1); map2D(dot)).  Replaces
+ * interp.run(bf_schedule(bf), [img]) for the four binomial schedules.
+ * img/out: H x W fp32 row-major device buffers (no aliasing). */
+enum {
+  ELV_BF_NAIVE = 0,          /* lowerToC(bf)                                  */
+  ELV_BF_NAIVE_PAR = 1,      /* topDown(parallel) ; lowerToC                  */
+  ELV_BF_SEPARATED = 2,      /* topDown(separateDot) ; lowerToC               */
+  ELV_BF_SEPARATED_PAR = 3,  /* separateDot ; parallel ; lowerToC             */
+  ELV_BF_NUM_VARIANTS = 4
+};
+int elv_binomial(int variant, const float* img, float* out, int H, int W,
+                 int ld_in, int ld_out, void* stream);
+const char* elv_binomial_variant_name(int variant);
+
 /* Row-sharded GEMM over ndev GPUs in ONE process (mapPar(xo) of the parallel
  * schedule as the shard axis): B is broadcast from devs[0] with
  * NCCL (elv_nccl_init must have been called with the same devices), each

@@ -12,6 +12,7 @@ Contents
     tests/golden/make_golden.py, which imports the reference).
   * `mm_f64`: numpy f64 GEMM for shapes the C loop is too slow for.
   * `bound`/`check`: the parity tolerance of SURVEY.md §8(d).
+  * `bf_interp_f64` / `bf_bound`: the same for the binomial-filter path.
 """
 
 from __future__ import annotations
@@ -48,6 +49,10 @@ def _load():
             f = getattr(lib, fn)
             f.restype = None
             f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3
+        for fn in ("oracle_bf_naive_f64", "oracle_bf_separated_f64"):
+            f = getattr(lib, fn)
+            f.restype = None
+            f.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int] * 2
         _lib = lib
     return _lib
 
@@ -68,6 +73,29 @@ def mm_interp_f64(A, B, schedule: str = "baseline") -> np.ndarray:
     if schedule not in SCHEDULES:
         raise KeyError(schedule)
     return _call("oracle_mm_seq_f64", A, B)
+
+
+def bf_interp_f64(img, schedule: str = "naive") -> np.ndarray:
+    """What interp.run(binomial_schedule(bf), [img]) returns, bit-exactly."""
+    img = np.ascontiguousarray(img, np.float32)
+    H, W = img.shape
+    out = np.empty((H, W), np.float64)
+    fn = {"naive": "oracle_bf_naive_f64", "naivePar": "oracle_bf_naive_f64",
+          "separated": "oracle_bf_separated_f64", "separatedPar": "oracle_bf_separated_f64"}[schedule]
+    getattr(_load(), fn)(img.ctypes.data, out.ctypes.data, H, W)
+    return out
+
+
+def bf_bound(img, tau: float = 1.0) -> np.ndarray:
+    """fp32 tolerance for the 9-tap stencil: tau * 9 * 2^-24 * (|w| * |img|)
+    (the deterministic gamma_n bound for <= 12 roundings of non-negative
+    weights; the weights sum to 1)."""
+    a = np.abs(np.asarray(img, np.float64))
+    p = np.pad(a, 1, mode="edge")
+    H, W = a.shape
+    w = np.array([[1, 2, 1], [2, 4, 2], [1, 2, 1]]) / 16.0
+    mag = sum(w[i, j] * p[i:i + H, j:j + W] for i in range(3) for j in range(3))
+    return tau * 9 * 2.0 ** -24 * mag
 
 
 def absprod(A, B) -> np.ndarray:

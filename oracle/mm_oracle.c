@@ -64,3 +64,38 @@ void oracle_absprod_f64(const float* A, const float* B, double* C, int M, int N,
   }
   free(bt);
 }
+
+/* Binomial filter: what interp.run returns for the
+ * naive term -- dot(join(w2d), join(nbh)) folded left over the 9 taps in
+ * row-major order from 0.0 -- and for the separated term (separateDot,
+ * rules.py:485-513): h_r = ((0 + 1 x_r0) + 2 x_r1) + 1 x_r2 per window row,
+ * out = ((0 + w0 h_0) + w1 h_1) + w0 h_2.  Borders clamp (padClamp,
+ * interp.py:127-132).  The par schedules evaluate identically. */
+static int clampi(int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
+
+void oracle_bf_naive_f64(const float* img, double* out, int H, int W) {
+  static const double w[9] = {0.0625, 0.125, 0.0625, 0.125, 0.25, 0.125, 0.0625, 0.125, 0.0625};
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < W; ++j) {
+      double acc = 0.0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          acc = acc + w[3 * a + b] * (double)img[(size_t)clampi(i + a - 1, H - 1) * W + clampi(j + b - 1, W - 1)];
+      out[(size_t)i * W + j] = acc;
+    }
+}
+
+void oracle_bf_separated_f64(const float* img, double* out, int H, int W) {
+  static const double wh[3] = {1.0, 2.0, 1.0}, wv[3] = {0.0625, 0.125, 0.0625};
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < W; ++j) {
+      double acc = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        const float* row = img + (size_t)clampi(i + a - 1, H - 1) * W;
+        double h = 0.0;
+        for (int b = 0; b < 3; ++b) h = h + wh[b] * (double)row[clampi(j + b - 1, W - 1)];
+        acc = acc + wv[a] * h;
+      }
+      out[(size_t)i * W + j] = acc;
+    }
+}

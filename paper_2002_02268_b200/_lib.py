@@ -22,7 +22,7 @@ EXPORTS = (
     "elv_nccl_destroy", "elv_gemm_rowshard", "elv_last_error", "elv_abi_version",
     "elv_variant_name", "elv_tf32x3_a_planes_bytes", "elv_tf32x3_b_planes_bytes",
     "elv_tf32x3_split_a", "elv_tf32x3_split_b", "elv_tf32x3_split_b_packed",
-    "elv_tf32x3_gemm_planes",
+    "elv_tf32x3_gemm_planes", "elv_binomial", "elv_binomial_variant_name",
 )
 
 _lib = None
@@ -63,6 +63,8 @@ def load():
         "elv_tf32x3_split_b": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
         "elv_tf32x3_split_b_packed": (c_int, [c_vp, c_int, c_int, c_vp, c_vp]),
         "elv_tf32x3_gemm_planes": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
+        "elv_binomial": (c_int, [c_int, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
+        "elv_binomial_variant_name": (ctypes.c_char_p, [c_int]),
         "elv_last_error": (ctypes.c_char_p, []),
         "elv_abi_version": (c_int, []),
         "elv_variant_name": (ctypes.c_char_p, [c_int]),

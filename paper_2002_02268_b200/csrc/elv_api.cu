@@ -303,6 +303,21 @@ int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
   return tf32x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
 }
 
+const char* elv_binomial_variant_name(int v) {
+  static const char* names[ELV_BF_NUM_VARIANTS] = {"naive", "naivePar", "separated", "separatedPar"};
+  return (v >= 0 && v < ELV_BF_NUM_VARIANTS) ? names[v] : "unknown";
+}
+
+int elv_binomial(int variant, const float* img, float* out, int H, int W, int ld_in, int ld_out,
+                 void* stream) {
+  if (bad_ptr(img) || bad_ptr(out)) return set_error(ELV_EINVAL, "binomial: null pointer");
+  if (H < 1 || W < 1 || ld_in < W || ld_out < W)
+    return set_error(ELV_EINVAL, "binomial: bad shape (H=%d W=%d ld_in=%d ld_out=%d)", H, W, ld_in, ld_out);
+  if (variant < 0 || variant >= ELV_BF_NUM_VARIANTS)
+    return set_error(ELV_EVARIANT, "binomial: unknown variant %d", variant);
+  return launch_binomial(variant, img, out, H, W, ld_in, ld_out, (cudaStream_t)stream);
+}
+
 int elv_nccl_init(int ndev, const int* devs) {
   std::lock_guard<std::mutex> lk(g_nccl_mu);
   if (ndev < 1 || devs == nullptr) return set_error(ELV_EINVAL, "nccl_init: bad device list");

@@ -53,4 +53,8 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
                        cudaStream_t st);
 int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st);
 
+// binomial filter (stencil.cu)
+int launch_binomial(int variant, const float* img, float* out, int H, int W, int ldi, int ldo,
+                    cudaStream_t st);
+
 }  // namespace elv

@@ -225,6 +225,26 @@ class HostPipeline:
 _PIPELINE_MIN_BYTES = 64 << 20
 
 
+def _run_binomial(e, img, device=None):
+    """The one-argument programs: the binomial-filter schedules (binomial.py)."""
+    from . import binomial
+    variant, H, W = binomial.decode(e)
+    kind = type(img)
+    t = _as_host_f32(img)
+    if t.dim() != 2 or tuple(t.shape) != (H, W):
+        raise EvalError(f"the term is typed for a {H}x{W} image, got {tuple(t.shape)}")
+    if device is None:
+        device = t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    src = t.to(device, torch.float32).contiguous()
+    out = torch.empty_like(src)
+    binomial.launch(variant, src, out)
+    if kind is list:
+        return out.double().cpu().tolist()
+    if kind is np.ndarray:
+        return out.cpu().numpy()
+    return out if t.is_cuda else out.cpu()
+
+
 def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     """Evaluate the scheduled mm program `e` applied to `[A, B]` on a B200.
 
@@ -235,6 +255,8 @@ def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     pinned host memory -- the result is written into and returned.  Large
     host-resident problems go through `HostPipeline` (transfers overlapped
     with the kernel)."""
+    if len(args) == 1:
+        return _run_binomial(e, args[0], device)
     if len(args) != 2:
         raise EvalError(f"the mm program takes 2 arguments, got {len(args)}")
     kinds = [type(a) for a in args]

@@ -60,6 +60,26 @@ def run_case(name, sched, M, N, K, seed=7):
             "macs": Mp * Np * Kp}
 
 
+BF_CASES = [(1, 1), (2, 3), (7, 9), (24, 40)]
+
+
+def run_bf_cases():
+    """Binomial-filter schedules through the reference interpreter."""
+    from paper_2002_02268_b200 import binomial
+    s = S()
+    out = []
+    for H, W in BF_CASES:
+        img = synth.matrix(H, W, 9, 2)
+        res = {}
+        for name in binomial.SCHEDULE_NAMES:
+            t = binomial.apply(name, H, W)
+            res[name] = np.array(s.interp.run(t, [img.tolist()]), np.float64)
+        fname = f"bf_{H}x{W}"
+        np.savez_compressed(os.path.join(HERE, f"{fname}.npz"), img=img, **res)
+        out.append({"name": fname, "H": H, "W": W, "seed": 9})
+    return out
+
+
 def kats():
     """Known answers from the reference SPEC, evaluated by the interpreter."""
     s = S()
@@ -73,7 +93,7 @@ def kats():
 
 
 def main():
-    meta = {"cases": [], "kats": kats()}
+    meta = {"cases": [], "kats": kats(), "bf_cases": run_bf_cases()}
     for c in CASES:
         info = run_case(*c)
         print(info, flush=True)
