@@ -72,10 +72,23 @@ constexpr int BAND = 32, BCOLS = 256;
 
 __device__ __forceinline__ void stage_halo(float (*tile)[BCOLS + 2], const float* __restrict__ img, int H,
                                            int W, int ldi, int r0, int c0) {
-  for (int e = threadIdx.x; e < (BAND + 2) * (BCOLS + 2); e += blockDim.x) {
-    const int rr = e / (BCOLS + 2), cc = e - rr * (BCOLS + 2);
-    const int gi = clampi(r0 + rr - 1, H - 1), gj = clampi(c0 + cc - 1, W - 1);
-    tile[rr][cc] = __ldg(img + (size_t)gi * ldi + gj);
+  // thread t stages global column c0 + t into tile column t + 1 for all
+  // BAND + 2 rows (one coalesced load per row, all rows in flight); threads
+  // 0 and 1 also stage the left / right halo columns.  Clamping = padClamp.
+  const int t = threadIdx.x;
+  const int gj = clampi(c0 + t, W - 1);
+  const int hj = t == 0 ? clampi(c0 - 1, W - 1) : clampi(c0 + BCOLS, W - 1);
+  float v[BAND + 2], hv[BAND + 2];
+#pragma unroll
+  for (int rr = 0; rr < BAND + 2; ++rr) {
+    const float* row = img + (size_t)clampi(r0 + rr - 1, H - 1) * ldi;
+    v[rr] = __ldg(row + gj);
+    if (t < 2) hv[rr] = __ldg(row + hj);
+  }
+#pragma unroll
+  for (int rr = 0; rr < BAND + 2; ++rr) {
+    tile[rr][t + 1] = v[rr];
+    if (t < 2) tile[rr][t == 0 ? 0 : BCOLS + 1] = hv[rr];
   }
 }
 
