@@ -439,7 +439,7 @@ def main():
     # the GEMM launch here runs for tens of ms under the 1 kW cap: sustained denominator
     peak, bound, note = roofline_peak(args.variant, peaks, n_sms, cublas, sustained=True)
     achieved = 2.0 * sh.rows * N * K / (comp_ms * 1e-3) / 1e12
-    kernel = {"parallel_tf32x3": "k7_tf32x3", "parallel": "k6_sgemm_8x16"}.get(args.variant, args.variant)
+    kernel = {"parallel_tf32x3": "k7_tf32x3_pair<32>", "parallel": "k6_sgemm_cp<2>"}.get(args.variant, args.variant)
     roof = {"bound": "tensor" if bound == "tensor" else "fp32-simt", "achieved": achieved,
             "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic_from_profiles(f"{kernel}@{sh.rows}x{N}x{K}"),

@@ -399,7 +399,8 @@ template <int BKT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-               float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group) {
+               float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
+               unsigned int* __restrict__ wave_ctr) {
   constexpr int P_STAGES = PairCfg<BKT>::STAGES;
   constexpr int P_A_TILE = PairCfg<BKT>::A_TILE;
   constexpr int P_B_TILE = PairCfg<BKT>::B_TILE;
@@ -455,9 +456,11 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       // ---------------- TMA producer (both CTAs) ----------------
       const uint32_t full0 = mapa_rank(smem_u32(&full[0]), 0);
       int s = 0; uint32_t ph = 0;
-      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      int wave = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters, ++wave) {
         int m0, n0;
         coords(t, m0, n0);
+        if (wave_ctr != nullptr && wave > 0) wave_sync_wait(wave_ctr, (unsigned)(wave * gridDim.x));
         const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (P_BN / 2);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -471,6 +474,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           tma_load_2d_pair(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb);
           if (++s == P_STAGES) { s = 0; ph ^= 1; }
         }
+        if (wave_ctr != nullptr) atomicAdd(wave_ctr, 1u);
       }
     }
   } else if (warp == 1) {
@@ -664,15 +668,21 @@ static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
-// ELV_TF32X3_PAIR: 0 = 1-CTA kernel, 16 / 32 = cta_group::2 kernel with that BK
-static int pair_mode() {
-  static int v = -1;
-  if (v < 0) {
-    v = env_int("ELV_TF32X3_PAIR", 0);
-    if (v == 1) v = 16;
-    if (v != 0 && v != 16 && v != 32) v = 0;
+// Kernel choice.  Default: the cta_group::2 kernel with BK=32 (128B swizzle)
+// when there are at least as many 256x256 pair tiles as SMs (measured at
+// 32768^2 x 8192 under the power cap: 251-256 TF vs 244-245 TF for the 1-CTA
+// kernel, scripts/gpu_pairws.sh), else the 1-CTA kernel (twice the tiles for
+// small problems).  ELV_TF32X3_PAIR=0 / 16 / 32 forces a choice.
+static int pair_mode(int M, int N) {
+  static int forced = -2;
+  if (forced == -2) {
+    forced = env_int("ELV_TF32X3_PAIR", -1);
+    if (forced == 1) forced = 16;
+    if (forced != -1 && forced != 0 && forced != 16 && forced != 32) forced = -1;
   }
-  return v;
+  if (forced >= 0) return forced;
+  const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
+  return pair_tiles >= num_sms() ? 32 : 0;
 }
 // per-device wave counter (library-internal scratch, 4 bytes), zeroed on the
 // launch stream before every launch; ELV_WAVE_SYNC=0 disables the sync.
@@ -723,8 +733,9 @@ static int launch_pair(const CUtensorMap& m_ahi_unused, const float* a_hi, const
   const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
+  unsigned int* ctr = wave_counter(dev, st);
   k7_tf32x3_pair<BKT><<<2 * clusters, NUM_THREADS, PairCfg<BKT>::SMEM_BYTES, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT, with_lolo(K), tile_group(8));
+      ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT, with_lolo(K), tile_group(8), ctr);
   return check_launch("gemm_parallel_tf32x3_pair");
 }
 static inline size_t planes_bytes(int rows, int K) {
@@ -784,8 +795,9 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
     attr_dev = dev;
   }
-  if (pair_mode() == 16) return launch_pair<16>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  if (pair_mode() == 32) return launch_pair<32>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  const int pm = pair_mode(M, N);
+  if (pm == 16) return launch_pair<16>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (pm == 32) return launch_pair<32>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   unsigned int* ctr = wave_counter(dev, st);

@@ -195,3 +195,26 @@ def test_error_vs_k_sweep(cuda, variant):
         Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
         ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
         assert ok, f"{variant} K={K}: worst err/bound = {worst:.3g}"
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3"])
+def test_bench_shape_row_sample(cuda, variant):
+    """configs[3] maximum size (32768 x 32768 x 8192, the bench workload):
+    sampled rows and a column sample against the f64 oracle."""
+    name, tf = _sched(variant)
+    M, N, K = 32768, 32768, 8192
+    A, B = _device_inputs(M, N, K, 0, cuda)
+    term = schedules.apply(name, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf)
+    rows = torch.tensor([0, 255, 256, 16383, 16384, 32511, 32767], device=cuda)
+    cols = torch.tensor([0, 1, 255, 256, 20000, 32767], device=cuda)
+    Bh = B.cpu().numpy()
+    As = A[rows].cpu().numpy()
+    ok, worst = oracle.check(C[rows].cpu().numpy(), oracle.mm_f64(As, Bh), oracle.absprod_np(As, Bh), K)
+    assert ok, f"{variant} rows: worst err/bound = {worst:.3g}"
+    Ah = A.cpu().numpy()
+    Bc = Bh[:, cols.cpu().numpy()]
+    ok, worst = oracle.check(C[:, cols].cpu().numpy(), oracle.mm_f64(Ah, Bc), oracle.absprod_np(Ah, Bc), K)
+    assert ok, f"{variant} cols: worst err/bound = {worst:.3g}"
+    del C
+    torch.cuda.empty_cache()
