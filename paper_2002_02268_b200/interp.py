@@ -168,7 +168,7 @@ class HostPipeline:
         self.p, self.device = p, device
         M = p.M
         if chunk_rows is None:
-            chunk_rows = max(128, -(-M // 16))     # 16 row blocks: shorter fill / drain
+            chunk_rows = max(128, -(-M // 8))
         self.R = -(-chunk_rows // 128) * 128        # multiple of the kernels' row tile
         self.blocks = [(r0, min(r0 + self.R, M)) for r0 in range(0, M, self.R)]
 

@@ -19,3 +19,4 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k6_
   python scripts/profile_one.py --variant parallel --M 32768 --N 32768 --K 8192 --reps 2 > $OUT/prof_k6.log 2>&1; echo "ncu k6 rc=$?" >> $S
 timeout 600 ncu --set full --clock-control none -k regex:k_pack_b -s 1 -c 1 -o $OUT/prof_packb \
   python scripts/profile_one.py --variant parallel --M 8192 --N 32768 --K 8192 --reps 2 > $OUT/prof_packb.log 2>&1; echo "ncu packb rc=$?" >> $S
+timeout 600 python bench.py --workload binomial > $OUT/bench_bf.jsonl 2> $OUT/bench_bf.err; echo "bench bf rc=$?" >> $S
