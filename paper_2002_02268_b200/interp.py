@@ -245,20 +245,55 @@ def _run_binomial(e, img, device=None):
     return out if t.is_cuda else out.cpu()
 
 
-def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
-    """Evaluate the scheduled mm program `e` applied to `[A, B]` on a B200.
+def _no_template(err) -> bool:
+    return str(err).startswith("no B200 kernel for term")
 
-    Mirrors stratir.interp.run (interp.py:157-162).  Host inputs are copied to
-    the GPU, the kernel runs, and the result comes back in the caller's
-    representation (nested lists for lists, numpy for numpy, tensors for
-    tensors).  `out` (optional) is a preallocated M x N fp32 tensor -- e.g.
-    pinned host memory -- the result is written into and returned.  Large
-    host-resident problems go through `HostPipeline` (transfers overlapped
-    with the kernel)."""
+
+def _run_generic(e, args, device=None):
+    """Programs the template dispatch does not recognise: one generated
+    kernel per term (codegen.py, the GPU analogue of SPEC's codegen-c)."""
+    from . import codegen
+    kinds = [type(a) for a in args]
+    ts = [_as_host_f32(a) for a in args]
+    if device is None:
+        cuda_in = [t for t in ts if t.is_cuda]
+        device = cuda_in[0].device if cuda_in else torch.device("cuda", torch.cuda.current_device())
+    try:
+        out = codegen.run(e, [t.to(device, torch.float32) for t in ts])
+    except codegen.CodegenError as err:
+        raise EvalError(f"no B200 kernel for term: {err}") from None
+    if kinds and kinds[0] is list:
+        return out.double().cpu().tolist()
+    if kinds and kinds[0] is np.ndarray:
+        return out.cpu().numpy()
+    return out if (ts and ts[0].is_cuda) else out.cpu()
+
+
+def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
+    """Evaluate the program `e` applied to `args` on a B200.
+
+    Mirrors stratir.interp.run (interp.py:157-162).  The seven GEMM schedules
+    and the four binomial schedules run their hand-written kernels (template
+    dispatch); any other well-typed program over the primitive vocabulary runs
+    a generated kernel (codegen.py).  Host inputs are copied to the GPU and
+    the result comes back in the caller's representation (nested lists for
+    lists, numpy for numpy, tensors for tensors).  `out` (optional, GEMM
+    path) is a preallocated M x N fp32 tensor -- e.g. pinned host memory --
+    the result is written into and returned.  Large host-resident GEMMs go
+    through `HostPipeline` (transfers overlapped with the kernel)."""
+    try:
+        return _run_template(e, args, device=device, tf32x3=tf32x3, out=out)
+    except S().interp.EvalError as err:
+        if not _no_template(err):
+            raise
+        return _run_generic(e, args, device)
+
+
+def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     if len(args) == 1:
         return _run_binomial(e, args[0], device)
     if len(args) != 2:
-        raise EvalError(f"the mm program takes 2 arguments, got {len(args)}")
+        raise EvalError(f"no B200 kernel for term: {len(args)}-argument program")
     kinds = [type(a) for a in args]
     ts = [_as_host_f32(a) for a in args]
     for t in ts:

@@ -1,0 +1,56 @@
+"""GPU: generated kernels (codegen.py) against the reference interpreter
+itself (stratir.interp.run from baseline/_ref, used here only as a checker),
+and the template kernels against the generated ones."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2002_02268_b200 import binomial, codegen, interp, schedules, synth
+from paper_2002_02268_b200._ref import S
+
+from test_codegen import corpus
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(term, seed=3):
+    c = codegen.compile_term(term)
+    return [synth.matrix(*shp, seed, i) if len(shp) == 2 else synth.uniform(shp[0], seed, i)
+            for i, shp in enumerate(c.in_shapes)]
+
+
+@pytest.mark.parametrize("name,term", list(corpus().items()))
+def test_generated_kernel_matches_reference_interpreter(cuda, name, term):
+    s = S()
+    args = _inputs(term)
+    ref = np.array(s.interp.run(term, [a.tolist() for a in args]), np.float64)
+    got = codegen.run(term, [torch.from_numpy(a).to(cuda) for a in args]).cpu().numpy().astype(np.float64)
+    assert got.shape == ref.shape
+    # fp32 with separately rounded ops (--fmad=false) vs the interpreter's
+    # f64: every program here folds at most 64 terms of magnitude <= 4
+    assert np.all(np.abs(got - ref) <= 64 * 4 * 2.0 ** -23), name
+
+
+def test_run_falls_back_to_generated_kernel(cuda):
+    """interp.run: a schedule the templates do not know still runs (on the GPU)."""
+    term = corpus()["user_tile16"]
+    A = synth.matrix(32, 8, 1, 0)
+    B = synth.matrix(8, 48, 1, 1)
+    C = interp.run(term, [A, B])
+    ok, worst = oracle.check(C, oracle.mm_f64(A, B), oracle.absprod_np(A, B), 8)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("name", schedules.SCHEDULE_NAMES)
+def test_template_and_generated_kernels_agree(cuda, name):
+    M, N, K = 64, 96, 64
+    term = schedules.apply(name, M, N, K).term
+    A = torch.from_numpy(synth.matrix(M, K, 2, 0)).to(cuda)
+    B = torch.from_numpy(synth.matrix(K, N, 2, 1)).to(cuda)
+    gen = codegen.run(term, [A, B]).cpu().numpy()
+    tpl = interp.run_tensor(term, A, B).cpu().numpy()
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    ref, ab = oracle.mm_interp_f64(Ah, Bh, name), oracle.absprod_np(Ah, Bh)
+    assert oracle.check(gen, ref, ab, K)[0] and oracle.check(tpl, ref, ab, K)[0]
