@@ -113,6 +113,23 @@ int elv_tf32x3_split_b_packed(const float* packedB, int K, int N, void* b_planes
 int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
                            int M, int N, int K, int ldc, void* stream);
 
+/* Host-resident operands (the reference's own calling convention:
+ * interp.run takes and returns host values, interp.py:157-162).
+ * C_h = A_h . B_h; A_h, B_h, C_h are HOST pointers (pinned for overlap).
+ * The output is cut into R x Nc tiles: B column chunks and A row blocks
+ * cross PCIe on a library H2D stream in first-use order, each tile is
+ * prepared and multiplied on `stream` as soon as its operands arrive, and
+ * returns on a library D2H stream as soon as it is written.  Asynchronous on
+ * `stream` (synchronise it before reading C_h).  Same per-element arithmetic
+ * as elv_gemm.  The device workspace holds A, B, C and the per-tile
+ * prepared operands: size it with elv_gemm_host_workspace_bytes. */
+size_t elv_gemm_host_workspace_bytes(int variant, int M, int N, int K);
+int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h,
+                  int M, int N, int K, int lda, int ldb, int ldc,
+                  void* workspace, size_t workspace_bytes, void* stream);
+/* The tile shape elv_gemm_host uses (rows x cols). */
+int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols);
+
 /* Synthetic inputs: X[i] = U(-1,1) with 24-bit resolution from
  * splitmix64((seed << 48) ^ (tensor_id << 40) ^ (offset + i)); bit-identical
  * to paper_2002_02268_b200.synth.uniform() on the host. */

@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libelevate_b200.so")
-SOURCES = ["elv_api.cu", "simt_gemm.cu", "tf32x3_gemm.cu", "stencil.cu"]
+SOURCES = ["elv_api.cu", "simt_gemm.cu", "tf32x3_gemm.cu", "stencil.cu", "host_pipeline.cu"]
 HEADERS = ["elv_common.cuh", os.path.join("..", "..", "include", "elevate_b200.h")]
 
 NVCC_FLAGS = [

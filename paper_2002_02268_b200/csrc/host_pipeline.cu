@@ -1,0 +1,271 @@
+// Host-resident operands: C_h = A_h . B_h with PCIe traffic overlapped with
+// the GEMM (elv_gemm_host, include/elevate_b200.h).
+//
+// This is the reference's calling convention -- interp.run(e, [A, B]) takes
+// host values and returns a host value (reference pkg/src/stratir/interp.py:
+// 157-162) -- made fast: the output is cut into R x Nc tiles; the H2D stream
+// brings in B column chunks and A row blocks in the order that enables C
+// tiles soonest, the caller's stream prepares (packB / tf32 split) and
+// multiplies each tile as soon as both its operands have landed, and the D2H
+// stream returns each C tile as soon as it is written.  PCIe is full duplex
+// (measured ~55 GB/s each way, ~100 GB/s both), so for large problems the
+// step is bound by the D2H of C (the largest transfer) plus pipeline fill.  Tiles of C are independent (the mapPar axis), and each
+// tile's per-element arithmetic is the single-launch kernel's, so the result
+// equals elv_gemm's.
+
+#include "elv_common.cuh"
+
+#include <stdlib.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+namespace elv {
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+struct HostPlan {
+  int R, Nc, nrb, ncb;
+  bool packed_a;                 // variant 6: pack A per row block (cp.async kernel)
+  size_t off_a, off_b, off_c, off_pa, stride_pa, off_pb, stride_pb, total;
+};
+
+// Tile sizes.  Small problems: one tile (plain H2D -> GEMM -> D2H).  Large:
+// 8-16 row blocks (multiples of the 256-row pair tile) x column chunks of
+// about 8192 columns (multiples of 256), so the first C tile is ready after
+// a small slice of A and one chunk of B have crossed PCIe and each GEMM
+// launch still fills several waves of the persistent grid.  Measured at
+// 32768 x 32768 x 8192 (3xTF32, gpurun_out/s2d): 2048x8192 and 4096x4096
+// tiles 97.6-98.1 ms, 4096x8192 100.6 ms, 8192x8192 102.1 ms; the D2H of C
+// (4 GiB at ~50 GB/s while H2D runs) is the bound.
+HostPlan make_plan(int v, int M, int N, int K) {
+  HostPlan p{};
+  const double bytes = 4.0 * ((double)M * K + (double)K * N + (double)M * N);
+  p.R = M;
+  p.Nc = N;
+  if (bytes >= (double)(64 << 20)) {
+    const int row_blocks = M >= 8192 ? 16 : (M >= 2048 ? 8 : (M >= 512 ? 2 : 1));
+    p.R = (int)up((size_t)ceil_div(M, row_blocks), 256);
+    if (p.R > M) p.R = M;
+    if (N >= 16384) {
+      const int chunks = ceil_div(N, 8192);
+      p.Nc = (int)up((size_t)ceil_div(N, chunks), 256);
+      if (p.Nc > N) p.Nc = N;
+    }
+  }
+  // test hook: ELV_HOST_TILES="R,Nc" forces the tile shape (read per call)
+  if (const char* t = getenv("ELV_HOST_TILES")) {
+    int r = 0, c = 0;
+    if (sscanf(t, "%d,%d", &r, &c) == 2 && r > 0 && c > 0) {
+      p.R = r < M ? r : M;
+      p.Nc = c < N ? c : N;
+    }
+  }
+  p.nrb = ceil_div(M, p.R);
+  p.ncb = ceil_div(N, p.Nc);
+  p.packed_a = v == ELV_PARALLEL && parallel_uses_packed_a(p.R, p.Nc);
+  size_t o = 0;
+  p.off_a = o;  o = up(o + (size_t)M * K * 4, kAlign);
+  p.off_b = o;  o = up(o + (size_t)K * N * 4, kAlign);
+  p.off_c = o;  o = up(o + (size_t)M * N * 4, kAlign);
+  p.stride_pa = 0;
+  if (v == ELV_PARALLEL_TF32X3) p.stride_pa = up(tf32x3_a_planes_bytes(p.R, K), kAlign);
+  else if (p.packed_a) p.stride_pa = up(pack_a_bytes(p.R, K), kAlign);
+  p.off_pa = o;  o += p.stride_pa * p.nrb;
+  p.stride_pb = 0;
+  if (v == ELV_PARALLEL_TF32X3) p.stride_pb = up(tf32x3_b_planes_bytes(p.Nc, K), kAlign);
+  else if (v >= ELV_ARRAYPACKING) p.stride_pb = up(elv_pack_b_bytes(K, p.Nc), kAlign);
+  p.off_pb = o;  o += p.stride_pb * p.ncb;
+  p.total = o + kAlign;   // slack for aligning the caller's base pointer
+  return p;
+}
+
+// Per-device copy streams and an event pool (library-internal, created once).
+struct DeviceRes {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> events;
+  std::mutex mu;
+};
+DeviceRes g_res[64];
+
+int get_events(DeviceRes& r, size_t n) {
+  while (r.events.size() < n) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(ELV_ECUDA, "gemm_host: cudaEventCreate: %s", cudaGetErrorString(cudaGetLastError()));
+    r.events.push_back(e);
+  }
+  return ELV_OK;
+}
+
+#define CK(call, what)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return set_error(ELV_ECUDA, "gemm_host: %s: %s", what, cudaGetErrorString(e_)); \
+  } while (0)
+
+}  // namespace
+}  // namespace elv
+
+using namespace elv;
+
+extern "C" {
+
+size_t elv_gemm_host_workspace_bytes(int variant, int M, int N, int K) {
+  if (M < 1 || N < 1 || K < 1 || variant < 0 || variant >= ELV_NUM_VARIANTS) return 0;
+  return make_plan(variant, M, N, K).total;
+}
+
+int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols) {
+  if (M < 1 || N < 1 || K < 1 || variant < 0 || variant >= ELV_NUM_VARIANTS)
+    return set_error(ELV_EINVAL, "gemm_host_tiles: bad arguments");
+  const HostPlan p = make_plan(variant, M, N, K);
+  if (rows) *rows = p.R;
+  if (cols) *cols = p.Nc;
+  return ELV_OK;
+}
+
+int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, int M, int N, int K,
+                  int lda, int ldb, int ldc, void* workspace, size_t workspace_bytes, void* stream) {
+  if (A_h == nullptr || B_h == nullptr || C_h == nullptr)
+    return set_error(ELV_EINVAL, "gemm_host: null matrix pointer");
+  if (M < 1 || N < 1 || K < 1)
+    return set_error(ELV_EINVAL, "gemm_host: sizes must be positive (M=%d N=%d K=%d)", M, N, K);
+  if (lda < K || ldb < N || ldc < N)
+    return set_error(ELV_EINVAL, "gemm_host: leading dimension too small (lda=%d ldb=%d ldc=%d)", lda, ldb, ldc);
+  if (variant < 0 || variant >= ELV_NUM_VARIANTS) return set_error(ELV_EVARIANT, "unknown variant %d", variant);
+  const HostPlan p = make_plan(variant, M, N, K);
+  if (workspace == nullptr || workspace_bytes < p.total)
+    return set_error(ELV_EWORKSPACE, "gemm_host: needs %zu workspace bytes, got %zu", p.total, workspace_bytes);
+  int dev = 0;
+  CK(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return set_error(ELV_EINVAL, "gemm_host: device %d out of range", dev);
+  DeviceRes& r = g_res[dev];
+  std::lock_guard<std::mutex> lk(r.mu);
+  if (r.h2d == nullptr) {
+    CK(cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking), "create h2d stream");
+    CK(cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking), "create d2h stream");
+  }
+  const int ntiles = p.nrb * p.ncb;
+  // events: [0] entry, [1] h2d done, [2 .. 2+nrb) A blocks, [.. +ncb) B chunks, [.. +ntiles) tiles
+  int rc = get_events(r, 2 + p.nrb + p.ncb + ntiles);
+  if (rc) return rc;
+  cudaEvent_t* ev = r.events.data();
+  cudaEvent_t ev_entry = ev[0], ev_end = ev[1];
+  cudaEvent_t* ev_a = ev + 2;
+  cudaEvent_t* ev_b = ev_a + p.nrb;
+  cudaEvent_t* ev_t = ev_b + p.ncb;
+
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* base = reinterpret_cast<uint8_t*>(up(reinterpret_cast<uintptr_t>(workspace), kAlign));
+  float* A_d = reinterpret_cast<float*>(base + p.off_a);
+  float* B_d = reinterpret_cast<float*>(base + p.off_b);
+  float* C_d = reinterpret_cast<float*>(base + p.off_c);
+  auto prep_a = [&](int i) { return base + p.off_pa + p.stride_pa * i; };
+  auto prep_b = [&](int j) { return base + p.off_pb + p.stride_pb * j; };
+
+  // the copy streams start after everything already queued on the caller's stream
+  CK(cudaEventRecord(ev_entry, st), "record entry");
+  CK(cudaStreamWaitEvent(r.h2d, ev_entry, 0), "h2d wait entry");
+  CK(cudaStreamWaitEvent(r.d2h, ev_entry, 0), "d2h wait entry");
+
+  // H2D order: start with B chunk 0 and A block 0, then repeatedly bring
+  // whichever operand enables more new C tiles per byte (an A block enables
+  // one tile per B chunk already present and vice versa), so the GEMM and the
+  // D2H stream get work as early as PCIe allows.
+  struct Item { bool is_b; int idx; };
+  std::vector<Item> order;
+  std::vector<int> pos_a(p.nrb), pos_b(p.ncb);
+  {
+    int na = 0, nb = 0;
+    const double a_bytes = (double)p.R * K, b_bytes = (double)K * p.Nc;
+    while (na < p.nrb || nb < p.ncb) {
+      bool take_b;
+      if (nb == 0) take_b = true;
+      else if (na == 0) take_b = false;
+      else if (na == p.nrb) take_b = true;
+      else if (nb == p.ncb) take_b = false;
+      else take_b = (double)na / b_bytes > (double)nb / a_bytes;
+      if (take_b) { pos_b[nb] = (int)order.size(); order.push_back({true, nb++}); }
+      else { pos_a[na] = (int)order.size(); order.push_back({false, na++}); }
+    }
+  }
+  for (const Item& it : order) {
+    if (it.is_b) {
+      const int c0 = it.idx * p.Nc, nc = N - c0 < p.Nc ? N - c0 : p.Nc;
+      CK(cudaMemcpy2DAsync(B_d + c0, (size_t)N * 4, B_h + c0, (size_t)ldb * 4, (size_t)nc * 4, K,
+                           cudaMemcpyHostToDevice, r.h2d), "H2D B chunk");
+      CK(cudaEventRecord(ev_b[it.idx], r.h2d), "record B chunk");
+    } else {
+      const int r0 = it.idx * p.R, nr = M - r0 < p.R ? M - r0 : p.R;
+      CK(cudaMemcpy2DAsync(A_d + (size_t)r0 * K, (size_t)K * 4, A_h + (size_t)r0 * lda, (size_t)lda * 4,
+                           (size_t)K * 4, nr, cudaMemcpyHostToDevice, r.h2d), "H2D A block");
+      CK(cudaEventRecord(ev_a[it.idx], r.h2d), "record A block");
+    }
+  }
+
+  // tiles in the order their operands land (ties: row-major)
+  std::vector<int> tiles(ntiles);
+  for (int t = 0; t < ntiles; ++t) tiles[t] = t;
+  std::stable_sort(tiles.begin(), tiles.end(), [&](int x, int y) {
+    const int rx = std::max(pos_a[x / p.ncb], pos_b[x % p.ncb]);
+    const int ry = std::max(pos_a[y / p.ncb], pos_b[y % p.ncb]);
+    return rx < ry;
+  });
+
+  // prepare + multiply tile by tile on the caller's stream
+  std::vector<char> have_a(p.nrb, 0), have_b(p.ncb, 0);
+  for (int t : tiles) {
+    const int i = t / p.ncb, j = t % p.ncb;
+    const int r0 = i * p.R, nr = M - r0 < p.R ? M - r0 : p.R;
+    const int c0 = j * p.Nc, nc = N - c0 < p.Nc ? N - c0 : p.Nc;
+    const float* Ai = A_d + (size_t)r0 * K;
+    if (!have_b[j]) {
+      CK(cudaStreamWaitEvent(st, ev_b[j], 0), "wait B chunk");
+      if (variant == ELV_PARALLEL_TF32X3) rc = tf32x3_split_b(B_d + c0, K, nc, N, false, prep_b(j), st);
+      else if (variant >= ELV_ARRAYPACKING) rc = launch_pack_b(B_d + c0, reinterpret_cast<float*>(prep_b(j)), K, nc, N, st);
+      if (rc) return rc;
+      have_b[j] = 1;
+    }
+    if (!have_a[i]) {
+      CK(cudaStreamWaitEvent(st, ev_a[i], 0), "wait A block");
+      if (variant == ELV_PARALLEL_TF32X3) rc = tf32x3_split_a(Ai, nr, K, K, prep_a(i), st);
+      else if (p.packed_a) rc = launch_pack_a(Ai, reinterpret_cast<float*>(prep_a(i)), nr, K, K, st);
+      if (rc) return rc;
+      have_a[i] = 1;
+    }
+    float* Cij = C_d + (size_t)r0 * N + c0;
+    if (variant == ELV_PARALLEL_TF32X3) {
+      rc = tf32x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st);
+    } else if (variant == ELV_PARALLEL && p.packed_a && parallel_uses_packed_a(nr, nc)) {
+      rc = launch_parallel_packed(reinterpret_cast<const float*>(prep_a(i)),
+                                  reinterpret_cast<const float*>(prep_b(j)), Cij, nr, nc, K, N, st);
+    } else if (variant >= ELV_ARRAYPACKING) {
+      rc = launch_simt(variant, Ai, nullptr, reinterpret_cast<const float*>(prep_b(j)), Cij, nr, nc, K, K, 0,
+                       N, st);
+    } else {
+      rc = launch_simt(variant, Ai, B_d + c0, nullptr, Cij, nr, nc, K, K, N, N, st);
+    }
+    if (rc) return rc;
+    CK(cudaEventRecord(ev_t[t], st), "record tile");
+  }
+
+  // D2H each tile as soon as it is written
+  for (int t : tiles) {
+    const int i = t / p.ncb, j = t % p.ncb;
+    const int r0 = i * p.R, nr = M - r0 < p.R ? M - r0 : p.R;
+    const int c0 = j * p.Nc, nc = N - c0 < p.Nc ? N - c0 : p.Nc;
+    CK(cudaStreamWaitEvent(r.d2h, ev_t[t], 0), "d2h wait tile");
+    CK(cudaMemcpy2DAsync(C_h + (size_t)r0 * ldc + c0, (size_t)ldc * 4, C_d + (size_t)r0 * N + c0,
+                         (size_t)N * 4, (size_t)nc * 4, nr, cudaMemcpyDeviceToHost, r.d2h), "D2H C tile");
+  }
+  CK(cudaEventRecord(ev_end, r.d2h), "record end");
+  CK(cudaStreamWaitEvent(st, ev_end, 0), "join d2h");
+  return ELV_OK;
+}
+
+}  // extern "C"

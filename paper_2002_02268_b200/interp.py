@@ -21,6 +21,7 @@ SURVEY.md §8(d) (see `tolerance.py`).
 
 from __future__ import annotations
 
+import ctypes
 import os
 import weakref
 
@@ -153,73 +154,57 @@ def _as_host_f32(x):
 
 
 class HostPipeline:
-    """Host-resident A, B -> host C with the transfers overlapped.
+    """Host-resident A, B -> host C with the transfers overlapped: a thin
+    binding of the C-ABI host pipeline `elv_gemm_host` (csrc/host_pipeline.cu).
 
-    B goes to the device first (every row block needs all of it) and is
-    prepared once (packB / tf32 split).  A and C move in row blocks: block i+1
-    is copied in on one stream while block i is multiplied on the compute
-    stream and block i-1 is copied out on a third stream (PCIe is full
-    duplex).  Row blocks of C are independent (the mapPar axis), and the
-    per-row arithmetic is the single-launch kernel's, so the result is
-    bit-identical to `gemm`."""
+    The output is cut into R x Nc tiles; B column chunks and A row blocks
+    cross PCIe on the library's H2D stream in first-use order, each tile is
+    prepared (packB / tf32 split) and multiplied on the compute stream as soon
+    as its operands land, and goes back on the D2H stream as soon as it is
+    written (PCIe is full duplex).  Tiles of C are independent (the mapPar
+    axis) and each tile's per-element arithmetic is the single-launch
+    kernel's, so the result is bit-identical to `gemm`.  The device workspace
+    (A, B, C and the prepared operands) is torch-owned and cached here."""
 
-    def __init__(self, p: dispatch.KernelPlan, device, chunk_rows: int | None = None):
+    def __init__(self, p: dispatch.KernelPlan, device):
         self.lib = _lib.load()
         self.p, self.device = p, device
-        M = p.M
-        if chunk_rows is None:
-            chunk_rows = max(128, -(-M // 8))
-        self.R = -(-chunk_rows // 128) * 128        # multiple of the kernels' row tile
-        self.blocks = [(r0, min(r0 + self.R, M)) for r0 in range(0, M, self.R)]
+        self.ws_bytes = self.lib.elv_gemm_host_workspace_bytes(p.variant, p.M, p.N, p.K)
+        self.ws = torch.empty(self.ws_bytes, device=device, dtype=torch.uint8)
+        r, c = ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.elv_gemm_host_tiles(p.variant, p.M, p.N, p.K, ctypes.byref(r),
+                                                ctypes.byref(c)), "elv_gemm_host_tiles")
+        self.tile = (r.value, c.value)
 
-    def __call__(self, A_h: torch.Tensor, B_h: torch.Tensor, out_h: torch.Tensor) -> torch.Tensor:
-        p, lib, dev = self.p, self.lib, self.device
-        M, N, K, v = p.M, p.N, p.K, p.variant
-        comp = torch.cuda.current_stream(dev)
-        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        A_d = torch.empty((M, K), device=dev)
-        B_d = torch.empty((K, N), device=dev)
-        C_d = torch.empty((M, N), device=dev)
-        ev_b = torch.cuda.Event()
-        ev_a = [torch.cuda.Event() for _ in self.blocks]
-        ev_c = [torch.cuda.Event() for _ in self.blocks]
-        with torch.cuda.stream(s_in):
-            B_d.copy_(B_h, non_blocking=True)
-            ev_b.record(s_in)
-            for (r0, r1), ev in zip(self.blocks, ev_a):
-                A_d[r0:r1].copy_(A_h[r0:r1], non_blocking=True)
-                ev.record(s_in)
-        st = comp.cuda_stream
-        comp.wait_event(ev_b)
-        ws = None
-        if v in (4, 5, 6):
-            ws = torch.empty(lib.elv_pack_b_bytes(K, N), device=dev, dtype=torch.uint8)
-            _lib.check(lib.elv_pack_b(B_d.data_ptr(), ws.data_ptr(), K, N, N, 32, st), "elv_pack_b")
-        elif v == 7:
-            ws = torch.empty(lib.elv_tf32x3_b_planes_bytes(N, K), device=dev, dtype=torch.uint8)
-            a_pl = torch.empty(lib.elv_tf32x3_a_planes_bytes(self.R, K), device=dev, dtype=torch.uint8)
-            _lib.check(lib.elv_tf32x3_split_b(B_d.data_ptr(), K, N, N, ws.data_ptr(), st), "split_b")
-        for (r0, r1), ea, ec in zip(self.blocks, ev_a, ev_c):
-            comp.wait_event(ea)
-            rows = r1 - r0
-            a_ptr = A_d.data_ptr() + 4 * r0 * K
-            c_ptr = C_d.data_ptr() + 4 * r0 * N
-            if v in (4, 5, 6):
-                rc = lib.elv_gemm_prepacked(v, a_ptr, ws.data_ptr(), c_ptr, rows, N, K, K, N, st)
-            elif v == 7:
-                _lib.check(lib.elv_tf32x3_split_a(a_ptr, rows, K, K, a_pl.data_ptr(), st), "split_a")
-                rc = lib.elv_tf32x3_gemm_planes(a_pl.data_ptr(), ws.data_ptr(), c_ptr, rows, N, K, N, st)
-            else:
-                rc = lib.elv_gemm_compute(v, a_ptr, B_d.data_ptr(), c_ptr, rows, N, K, K, N, N, None, 0, st)
-            _lib.check(rc, f"row block {r0}:{r1}")
-            ec.record(comp)
-        with torch.cuda.stream(s_out):
-            for (r0, r1), ec in zip(self.blocks, ev_c):
-                s_out.wait_event(ec)
-                out_h[r0:r1].copy_(C_d[r0:r1], non_blocking=True)
-        s_out.synchronize()
-        comp.synchronize()
+    def __call__(self, A_h: torch.Tensor, B_h: torch.Tensor, out_h: torch.Tensor,
+                 sync: bool = True) -> torch.Tensor:
+        p = self.p
+        for t, shape in ((A_h, (p.M, p.K)), (B_h, (p.K, p.N)), (out_h, (p.M, p.N))):
+            if t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != shape or t.stride(-1) != 1:
+                raise EvalError(f"host pipeline expects row-major fp32 host matrices {shape}")
+        st = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            rc = self.lib.elv_gemm_host(p.variant, A_h.data_ptr(), B_h.data_ptr(), out_h.data_ptr(),
+                                        p.M, p.N, p.K, A_h.stride(0), B_h.stride(0), out_h.stride(0),
+                                        self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
+        _lib.check(rc, f"elv_gemm_host[{p.variant_name}]")
+        if sync:
+            st.synchronize()
         return out_h
+
+
+_host_pipes: dict = {}
+
+
+def host_pipeline(p: dispatch.KernelPlan, device) -> HostPipeline:
+    """One cached HostPipeline (and its device workspace) per plan and device."""
+    key = (p.variant, p.M, p.N, p.K, str(device))
+    hp = _host_pipes.get(key)
+    if hp is None:
+        if len(_host_pipes) >= 4:
+            _host_pipes.clear()
+        hp = _host_pipes[key] = HostPipeline(p, device)
+    return hp
 
 
 _PIPELINE_MIN_BYTES = 64 << 20
@@ -311,7 +296,7 @@ def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out
         dst = out if out is not None else torch.empty((p.M, p.N), dtype=torch.float32,
                                                       pin_memory=A_h.is_pinned())
         with torch.cuda.device(device):
-            HostPipeline(p, device)(A_h, B_h, dst)
+            host_pipeline(p, device)(A_h, B_h, dst)
         if kinds[0] is list:
             return dst.double().tolist()
         if kinds[0] is np.ndarray:

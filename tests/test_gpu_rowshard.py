@@ -16,6 +16,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import oracle
+
 from paper_2002_02268_b200 import dispatch, distributed as D, interp, schedules, synth
 
 pytestmark = pytest.mark.gpu
@@ -96,28 +98,55 @@ def test_two_ranks_share_one_gpu_over_gloo(cuda, variant):
     assert np.array_equal(C, ref)
 
 
-@pytest.mark.parametrize("variant", ["baseline", "loopPerm", "parallel", "parallel_tf32x3"])
-def test_host_pipeline_bitwise_equals_device_path(cuda, variant):
-    """interp.run on host tensors large enough for HostPipeline (row blocks with
-    overlapped H2D / GEMM / D2H) returns exactly the single-launch result."""
+@pytest.mark.parametrize("tiles", [None, "384,1280"])
+@pytest.mark.parametrize("variant", ["baseline", "loopPerm", "arrayPacking", "parallel", "parallel_tf32x3"])
+def test_host_pipeline_bitwise_equals_device_path(cuda, variant, tiles, monkeypatch):
+    """interp.run on host tensors through the C-ABI host pipeline
+    (elv_gemm_host: tiles of C with overlapped H2D / GEMM / D2H) returns
+    exactly the single-launch result -- with the default tiling and with a
+    forced 384 x 1280 tiling that leaves ragged row and column tails."""
     sched, tf = ("parallel", True) if variant == "parallel_tf32x3" else (variant, False)
-    M, N, K = 1100, 4096, 2048          # 52 MiB of A+C... plus tails in M
+    M, N, K = 1100, 4096, 2048
     if variant == "baseline":
         M, N, K = 1100, 4096, 512
     from paper_2002_02268_b200 import interp as I
-    old = I._PIPELINE_MIN_BYTES
-    I._PIPELINE_MIN_BYTES = 1 << 20
-    try:
-        term = schedules.apply_padded(sched, M, N, K).term
-        A = torch.from_numpy(synth.matrix(M, K, 8, 0)).pin_memory()
-        B = torch.from_numpy(synth.matrix(K, N, 8, 1)).pin_memory()
-        C_host = I.run(term, [A, B], tf32x3=tf)
-        assert not C_host.is_cuda
-        p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf)
-        C_dev = I.gemm(p, A.to(cuda), B.to(cuda)).cpu()
-        assert torch.equal(C_host, C_dev)
-    finally:
-        I._PIPELINE_MIN_BYTES = old
+    monkeypatch.setattr(I, "_PIPELINE_MIN_BYTES", 1 << 20)
+    if tiles:
+        monkeypatch.setenv("ELV_HOST_TILES", tiles)
+    I._host_pipes.clear()
+    term = schedules.apply_padded(sched, M, N, K).term
+    A = torch.from_numpy(synth.matrix(M, K, 8, 0)).pin_memory()
+    B = torch.from_numpy(synth.matrix(K, N, 8, 1)).pin_memory()
+    C_host = I.run(term, [A, B], tf32x3=tf)
+    assert not C_host.is_cuda
+    p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf)
+    if tiles:
+        assert I._host_pipes and next(iter(I._host_pipes.values())).tile == (384, 1280)
+    C_dev = I.gemm(p, A.to(cuda), B.to(cuda)).cpu()
+    assert torch.equal(C_host, C_dev)
+    I._host_pipes.clear()
+
+
+def test_host_pipeline_large_default_tiling(cuda):
+    """The default tiling at a bench-like shape (8 row blocks x 8192-column
+    chunks) and repeated calls reusing the cached workspace: row samples
+    against the f64 oracle, and call 2 == call 1."""
+    from paper_2002_02268_b200 import interp as I
+    M, N, K = 4096, 16384, 1024
+    term = schedules.apply("parallel", M, N, K).term
+    A = torch.from_numpy(synth.matrix(M, K, 9, 0)).pin_memory()
+    B = torch.from_numpy(synth.matrix(K, N, 9, 1)).pin_memory()
+    C1 = torch.empty((M, N), pin_memory=True)
+    I.run(term, [A, B], tf32x3=True, out=C1)
+    hp = I._host_pipes[(7, M, N, K, str(torch.device("cuda", torch.cuda.current_device())))]
+    assert hp.tile == (512, 8192)
+    C2 = torch.empty((M, N), pin_memory=True)
+    I.run(term, [A, B], tf32x3=True, out=C2)
+    assert torch.equal(C1, C2)
+    rows = np.r_[0:4, 511:514, M - 3:M]
+    An, Bn = A.numpy(), B.numpy()
+    ok, worst = oracle.check(C1.numpy()[rows], oracle.mm_f64(An[rows], Bn), oracle.absprod_np(An[rows], Bn), K)
+    assert ok, worst
 
 
 def test_c_abi_rowshard_single_process(cuda):
