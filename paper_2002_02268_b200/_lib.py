@@ -11,7 +11,8 @@ import os
 
 from ._ref import S
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libelevate_b200.so")
+LIB_PATH = os.environ.get("ELV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                   "libelevate_b200.so")
 
 ELV_OK, ELV_EINVAL, ELV_EVARIANT, ELV_ECUDA, ELV_ENCCL, ELV_EWORKSPACE = 0, -1, -2, -3, -4, -5
 

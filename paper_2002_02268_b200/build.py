@@ -41,28 +41,32 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = True, defines: tuple = (), out: str | None = None) -> str:
+    """Compile SOURCES into `out` (default: the in-tree LIB).  `defines`
+    (e.g. ("ELV_K7_PROF",)) produce instrumented tuning builds, which go to
+    a separate path and are loaded with ELV_LIB=<path>."""
+    target = out or LIB
+    if not force and not defines and not _stale():
         return LIB
     objs = []
-    build_dir = os.path.join(PKG, "_build")
+    build_dir = os.path.join(PKG, "_build" + ("_" + "_".join(defines).lower() if defines else ""))
     os.makedirs(build_dir, exist_ok=True)
     for s in SOURCES:
         obj = os.path.join(build_dir, s.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-c",
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(REPO, "include"), "-c",
                os.path.join(CSRC, s), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
            "-o", tmp, "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

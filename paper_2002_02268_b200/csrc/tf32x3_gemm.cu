@@ -341,7 +341,24 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 // Per SM this halves the B operand's SMEM reads and L2->SMEM fills relative
 // to the 1-CTA kernel (the 1-CTA kernel measured L1/SMEM throughput 88 %,
 // its limiter), for the same MMA work.
+#ifdef ELV_K7_PROF
+// cycle accounting for tuning builds only (scripts/k7_prof.sh):
+// [0] MMA: waiting tempty  [1] MMA: waiting full  [2] MMA: total
+// [3] producer: waiting empty  [4] producer: wave sync  [5] epilogue: waiting tfull
+// [6] epilogue: drain  [7] tiles
+__device__ unsigned long long g_k7_prof[512][8];
+#define PROF_T(x) const long long x = clock64()
+#define PROF_ADD(i, v) prof[i] += (unsigned long long)(v)
+#else
+#define PROF_T(x)
+#define PROF_ADD(i, v)
+#endif
+
 constexpr int P_BM = 128;                          // rows per CTA (pair: 256)
+// warps: 0 TMA producer, 1 MMA issuer, 2..9 epilogue (two per TMEM lane
+// group, one per 128-column half, so the accumulators drain twice as fast)
+constexpr int P_NUM_THREADS = 320;
+constexpr int P_EPI_WARPS = 8;
 constexpr int P_BN = 256;                          // columns per pair tile (128 per CTA staged)
 template <int BKT> struct PairCfg {
   static constexpr int STAGES = BKT == 32 ? 3 : 6;
@@ -396,7 +413,7 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
 }
 
 template <int BKT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
@@ -414,6 +431,9 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef ELV_K7_PROF
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int tiles_m = (M + 2 * P_BM - 1) / (2 * P_BM), tiles_n = (N + P_BN - 1) / P_BN;
@@ -425,7 +445,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
     for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 8);                       // 4 epilogue warps x 2 CTAs (leader's copy)
+    mbar_init(&tempty[0], 2 * P_EPI_WARPS);         // epilogue warps of both CTAs (leader's copy)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -460,10 +480,16 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       for (int t = cluster_id; t < num_tiles; t += num_clusters, ++wave) {
         int m0, n0;
         coords(t, m0, n0);
+        PROF_T(w0);
         if (wave_ctr != nullptr && wave > 0) wave_sync_wait(wave_ctr, (unsigned)(wave * gridDim.x));
+        PROF_T(w1);
+        PROF_ADD(4, w1 - w0);
         const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (P_BN / 2);
         for (int kb = 0; kb < num_kb; ++kb) {
+          PROF_T(e0);
           mbar_wait(&empty[s], ph ^ 1);
+          PROF_T(e1);
+          PROF_ADD(3, e1 - e0);
           uint8_t* st = smem + s * P_STAGE_BYTES;
           if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
           const uint32_t bar = full0 + (uint32_t)(s * 8);
@@ -483,11 +509,19 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       int s = 0; uint32_t ph = 0;
       int it = 0;
       const uint32_t d_big = tmem_base, d_small = tmem_base + (uint32_t)P_BN;
+      PROF_T(m_start);
       for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+        PROF_T(q0);
         mbar_wait(&tempty[0], (uint32_t)(it & 1) ^ 1);
+        PROF_T(q1);
+        PROF_ADD(0, q1 - q0);
+        PROF_ADD(7, 1);
         tc_fence_after();
         for (int kb = 0; kb < num_kb; ++kb) {
+          PROF_T(f0);
           mbar_wait(&full[s], ph);
+          PROF_T(f1);
+          PROF_ADD(1, f1 - f0);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * P_STAGE_BYTES);
           const uint64_t ahi = umma_desc_k<BKT>(st);
@@ -508,9 +542,11 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
         }
         tc_commit_pair(&tfull[0]);              // accumulators ready in both CTAs
       }
+      PROF_T(m_end);
+      PROF_ADD(2, m_end - m_start);
     }
   } else {
-    // ---------------- epilogue (warps 2..5, both CTAs) ----------------
+    // ---------------- epilogue (warps 2..9, both CTAs) ----------------
     const int g = warp & 3;
     const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
     const uint32_t tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
@@ -518,20 +554,34 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
       int m0, n0;
       coords(t, m0, n0);
+      PROF_T(d0);
       mbar_wait(&tfull[0], (uint32_t)(it & 1));
+      PROF_T(d1);
+      PROF_ADD(5, d1 - d0);
       tc_fence_after();
+      // warp -> TMEM lane group g (rows), column half h; each thread owns one
+      // row and writes 128 B runs of it
+      const int h = (warp - 2) >> 2;
       const int row = m0 + (int)rank * P_BM + g * 32 + lane;
       float* crow = C + (size_t)row * ldc;
       const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16);
+      constexpr int NCH = P_BN / 2 / 32;             // 32-column chunks per half
 #pragma unroll 1
-      for (int c = 0; c < P_BN / 32; ++c) {
+      for (int c = 0; c < NCH; ++c) {
+        const int cc = h * NCH + c;
         uint32_t rb[32], rs[32];
-        tmem_ld_32x32b_x32(lane_base + (uint32_t)(c * 32), rb);
-        tmem_ld_32x32b_x32(lane_base + (uint32_t)(P_BN + c * 32), rs);
+        tmem_ld_32x32b_x32(lane_base + (uint32_t)(cc * 32), rb);
+        tmem_ld_32x32b_x32(lane_base + (uint32_t)(P_BN + cc * 32), rs);
+        if (c == NCH - 1) {
+          // this warp's accumulator columns are in registers: release TMEM
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty0);
+        }
         float v[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
-        const int col = n0 + c * 32;
+        const int col = n0 + cc * 32;
         if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
@@ -545,11 +595,14 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty0);
+      PROF_T(d2);
+      PROF_ADD(6, d2 - d1);
     }
   }
+#ifdef ELV_K7_PROF
+  if (lane == 0 && warp <= 2 && blockIdx.x < 512)
+    for (int i = 0; i < 8; ++i) if (prof[i]) atomicAdd(&g_k7_prof[blockIdx.x][i], prof[i]);
+#endif
 
   tc_fence_before();
   __syncthreads();
@@ -734,7 +787,7 @@ static int launch_pair(const CUtensorMap& m_ahi_unused, const float* a_hi, const
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
   unsigned int* ctr = wave_counter(dev, st);
-  k7_tf32x3_pair<BKT><<<2 * clusters, NUM_THREADS, PairCfg<BKT>::SMEM_BYTES, st>>>(
+  k7_tf32x3_pair<BKT><<<2 * clusters, P_NUM_THREADS, PairCfg<BKT>::SMEM_BYTES, st>>>(
       ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT, with_lolo(K), tile_group(8), ctr);
   return check_launch("gemm_parallel_tf32x3_pair");
 }
@@ -823,3 +876,14 @@ int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_b
 }
 
 }  // namespace elv
+
+#ifdef ELV_K7_PROF
+extern "C" int elv_debug_k7_prof(unsigned long long* host, int reset) {
+  cudaMemcpyFromSymbol(host, elv::g_k7_prof, sizeof(elv::g_k7_prof));
+  if (reset) {
+    static unsigned long long zeros[512][8];
+    cudaMemcpyToSymbol(elv::g_k7_prof, zeros, sizeof(zeros));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
