@@ -48,7 +48,11 @@ HostPlan make_plan(int v, int M, int N, int K) {
   p.R = M;
   p.Nc = N;
   if (bytes >= (double)(64 << 20)) {
-    const int row_blocks = M >= 8192 ? 16 : (M >= 2048 ? 8 : (M >= 512 ? 2 : 1));
+    // 3xTF32 is PCIe-bound (GEMM ~ D2H time): finer row blocks start the D2H
+    // stream sooner.  The SIMT variants are GEMM-bound (~4.6x the PCIe time):
+    // 8 row blocks keep each launch at >= 6 waves of 128x256 tiles.
+    const int fine = v == ELV_PARALLEL_TF32X3 ? 16 : 8;
+    const int row_blocks = M >= 8192 ? fine : (M >= 2048 ? 8 : (M >= 512 ? 2 : 1));
     p.R = (int)up((size_t)ceil_div(M, row_blocks), 256);
     if (p.R > M) p.R = M;
     if (N >= 16384) {

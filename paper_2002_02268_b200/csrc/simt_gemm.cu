@@ -773,6 +773,119 @@ k6_sgemm_cp(const float* __restrict__ PA, const float* __restrict__ PB, float* _
   }
 }
 
+// Small problems (fewer 128x256 tiles than SMs, e.g. 1024^3 -> 32): 64x64
+// tiles so every SM gets work, 64 threads x 8x8 outputs (4 LDS.128 per 64
+// FFMA, so SMEM bandwidth is not the bound), the same packed operands and
+// 4-stage cp.async ring as k6_sgemm_cp.  A 64-row tile is one half of a
+// 128-row packedA panel.  Same sequential fmaf chain per element.
+constexpr int SM_BM = 64, SM_BN = 64, SM_BK = 16, SM_STAGES = 4;
+constexpr int SM_SMEM = SM_STAGES * SM_BK * (SM_BM + SM_BN) * 4;   // 32 KB
+
+__global__ void __launch_bounds__(64, 4)
+k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
+               int M, int N, int K, int ldc) {
+  extern __shared__ __align__(16) float smem_s[];
+  float* As = smem_s;                                  // [STAGES][BK][64]
+  float* Bs = smem_s + SM_STAGES * SM_BK * SM_BM;      // [STAGES][BK][64]
+  const int tid = threadIdx.x;
+  const int trow = (tid >> 3) * 4, tcol = (tid & 7) * 4;   // + {0..3, 32..35} each
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+  const int tiles_m = (M + SM_BM - 1) / SM_BM, tiles_n = (N + SM_BN - 1) / SM_BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nkb = (K + SM_BK - 1) / SM_BK;
+
+  for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    const int tm = t % tiles_m, tn = t / tiles_m;      // column-major: neighbours share B panels
+    const int row0 = tm * SM_BM, col0 = tn * SM_BN;
+    const float* pa = PA + (size_t)(row0 >> 7) * K * 128 + (row0 & 127);
+    const float* pb = PB + (size_t)(col0 >> 5) * K * kPanel;
+    auto issue = [&](int kb, int slot) {
+      const int k0 = kb * SM_BK;
+#pragma unroll
+      for (int i = 0; i < SM_BK * 16 / 64; ++i) {      // A: BK rows x 64 floats = 256 float4
+        const int q = tid + i * 64;
+        const int kk = q >> 4, c4 = (q & 15) * 4;
+        const int gk = k0 + kk;
+        cp_async16(&As[(slot * SM_BK + kk) * SM_BM + c4], pa + (size_t)min(gk, K - 1) * 128 + c4,
+                   gk < K ? 16 : 0);
+      }
+#pragma unroll
+      for (int i = 0; i < SM_BK * 16 / 64; ++i) {      // B: 2 panels x BK rows x 32 floats
+        const int q = tid + i * 64;
+        const int pnl = q / (SM_BK * 8), w = q % (SM_BK * 8);
+        const int kk = w >> 3, c4 = (w & 7) * 4;
+        const int gk = k0 + kk;
+        cp_async16(&Bs[(slot * SM_BK + kk) * SM_BN + pnl * 32 + c4],
+                   pb + ((size_t)pnl * K + min(gk, K - 1)) * kPanel + c4, gk < K ? 16 : 0);
+      }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+#pragma unroll
+    for (int st = 0; st < SM_STAGES - 1; ++st) {
+      if (st < nkb) issue(st, st);
+      cp_async_commit();
+    }
+    for (int kb = 0; kb < nkb; ++kb) {
+      cp_async_wait<SM_STAGES - 2>();
+      __syncthreads();
+      const int nk = kb + SM_STAGES - 1;
+      if (nk < nkb) issue(nk, nk % SM_STAGES);
+      cp_async_commit();
+      const float* as = As + (kb % SM_STAGES) * SM_BK * SM_BM;
+      const float* bs = Bs + (kb % SM_STAGES) * SM_BK * SM_BN;
+      float a[2][8], b[2][8];
+      auto lfrag = [&](int slot, int k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * SM_BM + trow);
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * SM_BM + trow + 32);
+        const float4 b0 = *reinterpret_cast<const float4*>(bs + k * SM_BN + tcol);
+        const float4 b1 = *reinterpret_cast<const float4*>(bs + k * SM_BN + tcol + 32);
+        a[slot][0] = a0.x; a[slot][1] = a0.y; a[slot][2] = a0.z; a[slot][3] = a0.w;
+        a[slot][4] = a1.x; a[slot][5] = a1.y; a[slot][6] = a1.z; a[slot][7] = a1.w;
+        b[slot][0] = b0.x; b[slot][1] = b0.y; b[slot][2] = b0.z; b[slot][3] = b0.w;
+        b[slot][4] = b1.x; b[slot][5] = b1.y; b[slot][6] = b1.z; b[slot][7] = b1.w;
+      };
+      lfrag(0, 0);
+#pragma unroll
+      for (int k = 0; k < SM_BK; ++k) {
+        if (k + 1 < SM_BK) lfrag((k + 1) & 1, k + 1);
+#pragma unroll
+        for (int i = 0; i < 8; i += 2)
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            acc[i][j] = fmaf(a[k & 1][i], b[k & 1][j], acc[i][j]);
+            acc[i][j + 1] = fmaf(a[k & 1][i], b[k & 1][j + 1], acc[i][j + 1]);
+            acc[i + 1][j + 1] = fmaf(a[k & 1][i + 1], b[k & 1][j + 1], acc[i + 1][j + 1]);
+            acc[i + 1][j] = fmaf(a[k & 1][i + 1], b[k & 1][j], acc[i + 1][j]);
+          }
+      }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = col0 + tcol + h * 32;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float* v = &acc[i][h * 4];
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // packA: packedA[p][k][r] = A[128p + r][k], zero past M.  32x32 tiles through
 // SMEM so both the row reads of A and the panel-row writes coalesce.
 __global__ void __launch_bounds__(256)
@@ -856,6 +969,10 @@ int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStr
 // the packed-A cp.async kernel serves the large-problem regime of the
 // parallel schedule (the same regime as the 8x16 kernel); ELV_SGEMM_CP=0
 // falls back to the raw-A kernels for tuning comparisons.
+static bool parallel_small(int M, int N) {
+  return (long long)((M + 127) / 128) * ((N + 127) / 128) < num_sms();
+}
+
 bool parallel_uses_packed_a(int M, int N) {
   static int enabled = -1;
   if (enabled < 0) {
@@ -864,7 +981,7 @@ bool parallel_uses_packed_a(int M, int N) {
   }
   if (!enabled) return false;
   const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
-  return tiles >= 2LL * num_sms();
+  return tiles >= 2LL * num_sms() || parallel_small(M, N);
 }
 
 size_t pack_a_bytes(int M, int K) { return (size_t)((M + 127) / 128) * 128 * (size_t)K * sizeof(float); }
@@ -877,6 +994,21 @@ int launch_pack_a(const float* A, float* packedA, int M, int K, int lda, cudaStr
 
 int launch_parallel_packed(const float* packedA, const float* packedB, float* C, int M, int N, int K, int ldc,
                            cudaStream_t st) {
+  if (parallel_small(M, N)) {
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      cudaError_t e = cudaFuncSetAttribute(k6_sgemm_small, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_SMEM);
+      if (e != cudaSuccess) return set_error(ELV_ECUDA, "sgemm_small smem attribute: %s", cudaGetErrorString(e));
+      attr_dev = dev;
+    }
+    const long long tiles = (long long)((M + SM_BM - 1) / SM_BM) * ((N + SM_BN - 1) / SM_BN);
+    long long grid = (long long)num_sms() * 4;
+    if (grid > tiles) grid = tiles;
+    k6_sgemm_small<<<(unsigned)grid, 64, SM_SMEM, st>>>(packedA, packedB, C, M, N, K, ldc);
+    return check_launch("gemm_parallel_small");
+  }
   static int order = -1;
   if (order < 0) {
     const char* e = getenv("ELV_SGEMM_ORDER");

@@ -36,14 +36,23 @@
 namespace elv {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 16;        // BK fp32 = 64 B rows (SWIZZLE_64B)
-constexpr int STAGES = 4;
+constexpr int BM = 128, BK = 16;                  // BK fp32 = 64 B rows (SWIZZLE_64B)
 constexpr int NUM_THREADS = 192;
 constexpr int A_TILE_BYTES = BM * BK * 4;         // 8 KB
-constexpr int B_TILE_BYTES = BN * BK * 4;         // 16 KB
-constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;   // 48 KB
-constexpr int TMEM_COLS = 512;                    // D_big + D_small, 256 fp32 columns each
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+constexpr int TMEM_COLS = 512;                    // pair kernel: D_big + D_small, 256 columns each
+
+// The 1-CTA kernel is templated on its N tile (256, 128 or 64): narrow tiles
+// give small problems (e.g. 1024^3: 32 tiles of 128x256 for 148 SMs) more
+// CTAs.  Per-element arithmetic does not depend on the tile shape.
+template <int TBN> struct OneCfg {
+  static constexpr int B_TILE = TBN * BK * 4;
+  static constexpr int STAGE = 2 * A_TILE_BYTES + 2 * B_TILE;
+  static constexpr int NST = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
+  static constexpr int TMEM = 2 * TBN;             // D_big | D_small
+  static constexpr int SMEM = NST * STAGE + 256 + 1024;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
+                                    ((uint32_t)(BM >> 4) << 24);
+};
 
 inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
@@ -147,8 +156,6 @@ __device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr) {
 }
 
 // instruction descriptor: D=f32, A=B=tf32, both K-major, N=256, M=128
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
 
 // Wave synchronisation of the persistent CTAs' producers: before loading its
 // (w+1)-th tile a producer waits until every CTA has issued the loads of its
@@ -174,7 +181,7 @@ __device__ __forceinline__ void wave_sync_wait(unsigned int* ctr, unsigned int t
 }
 
 struct TileSched {
-  int tiles_m, tiles_n, group;
+  int tiles_m, tiles_n, group, bn;
   __device__ void coords(int t, int& m0, int& n0) const {
     const int GROUP = group;                        // row-tiles per L2 group
     const int per_group = GROUP * tiles_n;
@@ -183,15 +190,21 @@ struct TileSched {
     const int gm = min(tiles_m - first_m, GROUP);
     const int in = t - g * per_group;
     m0 = (first_m + in % gm) * BM;
-    n0 = (in / gm) * BN;
+    n0 = (in / gm) * bn;
   }
 };
 
+template <int TBN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
           float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
           unsigned int* __restrict__ wave_ctr) {
+  constexpr int STAGES = OneCfg<TBN>::NST;
+  constexpr int STAGE_BYTES = OneCfg<TBN>::STAGE;
+  constexpr int B_TILE_BYTES = OneCfg<TBN>::B_TILE;
+  constexpr int BN = TBN;
+  constexpr uint32_t kIdesc = OneCfg<TBN>::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -201,7 +214,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN, group};
+  const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN, group, BN};
   const int num_tiles = sched.tiles_m * sched.tiles_n;
 
   if (warp == 0 && lane == 0) {
@@ -215,7 +228,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)), "r"(TMEM_COLS));
+                     smem_u32(tmem_holder)), "r"(OneCfg<TBN>::TMEM));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -328,7 +341,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(OneCfg<TBN>::TMEM));
   }
 }
 
@@ -621,29 +634,48 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// One row segment of 4 k's per thread: float4 in, two float4 out (rows of A
+// are K-major already, so the planes are a padded elementwise map).  2D grid:
+// x over Kp/4, y-stride over rows -- no 64-bit division per element.
+__device__ __forceinline__ void split_a_block(const float* __restrict__ A, float* __restrict__ hi,
+                                              float* __restrict__ lo, int M, int K, int lda, int Kp, bool vec,
+                                              int bx, int by, int gy) {
+  const int k = (bx * 256 + threadIdx.x) * 4;
+  if (k >= Kp) return;
+  for (int r = by; r < M; r += gy) {
+    const float* src = A + (size_t)r * lda + k;
+    float4 x;
+    if (vec && k + 3 < K) {
+      x = __ldg(reinterpret_cast<const float4*>(src));
+    } else {
+      x.x = k + 0 < K ? __ldg(src + 0) : 0.f;
+      x.y = k + 1 < K ? __ldg(src + 1) : 0.f;
+      x.z = k + 2 < K ? __ldg(src + 2) : 0.f;
+      x.w = k + 3 < K ? __ldg(src + 3) : 0.f;
+    }
+    const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+    const float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
+                                 tf32_rna(x.w - h.w));
+    const size_t o = (size_t)r * Kp + k;
+    *reinterpret_cast<float4*>(hi + o) = h;
+    *reinterpret_cast<float4*>(lo + o) = l;
+  }
+}
 __global__ void __launch_bounds__(256)
 k_split_a(const float* __restrict__ A, float* __restrict__ hi, float* __restrict__ lo, int M, int K,
-          int lda, int Kp) {
-  const long long total = (long long)M * Kp;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / Kp), k = (int)(i - (long long)r * Kp);
-    const float x = k < K ? __ldg(A + (size_t)r * lda + k) : 0.f;
-    const float h = tf32_rna(x);
-    hi[i] = h;
-    lo[i] = tf32_rna(x - h);
-  }
+          int lda, int Kp, bool vec) {
+  split_a_block(A, hi, lo, M, K, lda, Kp, vec, blockIdx.x, blockIdx.y, gridDim.y);
 }
 
 // 32x32 tiles through SMEM: reads of B rows and writes of Bt rows coalesce.
 // PACKED: the source is packedB panels [N/32][K][32] (the packB layout the
 // row-shard driver broadcasts) instead of row-major B.
 template <bool PACKED>
-__global__ void __launch_bounds__(256)
-k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* __restrict__ lo,
-                    int K, int N, int ldb, int Kp) {
+__device__ __forceinline__ void split_transpose_b_block(const float* __restrict__ B, float* __restrict__ hi,
+                                                        float* __restrict__ lo, int K, int N, int ldb, int Kp,
+                                                        int bx, int by) {
   __shared__ float t[32][33];
-  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int k0 = by * 32, n0 = bx * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -664,6 +696,23 @@ k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* 
       lo[(size_t)n * Kp + k] = tf32_rna(x - h);
     }
   }
+}
+template <bool PACKED>
+__global__ void __launch_bounds__(256)
+k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* __restrict__ lo,
+                    int K, int N, int ldb, int Kp) {
+  split_transpose_b_block<PACKED>(B, hi, lo, K, N, ldb, Kp, blockIdx.x, blockIdx.y);
+}
+
+// elv_gemm's prepare for variant 7 in one launch: blocks [0, ga) split A,
+// the rest split-transpose B (the two are independent).
+__global__ void __launch_bounds__(256)
+k_split_ab(const float* __restrict__ A, float* __restrict__ ahi, float* __restrict__ alo, int M, int lda,
+           bool vecA, int gxa, int gya, const float* __restrict__ B, float* __restrict__ bhi,
+           float* __restrict__ blo, int N, int ldb, int gxb, int K, int Kp) {
+  const int b = blockIdx.x, ga = gxa * gya;
+  if (b < ga) split_a_block(A, ahi, alo, M, K, lda, Kp, vecA, b % gxa, b / gxa, gya);
+  else split_transpose_b_block<false>(B, bhi, blo, K, N, ldb, Kp, (b - ga) % gxb, (b - ga) / gxb);
 }
 
 // ----------------------------------------------------------------------------
@@ -767,9 +816,8 @@ static int tile_group(int dflt) {
 }
 
 template <int BKT>
-static int launch_pair(const CUtensorMap& m_ahi_unused, const float* a_hi, const float* a_lo, const float* b_hi,
+static int launch_pair(const float* a_hi, const float* a_lo, const float* b_hi,
                        const float* b_lo, float* C, int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st) {
-  (void)m_ahi_unused;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   int rc = make_map(&ma_hi, a_hi, M, Kp, P_BM, BKT);
   if (!rc) rc = make_map(&ma_lo, a_lo, M, Kp, P_BM, BKT);
@@ -786,7 +834,7 @@ static int launch_pair(const CUtensorMap& m_ahi_unused, const float* a_hi, const
   const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
-  unsigned int* ctr = wave_counter(dev, st);
+  unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;   // one wave: nothing to sync
   k7_tf32x3_pair<BKT><<<2 * clusters, P_NUM_THREADS, PairCfg<BKT>::SMEM_BYTES, st>>>(
       ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT, with_lolo(K), tile_group(8), ctr);
   return check_launch("gemm_parallel_tf32x3_pair");
@@ -806,14 +854,23 @@ size_t tf32x3_workspace_bytes(int M, int N, int K) {
 }
 
 
+static void split_a_grid(int M, int Kp, int* gx, int* gy) {
+  *gx = (Kp / 4 + 255) / 256;
+  int y = num_sms() * 16 / *gx;
+  if (y < 1) y = 1;
+  if (y > M) y = M;
+  if (y > 65535) y = 65535;
+  *gy = y;
+}
+
 int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st) {
   const int Kp = (int)kpad(K);
   float* hi = align128(a_planes);
   float* lo = hi + (size_t)M * Kp;
-  long long blocks = ((long long)M * Kp + 255) / 256;
-  const long long cap = (long long)num_sms() * 16;
-  if (blocks > cap) blocks = cap;
-  k_split_a<<<(unsigned)blocks, 256, 0, st>>>(A, hi, lo, M, K, lda, Kp);
+  int gx, gy;
+  split_a_grid(M, Kp, &gx, &gy);
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
+  k_split_a<<<dim3(gx, gy), 256, 0, st>>>(A, hi, lo, M, K, lda, Kp, vec);
   return check_launch("tf32x3_split_a");
 }
 
@@ -827,6 +884,53 @@ int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_p
   return check_launch("tf32x3_split_b");
 }
 
+// N tile of the 1-CTA kernel: minimise waves x tile work / efficiency, with
+// the narrow tiles' SMEM-operand-bandwidth penalty (measured-order estimate:
+// 128 ~ 0.95, 64 ~ 0.67 of the 256-wide MMA rate).  ELV_TF32X3_BN forces one.
+static int one_cta_bn(int M, int N) {
+  static int forced = -2;
+  if (forced == -2) {
+    forced = env_int("ELV_TF32X3_BN", -1);
+    if (forced != 64 && forced != 128 && forced != 256) forced = -1;
+  }
+  if (forced > 0) return forced;
+  const int bns[3] = {256, 128, 64};
+  const double eff[3] = {1.0, 0.95, 0.67};
+  int best = 256;
+  double best_cost = 1e30;
+  for (int i = 0; i < 3; ++i) {
+    const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bns[i] - 1) / bns[i]);
+    const long long waves = (tiles + num_sms() - 1) / num_sms();
+    const double cost = (double)waves * bns[i] / eff[i];
+    if (cost < best_cost * 0.999) { best_cost = cost; best = bns[i]; }
+  }
+  return best;
+}
+
+template <int TBN>
+static int launch_one(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo, float* C,
+                      int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st) {
+  CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
+  int rc = make_map(&m_ahi, a_hi, M, Kp, BM);
+  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM);
+  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, TBN);
+  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, TBN);
+  if (rc) return rc;
+  static int attr_dev = -1;
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3<TBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         OneCfg<TBN>::SMEM);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
+    attr_dev = dev;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + TBN - 1) / TBN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  unsigned int* ctr = tiles > grid ? wave_counter(dev, st) : nullptr;
+  k7_tf32x3<TBN><<<grid, NUM_THREADS, OneCfg<TBN>::SMEM, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc,
+                                                                Kp / BK, with_lolo(K), tile_group(16), ctr);
+  return check_launch("gemm_parallel_tf32x3");
+}
+
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                        cudaStream_t st) {
   const int Kp = (int)kpad(K);
@@ -834,29 +938,15 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   const float* a_lo = a_hi + (size_t)M * Kp;
   const float* b_hi = align128(b_planes);
   const float* b_lo = b_hi + (size_t)N * Kp;
-  CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
-  int rc = make_map(&m_ahi, a_hi, M, Kp, BM);
-  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM);
-  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, BN);
-  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, BN);
-  if (rc) return rc;
-  static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
-    attr_dev = dev;
-  }
   const int pm = pair_mode(M, N);
-  if (pm == 16) return launch_pair<16>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  if (pm == 32) return launch_pair<32>(m_ahi, a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  unsigned int* ctr = wave_counter(dev, st);
-  k7_tf32x3<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / BK,
-                                                   with_lolo(K), tile_group(16), ctr);
-  return check_launch("gemm_parallel_tf32x3");
+  if (pm == 16) return launch_pair<16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (pm == 32) return launch_pair<32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  const int bn = one_cta_bn(M, N);
+  if (bn == 64) return launch_one<64>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (bn == 128) return launch_one<128>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  return launch_one<256>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
 }
 
 // elv_gemm workspace for variant 7 = [A planes | B planes]
@@ -864,9 +954,19 @@ int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
                    size_t ws_bytes, cudaStream_t st) {
   if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
-  int rc = tf32x3_split_a(A, M, K, lda, ws, st);
-  if (rc) return rc;
-  return tf32x3_split_b(B, K, N, ldb, false, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), st);
+  const int Kp = (int)kpad(K);
+  float* ahi = align128(ws);
+  float* alo = ahi + (size_t)M * Kp;
+  float* bhi = align128(static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K));
+  float* blo = bhi + (size_t)N * Kp;
+  int gxa, gya;
+  split_a_grid(M, Kp, &gxa, &gya);
+  const int gxb = (N + 31) / 32, gyb = (Kp + 31) / 32;
+  const long long blocks = (long long)gxa * gya + (long long)gxb * gyb;
+  if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tf32x3: problem too large for one split launch");
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
+  k_split_ab<<<(unsigned)blocks, 256, 0, st>>>(A, ahi, alo, M, lda, vec, gxa, gya, B, bhi, blo, N, ldb, gxb, K, Kp);
+  return check_launch("tf32x3_split_ab");
 }
 
 int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {

@@ -1,0 +1,10 @@
+#!/bin/bash
+# small-problem kernels (K7 narrow tiles, K6 64x64) + split_a: tests, ladder, bench
+OUT=gpurun_out/${1:-s2h}
+mkdir -p $OUT
+S=$OUT/summary.txt
+timeout 300 python __graft_entry__.py smoke > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $S
+timeout 1800 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $S
+tail -4 $OUT/pytest_gpu.log >> $S
+timeout 900 python bench.py --workload ladder > $OUT/ladder.jsonl 2> $OUT/ladder.err; echo "ladder rc=$?" >> $S
+timeout 900 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $S

@@ -1,0 +1,65 @@
+"""One small launch of every kernel path, for compute-sanitizer
+(memcheck / racecheck / synccheck):
+
+    compute-sanitizer --tool memcheck --error-exitcode 1 python scripts/sanitize_run.py
+
+Odd shapes exercise the predicated tails; the host pipeline runs with a
+forced ragged tiling.  Results are also checked against the f64 oracle so a
+sanitizer run doubles as a parity run."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import oracle  # noqa: E402
+from paper_2002_02268_b200 import binomial, interp, schedules, synth  # noqa: E402
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    quick = "--quick" in sys.argv
+    shapes = [(129, 257, 33)] if quick else [(129, 257, 33), (257, 1031, 513)]
+    names = list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]
+    for (M, N, K) in shapes:
+        A = synth.matrix(M, K, 5, 0)
+        B = synth.matrix(K, N, 5, 1)
+        ref, ab = oracle.mm_f64(A, B), oracle.absprod_np(A, B)
+        for v in names:
+            sched, tf = ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+            term = schedules.apply_padded(sched, M, N, K).term
+            C = interp.run_tensor(term, torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), tf32x3=tf)
+            torch.cuda.synchronize()
+            ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
+            print(f"{v:16s} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
+            assert ok
+    # host pipeline (elv_gemm_host) with ragged tiles
+    os.environ["ELV_HOST_TILES"] = "96,160"
+    M, N, K = 200, 300, 70
+    A = torch.from_numpy(synth.matrix(M, K, 6, 0)).pin_memory()
+    B = torch.from_numpy(synth.matrix(K, N, 6, 1)).pin_memory()
+    for v in ("parallel", "parallel_tf32x3", "loopPerm"):
+        sched, tf = ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+        p = interp.plan(schedules.apply_padded(sched, M, N, K).term, [(M, K), (K, N)], tf)
+        out = torch.empty((M, N), pin_memory=True)
+        interp.HostPipeline(p, dev)(A, B, out)
+        ok, worst = oracle.check(out.numpy(), oracle.mm_f64(A.numpy(), B.numpy()),
+                                 oracle.absprod_np(A.numpy(), B.numpy()), K)
+        print(f"host pipeline {v:16s} ok={ok} worst={worst:.3f}", flush=True)
+        assert ok
+    # binomial filter kernels
+    img = synth.matrix(67, 45, 7, 2)
+    for name in binomial.SCHEDULE_NAMES:
+        term = binomial.apply(name, 67, 45)
+        out = interp.run(term, [torch.from_numpy(img).to(dev)])
+        torch.cuda.synchronize()
+        refb = oracle.bf_interp_f64(img, name)
+        assert np.all(np.abs(out.cpu().numpy() - refb) <= oracle.bf_bound(img)), name
+        print(f"binomial {name} ok", flush=True)
+    print("sanitize_run: all paths ran")
+
+
+if __name__ == "__main__":
+    main()

@@ -43,8 +43,11 @@ def test_workspace_sizes():
     for v in range(4):
         assert lib.elv_gemm_workspace_bytes(v, 1024, 1024, 1024) == 0
     # packedB: ceil(N/256)*256 columns x K rows of fp32
-    for v in (4, 5, 6):
+    for v in (4, 5):
         assert lib.elv_gemm_workspace_bytes(v, 100, 1000, 33) == 1024 * 33 * 4
+    # parallel: + packedA (ceil(M/128)*128 rows x K) for small problems (64x64-tile
+    # kernel) and large ones (cp.async 128x256 kernel)
+    assert lib.elv_gemm_workspace_bytes(6, 100, 1000, 33) == 1024 * 33 * 4 + 128 * 33 * 4
     assert lib.elv_pack_b_bytes(33, 1000) == 1024 * 33 * 4
     # 3xTF32: hi/lo planes of A (M x Kp) and B^T (N x Kp), Kp = K rounded to 16
     assert lib.elv_gemm_workspace_bytes(7, 100, 200, 30) == (2 * 100 * 32 + 2 * 200 * 32) * 4 + 256

@@ -218,3 +218,38 @@ def test_bench_shape_row_sample(cuda, variant):
     assert ok, f"{variant} cols: worst err/bound = {worst:.3g}"
     del C
     torch.cuda.empty_cache()
+
+
+_TILE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repo!r})
+from paper_2002_02268_b200 import interp, schedules, synth
+M, N, K = {M}, {N}, {K}
+A = torch.empty((M, K), device="cuda"); B = torch.empty((K, N), device="cuda")
+synth.fill_device(A, 11, 0); synth.fill_device(B, 11, 1)
+t = schedules.apply_padded("parallel", M, N, K).term
+np.save({out!r}, interp.run_tensor(t, A, B, tf32x3=True).cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (300, 1000, 200)], ids=lambda s: "x".join(map(str, s)))
+def test_tf32x3_tile_widths_bitwise_identical(cuda, tmp_path, shape):
+    """The 1-CTA tcgen05 kernel at N tiles 256 / 128 / 64 (ELV_TF32X3_BN,
+    read once per process, so one subprocess each): per-element arithmetic
+    does not depend on the tile width -- bitwise equal -- and within the
+    oracle bound."""
+    import subprocess
+    import sys
+    M, N, K = shape
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for bn in (256, 128, 64):
+        out = str(tmp_path / f"c{bn}.npy")
+        env = dict(os.environ, ELV_TF32X3_BN=str(bn), ELV_TF32X3_PAIR="0")
+        subprocess.run([sys.executable, "-c", _TILE_SCRIPT.format(repo=repo, M=M, N=N, K=K, out=out)],
+                       env=env, check=True, timeout=300)
+        outs[bn] = np.load(out)
+    assert np.array_equal(outs[256], outs[128]) and np.array_equal(outs[256], outs[64])
+    A, B = synth.matrix(M, K, 11, 0), synth.matrix(K, N, 11, 1)
+    ok, worst = oracle.check(outs[64], oracle.mm_f64(A, B), oracle.absprod_np(A, B), K)
+    assert ok, worst
