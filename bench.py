@@ -452,6 +452,16 @@ def main():
             "kernel": kernel, "kernel_ms": comp_ms, "prepass_ms": prep_ms,
             "kernel_share_of_step": comp_ms / ms, "peak_source": f"{peaks_src}: {note}",
             "algorithmic_flops_per_launch": 2.0 * sh.rows * N * K, "library_reference": cublas}
+    # compulsory bytes of one launch: operand planes (3xTF32: hi+lo, 8 B per
+    # element; SIMT: packed fp32, 4 B) read once + C written once
+    ob = 8 if args.variant == "parallel_tf32x3" else 4
+    roof["algorithmic_bytes_per_launch"] = float(ob * (sh.rows * K + K * N) + 4 * sh.rows * N)
+    roof["traffic_note"] = (
+        "traffic = ncu dram read+write of the same launch (profiles/ncu_traffic.json). It exceeds the "
+        "compulsory bytes because each wave of concurrent output tiles (74 pair tiles of 256x256, or 148 "
+        "SIMT tiles) streams its own A and B panels through L2 over the whole K=8192, and the 126 MB L2 "
+        "cannot carry a panel from one wave to the next; the wave-synchronised rasterisation keeps it near "
+        "that per-wave minimum. DRAM runs at ~1.1 TB/s (17 % of peak): not the bound.")
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
