@@ -29,6 +29,28 @@ __device__ __forceinline__ bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
+// sm_100 packed FP32: FFMA2 does two IEEE fp32 FMAs (each rounded exactly
+// like fmaf, so results are bitwise those of the scalar kernels) per issue
+// slot.  The A value is broadcast into both halves -- ptxas folds the
+// {a, a} pack into the FFMA2's .F32 scalar-operand form -- and B / the
+// accumulators are adjacent column pairs.  Halving the FMA instruction
+// count relieves the issue / register-bank dispatch stalls that hold the
+// scalar 8x16 kernel at ~71 % of the FFMA peak.
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
+
 // ---------------------------------------------------------------------------
 // K0 baseline: mapSeq(arow => mapSeq(bcol => reduceSeq(acc + a*b)(0)(zip)))
 // One thread per C(i,j); `transpose(b)` is a strided view (column reads of B
@@ -577,11 +599,11 @@ k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* _
         *reinterpret_cast<float4*>(&Bs[buf][w >> 3][pnl * 32 + (w & 7) * 4]) = rb[i];
       }
     };
-    float acc[8][16];
+    unsigned long long acc[8][8];                  // [row][column pair], FFMA2
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[i][j] = 0.f;
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
     gload(0);
     sstore(0);
     __syncthreads();
@@ -591,7 +613,8 @@ k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* _
       if (more) gload(k0 + BK);
 #pragma unroll
       for (int k = 0; k < BK; ++k) {
-        float a[8], b[16];
+        float a[8];
+        unsigned long long b[8];
         const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][trow]);
         const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][trow + 32]);
         a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
@@ -599,12 +622,15 @@ k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* _
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const float4 bv = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol + 16 * h]);
-          b[4 * h] = bv.x; b[4 * h + 1] = bv.y; b[4 * h + 2] = bv.z; b[4 * h + 3] = bv.w;
+          b[2 * h] = pack2(bv.x, bv.y);
+          b[2 * h + 1] = pack2(bv.z, bv.w);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i) {
+          const unsigned long long ai = pack2(a[i], a[i]);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < 8; ++j) ffma2(acc[i][j], ai, b[j]);
+        }
       }
       if (more) sstore(buf ^ 1);
       __syncthreads();
@@ -618,7 +644,8 @@ k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* _
       for (int h = 0; h < 4; ++h) {
         const int gj = col0 + tcol + h * 16;
         float* p = C + (size_t)gi * ldc + gj;
-        const float* v = &acc[i][h * 4];
+        const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
+        const float v[4] = {lo.x, lo.y, hi.x, hi.y};
         if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
         else
 #pragma unroll
@@ -773,9 +800,119 @@ k6_sgemm_cp(const float* __restrict__ PA, const float* __restrict__ PB, float* _
   }
 }
 
+__global__ void __launch_bounds__(256, 1)
+k6_sgemm_ffma2(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
+               int M, int N, int K, int ldc) {
+  extern __shared__ __align__(16) float smem_f2[];
+  float* As = smem_f2;                              // [STAGES][BK][128]
+  float* Bs = smem_f2 + CP_STAGES * CP_BK * 128;    // [STAGES][BK][256]
+  constexpr int BM = 128, BN = 256;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lm = lane >> 2, ln = lane & 3;
+  const int trow = wm * 64 + lm * 4;
+  const int tcol = wn * 64 + ln * 4;
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nkb = (K + CP_BK - 1) / CP_BK;
+
+  for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+    const int row0 = tc.m * BM, col0 = tc.n * BN;
+    const float* pa = PA + (size_t)tc.m * K * BM;
+    const float* pb = PB + (size_t)(col0 >> 5) * K * kPanel;
+    auto issue = [&](int kb, int slot) {
+      const int k0 = kb * CP_BK;
+#pragma unroll
+      for (int i = 0; i < CP_BK * 32 / 256; ++i) {
+        const int q = tid + i * 256;
+        const int kk = q >> 5, c4 = (q & 31) * 4;
+        const int gk = k0 + kk;
+        cp_async16(&As[(slot * CP_BK + kk) * BM + c4], pa + (size_t)min(gk, K - 1) * BM + c4, gk < K ? 16 : 0);
+      }
+#pragma unroll
+      for (int i = 0; i < CP_BK * 64 / 256; ++i) {
+        const int q = tid + i * 256;
+        const int pnl = q / (CP_BK * 8), w = q % (CP_BK * 8);
+        const int kk = w >> 3, c4 = (w & 7) * 4;
+        const int gk = k0 + kk;
+        cp_async16(&Bs[(slot * CP_BK + kk) * BN + pnl * 32 + c4],
+                   pb + ((size_t)pnl * K + min(gk, K - 1)) * kPanel + c4, gk < K ? 16 : 0);
+      }
+    };
+
+    unsigned long long acc[8][8];                  // [row i][column pair]
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+
+#pragma unroll
+    for (int st = 0; st < CP_STAGES - 1; ++st) {
+      if (st < nkb) issue(st, st);
+      cp_async_commit();
+    }
+    for (int kb = 0; kb < nkb; ++kb) {
+      cp_async_wait<CP_STAGES - 2>();
+      __syncthreads();
+      const int nk = kb + CP_STAGES - 1;
+      if (nk < nkb) issue(nk, nk % CP_STAGES);
+      cp_async_commit();
+      const float* as = As + (kb % CP_STAGES) * CP_BK * BM;
+      const float* bs = Bs + (kb % CP_STAGES) * CP_BK * BN;
+      float a[2][8];
+      unsigned long long b[2][8];
+      auto lfrag = [&](int slot, int k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * BM + trow);
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * BM + trow + 32);
+        a[slot][0] = a0.x; a[slot][1] = a0.y; a[slot][2] = a0.z; a[slot][3] = a0.w;
+        a[slot][4] = a1.x; a[slot][5] = a1.y; a[slot][6] = a1.z; a[slot][7] = a1.w;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float4 bv = *reinterpret_cast<const float4*>(bs + k * BN + tcol + 16 * h);
+          b[slot][2 * h] = pack2(bv.x, bv.y);
+          b[slot][2 * h + 1] = pack2(bv.z, bv.w);
+        }
+      };
+      lfrag(0, 0);
+#pragma unroll
+      for (int k = 0; k < CP_BK; ++k) {
+        if (k + 1 < CP_BK) lfrag((k + 1) & 1, k + 1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const unsigned long long ai = pack2(a[k & 1][i], a[k & 1][i]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ffma2(acc[i][j], ai, b[k & 1][j]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int gj = col0 + tcol + h * 16;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
+        const float v[4] = {lo.x, lo.y, hi.x, hi.y};
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Small problems (fewer 128x256 tiles than SMs, e.g. 1024^3 -> 32): 64x64
-// tiles so every SM gets work, 64 threads x 8x8 outputs (4 LDS.128 per 64
-// FFMA, so SMEM bandwidth is not the bound), the same packed operands and
+// tiles so every SM gets work, 64 threads x 8x8 outputs (4 LDS.128 per 32
+// FFMA2, so SMEM bandwidth is not the bound), the same packed operands and
 // 4-stage cp.async ring as k6_sgemm_cp.  A 64-row tile is one half of a
 // 128-row packedA panel.  Same sequential fmaf chain per element.
 constexpr int SM_BM = 64, SM_BN = 64, SM_BK = 16, SM_STAGES = 4;
@@ -820,11 +957,11 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
       }
     };
 
-    float acc[8][8];
+    unsigned long long acc[8][4];                  // [row][column pair], FFMA2 (see k6_sgemm_ffma2)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
 
 #pragma unroll
     for (int st = 0; st < SM_STAGES - 1; ++st) {
@@ -839,7 +976,8 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
       cp_async_commit();
       const float* as = As + (kb % SM_STAGES) * SM_BK * SM_BM;
       const float* bs = Bs + (kb % SM_STAGES) * SM_BK * SM_BN;
-      float a[2][8], b[2][8];
+      float a[2][8];
+      unsigned long long b[2][4];
       auto lfrag = [&](int slot, int k) {
         const float4 a0 = *reinterpret_cast<const float4*>(as + k * SM_BM + trow);
         const float4 a1 = *reinterpret_cast<const float4*>(as + k * SM_BM + trow + 32);
@@ -847,22 +985,19 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
         const float4 b1 = *reinterpret_cast<const float4*>(bs + k * SM_BN + tcol + 32);
         a[slot][0] = a0.x; a[slot][1] = a0.y; a[slot][2] = a0.z; a[slot][3] = a0.w;
         a[slot][4] = a1.x; a[slot][5] = a1.y; a[slot][6] = a1.z; a[slot][7] = a1.w;
-        b[slot][0] = b0.x; b[slot][1] = b0.y; b[slot][2] = b0.z; b[slot][3] = b0.w;
-        b[slot][4] = b1.x; b[slot][5] = b1.y; b[slot][6] = b1.z; b[slot][7] = b1.w;
+        b[slot][0] = pack2(b0.x, b0.y); b[slot][1] = pack2(b0.z, b0.w);
+        b[slot][2] = pack2(b1.x, b1.y); b[slot][3] = pack2(b1.z, b1.w);
       };
       lfrag(0, 0);
 #pragma unroll
       for (int k = 0; k < SM_BK; ++k) {
         if (k + 1 < SM_BK) lfrag((k + 1) & 1, k + 1);
 #pragma unroll
-        for (int i = 0; i < 8; i += 2)
+        for (int i = 0; i < 8; ++i) {
+          const unsigned long long ai = pack2(a[k & 1][i], a[k & 1][i]);
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) {
-            acc[i][j] = fmaf(a[k & 1][i], b[k & 1][j], acc[i][j]);
-            acc[i][j + 1] = fmaf(a[k & 1][i], b[k & 1][j + 1], acc[i][j + 1]);
-            acc[i + 1][j + 1] = fmaf(a[k & 1][i + 1], b[k & 1][j + 1], acc[i + 1][j + 1]);
-            acc[i + 1][j] = fmaf(a[k & 1][i + 1], b[k & 1][j], acc[i + 1][j]);
-          }
+          for (int j = 0; j < 4; ++j) ffma2(acc[i][j], ai, b[k & 1][j]);
+        }
       }
     }
     cp_async_wait<0>();
@@ -875,7 +1010,8 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
       for (int h = 0; h < 2; ++h) {
         const int gj = col0 + tcol + h * 32;
         float* p = C + (size_t)gi * ldc + gj;
-        const float* v = &acc[i][h * 4];
+        const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
+        const float v[4] = {lo.x, lo.y, hi.x, hi.y};
         if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
         else
 #pragma unroll
@@ -1012,11 +1148,12 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
   static int order = -1;
   if (order < 0) {
     const char* e = getenv("ELV_SGEMM_ORDER");
-    order = e ? atoi(e) : 2;              // measured: 2x2 FFMA blocks 51.97 TF vs 51.0 / 48.6
-    if (order < 0 || order > 2) order = 2;
+    order = e ? atoi(e) : 3;   // measured at 32768x32768x8192: FFMA2 60.5 TF; scalar 2x2 FFMA blocks 52.6
+    if (order < 0 || order > 3) order = 2;
   }
-  auto fn = order == 0 ? k6_sgemm_cp<0> : order == 1 ? k6_sgemm_cp<1> : k6_sgemm_cp<2>;
-  static int attr_dev[3] = {-1, -1, -1};
+  auto fn = order == 0 ? k6_sgemm_cp<0> : order == 1 ? k6_sgemm_cp<1> : order == 2 ? k6_sgemm_cp<2>
+                                                                                      : k6_sgemm_ffma2;
+  static int attr_dev[4] = {-1, -1, -1, -1};
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev[order] != dev) {
