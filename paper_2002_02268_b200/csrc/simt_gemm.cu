@@ -308,11 +308,15 @@ __device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
   return {first_m + in % gm, in / gm};
 }
 
-template <bool PARALLEL>
-__global__ void __launch_bounds__(256, 2)
+// TBM = 128 (256 threads) or 64 (128 threads, small problems): the same
+// 8x8 register accumulators per thread, half the rows per CTA.
+template <bool PARALLEL, int TBM = G_BM>
+__global__ void __launch_bounds__(TBM * 2, 2)
 k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* __restrict__ C,
                int M, int N, int K, int lda, int ldc) {
   constexpr int NBUF = PARALLEL ? 2 : 1;
+  constexpr int G_BM = TBM;
+  constexpr int NT = TBM * 2;
   __shared__ __align__(16) float As[NBUF][G_BK][G_BM + G_APAD];
   __shared__ __align__(16) float Bs[NBUF][G_BK][G_BN];
 
@@ -327,7 +331,7 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
 
   // loader roles: A float4 (row = tid/2, k = (tid&1)*4); B float4 from panel tid/64
   const int a_r = tid >> 1, a_k = (tid & 1) * 4;
-  const int b_p = tid >> 6, b_in = tid & 63, b_k = b_in >> 3, b_c = (b_in & 7) * 4;
+  constexpr int BLD = 256 / NT;                    // float4 of B per thread per k-block
 
   const int tiles_m = (M + G_BM - 1) / G_BM, tiles_n = (N + G_BN - 1) / G_BN;
   const int num_tiles = tiles_m * tiles_n;
@@ -343,17 +347,30 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
-    const float* Bpanel = P + (size_t)((col0 >> 5) + b_p) * K * kPanel + b_c;
+    struct VB { float4 v[BLD]; };
     auto ldA = [&](int k0) { return load_a4<G_BM, G_BK>(A, M, K, lda, vecA, row0 + a_r, k0 + a_k); };
     auto ldB = [&](int k0) {
-      const int gk = k0 + b_k;
-      return gk < K ? __ldg(reinterpret_cast<const float4*>(Bpanel + (size_t)gk * kPanel))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      VB r;
+#pragma unroll
+      for (int i = 0; i < BLD; ++i) {
+        const int q = tid + i * NT;
+        const int b_p = q >> 6, b_in = q & 63, b_k = b_in >> 3, b_c = (b_in & 7) * 4;
+        const int gk = k0 + b_k;
+        r.v[i] = gk < K ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)((col0 >> 5) + b_p) * K + gk) * kPanel
+                                                                + b_c))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      return r;
     };
-    auto stage = [&](int buf, float4 va, float4 vb) {
+    auto stage = [&](int buf, float4 va, const VB& vb) {
       As[buf][a_k + 0][a_r] = va.x; As[buf][a_k + 1][a_r] = va.y;
       As[buf][a_k + 2][a_r] = va.z; As[buf][a_k + 3][a_r] = va.w;
-      *reinterpret_cast<float4*>(&Bs[buf][b_k][b_p * 32 + b_c]) = vb;
+#pragma unroll
+      for (int i = 0; i < BLD; ++i) {
+        const int q = tid + i * NT;
+        const int b_p = q >> 6, b_in = q & 63, b_k = b_in >> 3, b_c = (b_in & 7) * 4;
+        *reinterpret_cast<float4*>(&Bs[buf][b_k][b_p * 32 + b_c]) = vb.v[i];
+      }
     };
     auto compute = [&](int buf) {
 #pragma unroll
@@ -372,7 +389,8 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
     };
 
     if (PARALLEL) {
-      float4 va = ldA(0), vb = ldB(0);
+      float4 va = ldA(0);
+      VB vb = ldB(0);
       stage(0, va, vb);
       __syncthreads();
       int buf = 0;
@@ -1197,6 +1215,12 @@ int launch_simt(int variant, const float* A, const float* B, const float* packed
       return check_launch("gemm_arraypacking");
     }
     case ELV_CACHEBLOCKS: {
+      // fewer 128x128 tiles than SMs (e.g. 1024^3: 64): 64-row tiles, 128 threads
+      if ((long long)((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN) < num_sms()) {
+        dim3 grid((N + G_BN - 1) / G_BN, (M + 63) / 64);
+        k56_packed_8x8<false, 64><<<grid, 128, 0, st>>>(A, packedB, C, M, N, K, lda, ldc);
+        return check_launch("gemm_cacheblocks");
+      }
       dim3 grid((N + G_BN - 1) / G_BN, (M + G_BM - 1) / G_BM);
       k56_packed_8x8<false><<<grid, 256, 0, st>>>(A, packedB, C, M, N, K, lda, ldc);
       return check_launch("gemm_cacheblocks");
