@@ -201,8 +201,8 @@ def _interp_sample(args):
     return time.perf_counter() - t0
 
 
-def cpu_baseline_single(m=32, n=32, k=1024):
-    """Reference interpreter, 1 core, bounded sample (~10 s)."""
+def cpu_baseline_single(m=64, n=32, k=1024):
+    """Reference interpreter, 1 core, bounded sample (~12 s on the GPU box host)."""
     try:
         dt = _interp_sample((m, n, k, 0))
         kind = "reference"
