@@ -12,24 +12,35 @@ from the reference):
   * map, mapSeq, mapPar, mapSeqUnroll, mapVec: lazily indexed (the consumer's
     loop decides where the element is computed);
   * reduce / reduceSeq / reduceSeqUnroll: a sequential fold loop in the
-    reference's order (interp.py:84-89); array-valued accumulators (the
-    lifted reduces of the reordered GEMM schedules) are materialised in
-    per-thread ping-pong buffers;
+    reference's order (interp.py:84-89).  An array-valued accumulator (the
+    lifted reduces of the reordered GEMM schedules) whose operator is
+    elementwise -- element e of op(acc)(x) reads acc only at e, checked on a
+    symbolic element -- is folded per demanded element, so nested lifted
+    reduces become one scalar fold per output in the schedule's own order;
+    any other array accumulator is materialised (two per-thread buffers);
   * toMem / id: identity (values are views; materialisation is a
     performance choice, not semantics -- interp.py:143-144);
   * add / mult: fp32, compiled with --fmad=false so every operation rounds
     separately, like the interpreter's scalar ops (interp.py:145-148).
 
-One thread computes one output scalar.  This is the correct-by-construction
-path: it runs any schedule (including ones the user writes), but without
-the data-reuse engineering of the template kernels.  Kernels are built with
-NVRTC for sm_100a and cached per canonical term print (ir.pretty).
+Thread mapping: one thread per output scalar ("per-scalar") unless some
+array accumulator had to be materialised -- then every scalar would rebuild
+it, so the kernel is regenerated in destination-passing form: the result is
+written following the term's own producer structure (maps are loops, the
+outermost two of them the thread index; layout primitives transform the
+destination; small computing maps are materialised per thread), and no value
+is computed twice.  Kernels are built with NVRTC for sm_100a and cached per
+canonical term print (ir.pretty); `cpu_source` wraps the same code for a
+host compiler, which is how the CPU test suite checks it against the
+reference interpreter.
 """
 
 from __future__ import annotations
 
 import functools
 import itertools
+import random
+import re
 from dataclasses import dataclass
 from typing import Callable
 
@@ -50,10 +61,20 @@ class Scal:
     code: str
 
 
-@dataclass
 class Pair:
-    a: object
-    b: object
+    """A pair whose components are evaluated on first use (zip pairs an
+    element of each array; fst/snd pick one -- the other is never indexed)."""
+
+    def __init__(self, fa, fb):
+        self._fa, self._fb = fa, fb
+
+    @functools.cached_property
+    def a(self):
+        return self._fa()
+
+    @functools.cached_property
+    def b(self):
+        return self._fb()
 
 
 @dataclass
@@ -82,12 +103,21 @@ class Gen:
         self.indent = 1
         self.ids = itertools.count()
         self.dry = 0
+        self.emitted = 0                 # statements emitted or (dry) that would be
         self.consts: list[str] = []
+        self.decls: list[str] = []       # function-scope declarations (strict-map buffers)
+        self.par_sizes: list[int] = []   # extents of the parallel (thread) index levels
+        self.elementwise = True          # mode A: lifted array reduces fold per element
+        self.strict_maps = False         # mode B: materialise small computing maps
+        self.materialised = 0            # array reduces that had to be materialised
+        self.probing = 0                 # >0 inside shape probes
+        self.fold_depth = 0              # >0 inside a per-element fold
 
     def fresh(self, hint: str) -> str:
         return f"{hint}{next(self.ids)}"
 
     def emit(self, line: str) -> None:
+        self.emitted += 1
         if not self.dry:
             self.lines.append("  " * self.indent + line)
 
@@ -150,6 +180,94 @@ def _materialise(g: Gen, v, buf: str, shape: tuple) -> None:
     rec(v, shape, "0")
 
 
+class NotElementwise(Exception):
+    pass
+
+
+_IDENT = re.compile(r"[A-Za-z_][A-Za-z_0-9]*")
+
+
+@functools.lru_cache(maxsize=65536)
+def _same_index(a: str, b: str) -> bool:
+    """Do two generated index expressions (non-negative ints, + * / % min
+    max) denote the same value?  Equal text, or equal under 16 random
+    assignments of their variables (the layout algebra only produces
+    affine / div / mod forms, e.g. ((q / 32) * 32 + q % 32) == q)."""
+    if a == b:
+        return True
+    names = sorted((set(_IDENT.findall(a)) | set(_IDENT.findall(b))) - {"min", "max"})
+    pa, pb = a.replace("/", "//"), b.replace("/", "//")
+    rng = random.Random(hash((a, b)) & 0xFFFFFFFF)
+    try:
+        for _ in range(16):
+            env = {n: rng.randrange(0, 4096) for n in names}
+            env.update(min=min, max=max)
+            if eval(pa, {"__builtins__": {}}, env) != eval(pb, {"__builtins__": {}}, env):
+                return False
+    except Exception:
+        return False
+    return True
+
+
+def _sym_acc(g: Gen, shape: tuple, path: list, code: str, depth: int = 0):
+    """The accumulator as seen by one output element's fold: only element
+    `path` exists (as the scalar `code`); any other index raises (except in
+    shape probes, which index with placeholders)."""
+    if depth == len(shape):
+        return Scal(code)
+
+    def elem(i):
+        if not g.probing and not _same_index(i, path[depth]):
+            raise NotElementwise()
+        return _sym_acc(g, shape, path, code, depth + 1)
+    return Arr(shape[depth], elem, tuple(shape[depth + 1:]))
+
+
+def _lazy_nd(shape: tuple, leaf, path=()):
+    """An array value whose element at a full index path is leaf(path)."""
+    if len(path) == len(shape):
+        return leaf(list(path))
+    return Arr(shape[len(path)], lambda i: _lazy_nd(shape, leaf, path + (i,)), tuple(shape[len(path) + 1:]))
+
+
+def _fold_element(g: Gen, op: Fn, init, xs: Arr, shape: tuple, path: list):
+    acc = g.fresh("acc")
+    v0 = init
+    for q in path:
+        v0 = v0.elem(q)
+    g.emit(f"float {acc} = {v0.code};")
+    k = g.fresh("k")
+    g.open(f"for (int {k} = 0; {k} < {xs.size}; ++{k}) {{")
+    g.fold_depth += 1
+    try:
+        v = op.apply(_sym_acc(g, shape, path, acc)).apply(xs.elem(k))
+        for q in path:
+            v = v.elem(q)
+    finally:
+        g.fold_depth -= 1
+    if not isinstance(v, Scal):
+        raise CodegenError("reduce operator returned a non-scalar element")
+    g.emit(f"{acc} = {v.code};")
+    g.close()
+    return Scal(acc)
+
+
+def _is_elementwise(g: Gen, op: Fn, init, xs: Arr, shape: tuple) -> bool:
+    """Does element e of op(acc)(x) read acc at e only?  Probed on symbolic
+    indices in dry mode; then each demanded element of the reduce is its own
+    scalar left fold -- the interpreter's order (interp.py:84-89) per element."""
+    path = [f"__e{d}__" for d in range(len(shape))]
+    try:
+        g.dry_run(lambda: _fold_element(g, op, init, xs, shape, path))
+    except NotElementwise:
+        return False
+    return True
+
+
+def _lazy_reduce(g: Gen, op: Fn, init, xs: Arr, shape: tuple):
+    return _lazy_nd(shape, lambda path: _fold_element(g, op, init, xs, shape, path))
+
+
 def _reduce(g: Gen, op: Fn, init, xs: Arr):
     if isinstance(init, Scal):
         acc = g.fresh("acc")
@@ -164,18 +282,25 @@ def _reduce(g: Gen, op: Fn, init, xs: Arr):
         return Scal(acc)
     if isinstance(init, Arr):
         shape = shape_of(init)
+        # inside an element fold the enclosing check covers this reduce too
+        # (it evaluates the whole nest at a symbolic element)
+        if g.elementwise and (g.fold_depth > 0 or _is_elementwise(g, op, init, xs, shape)):
+            return _lazy_reduce(g, op, init, xs, shape)
+        g.materialised += 1
         n = 1
         for d in shape:
             n *= d
-        cur, nxt = g.fresh("accbuf"), g.fresh("nxtbuf")
-        g.emit(f"float {cur}[{n}], {nxt}[{n}];")
+        # two buffers, swapped by pointer after every step
+        ba, bb = g.fresh("accbuf"), g.fresh("accbuf")
+        cur, nxt = g.fresh("cur"), g.fresh("nxt")
+        g.emit(f"float {ba}[{n}], {bb}[{n}];")
+        g.emit(f"float* {cur} = {ba}; float* {nxt} = {bb};")
         _materialise(g, init, cur, shape)
         k = g.fresh("k")
         g.open(f"for (int {k} = 0; {k} < {xs.size}; ++{k}) {{")
         v = op.apply(_buffer_view(g, cur, shape)).apply(xs.elem(k))
         _materialise(g, v, nxt, shape)
-        j = g.fresh("c")
-        g.emit(f"for (int {j} = 0; {j} < {n}; ++{j}) {cur}[{j}] = {nxt}[{j}];")
+        g.emit(f"{{ float* sw = {cur}; {cur} = {nxt}; {nxt} = sw; }}")
         g.close()
         return _buffer_view(g, cur, shape)
     raise CodegenError("pair-valued reduce accumulators are not supported")
@@ -188,14 +313,32 @@ def _prim(g: Gen, p) -> object:
             def map_xs(xs):
                 if not isinstance(xs, Arr):
                     raise CodegenError(f"{k} expects an array")
-                elem_shape = g.dry_run(lambda: _shape_or_scalar(f.apply(xs.elem("0"))))
-                return Arr(xs.size, lambda i: f.apply(xs.elem(i)), elem_shape)
+                before = g.emitted
+                g.probing += 1
+                try:
+                    probe = g.dry_run(lambda: f.apply(xs.elem("0")))
+                finally:
+                    g.probing -= 1
+                emits = g.emitted > before
+                elem_shape = _shape_or_scalar(probe)
+                lazy = Arr(xs.size, lambda i: f.apply(xs.elem(i)), elem_shape)
+                n = xs.size
+                for d in elem_shape:
+                    n *= d
+                if g.strict_maps and emits and not isinstance(probe, Pair) and n <= STRICT_MAP_MAX:
+                    # the body computes (a reduce): evaluate each element once into
+                    # a per-thread buffer instead of once per consumer read
+                    buf = g.fresh("mbuf")
+                    g.emit(f"float {buf}[{n}];")
+                    _write(g, lazy, _out_buffer(buf, (xs.size,) + elem_shape))
+                    return _buffer_view(g, buf, (xs.size,) + elem_shape)
+                return lazy
             return Fn(map_xs)
         return Fn(map_f)
     if k in ("reduce", "reduceSeq", "reduceSeqUnroll"):
         return Fn(lambda op: Fn(lambda init: Fn(lambda xs: _reduce(g, op, init, xs))))
     if k == "zip":
-        return Fn(lambda a: Fn(lambda b: Arr(a.size, lambda i: Pair(a.elem(i), b.elem(i)), ())))
+        return Fn(lambda a: Fn(lambda b: Arr(a.size, lambda i: Pair(lambda: a.elem(i), lambda: b.elem(i)), ())))
     if k == "fst":
         return Fn(lambda pr: pr.a)
     if k == "snd":
@@ -284,6 +427,126 @@ def _compile(g: Gen, e, env):
 
 
 # ----------------------------------------------------------------------------
+# destination passing: where a value's elements are written
+
+STRICT_MAP_MAX = 4096      # floats: strict (materialised) maps stay per-thread arrays
+PAR_LEVELS = 2             # outermost map levels distributed over threads
+
+
+@dataclass
+class Out:
+    """An acceptor: `lval` for a scalar destination, else `size` + `at(i)`."""
+    size: int = 0
+    at: Callable[[str], "Out"] = None
+    lval: str = ""
+
+
+def _out_buffer(buf: str, shape: tuple, base: str = "0") -> Out:
+    if not shape:
+        return Out(lval=f"{buf}[{base}]")
+    stride = 1
+    for d in shape[1:]:
+        stride *= d
+    return Out(shape[0], lambda i: _out_buffer(buf, shape[1:], f"({base} + ({i}) * {stride})"))
+
+
+def _out_join(out: Out, m: int) -> Out:
+    """X : [n/m][m] written into out : [n]."""
+    return Out(out.size // m, lambda i: Out(m, lambda j: out.at(f"(({i}) * {m} + ({j}))")))
+
+
+def _out_split(out: Out, n: int) -> Out:
+    """X : [k*n] written into out : [k][n]."""
+    return Out(out.size * n, lambda q: out.at(f"(({q}) / {n})").at(f"(({q}) % {n})"))
+
+
+def _out_transpose(out: Out) -> Out:
+    """X : [m][n] written into out : [n][m]."""
+    m = out.at("0").size
+    return Out(m, lambda i: Out(out.size, lambda j: out.at(j).at(i)))
+
+
+def _write(g: Gen, v, out: Out) -> None:
+    """Emit loops storing every scalar of value `v` into `out`."""
+    if out.lval:
+        if not isinstance(v, Scal):
+            raise CodegenError("the program's result is not an array of scalars")
+        g.emit(f"{out.lval} = {v.code};")
+        return
+    if not isinstance(v, Arr):
+        raise CodegenError("the program's result is not an array of scalars")
+    i = g.fresh("w")
+    g.open(f"for (int {i} = 0; {i} < {v.size}; ++{i}) {{")
+    _write(g, v.elem(i), out.at(i))
+    g.close()
+
+
+LAYOUT_PRIMS = ("join", "asScalar", "split", "asVector", "transpose", "toMem", "id")
+
+
+def _layout_out(p, out: Out, x_shape: tuple) -> Out:
+    """Destination for X such that writing X there writes p(X) into `out`."""
+    if p.kind in ("join", "asScalar"):
+        return _out_join(out, x_shape[1])
+    if p.kind in ("split", "asVector"):
+        return _out_split(out, p.nats[0])
+    if p.kind == "transpose":
+        return _out_transpose(out)
+    return out
+
+
+def _shape_dry(g: Gen, e, env) -> tuple:
+    return g.dry_run(lambda: _shape_or_scalar(_compile(g, e, env)))
+
+
+def _accept(g: Gen, e, env, out: Out, par: int) -> None:
+    """Write the value of term `e` into `out`, following the term's own
+    producer structure (maps become loops -- the outermost PAR_LEVELS of them
+    thread indices -- layout primitives transform the destination, reduces
+    run once), so no element is computed more than once."""
+    ir = S().ir
+    head, args = ir.spine(e)
+    if isinstance(head, ir.Lam) and args:                     # (fun x => body)(a) ...
+        env2 = {**env, head.param: _compile(g, args[0], env)}
+        return _accept(g, ir.app(head.body, *args[1:]), env2, out, par)
+    if isinstance(head, ir.Prim):
+        k = head.kind
+        if k in ir.MAP_KINDS and len(args) == 2:
+            f, xs = args
+            if isinstance(f, ir.Prim) and f.kind in LAYOUT_PRIMS:
+                # map(join)(X) etc.: a per-element destination transform, no loop
+                shp = _shape_dry(g, xs, env)
+                return _accept(g, xs, env, Out(shp[0], lambda i: _layout_out(f, out.at(i), shp[1:])), par)
+            xv = _compile(g, xs, env)
+            if not isinstance(xv, Arr):
+                raise CodegenError(f"{k} expects an array")
+            if par > 0:
+                i = f"par{len(g.par_sizes)}"
+                g.par_sizes.append(xv.size)
+                _accept_fn(g, f, env, xv.elem(i), out.at(i), par - 1)
+            else:
+                i = g.fresh("i")
+                g.open(f"for (int {i} = 0; {i} < {xv.size}; ++{i}) {{")
+                _accept_fn(g, f, env, xv.elem(i), out.at(i), 0)
+                g.close()
+            return
+        if len(args) == 1 and k in LAYOUT_PRIMS:
+            shp = _shape_dry(g, args[0], env)
+            return _accept(g, args[0], env, _layout_out(head, out, shp), par)
+    _write(g, _compile(g, e, env), out)
+
+
+def _accept_fn(g: Gen, f, env, arg, out: Out, par: int) -> None:
+    ir = S().ir
+    if isinstance(f, ir.Lam):
+        return _accept(g, f.body, {**env, f.param: arg}, out, par)
+    fv = _compile(g, f, env)
+    if not isinstance(fv, Fn):
+        raise CodegenError("map over a non-function")
+    _write(g, fv.apply(arg), out)
+
+
+# ----------------------------------------------------------------------------
 # kernels
 
 @dataclass(frozen=True)
@@ -292,11 +555,13 @@ class Compiled:
     source: str
     in_shapes: tuple       # per input: array shape
     out_shape: tuple
+    threads: int = 1       # threads launched
+    mode: str = ""         # "per-scalar" or "destination-passing"
 
 
 def compile_term(term) -> Compiled:
     """CUDA source of `term` = fun(x0 : T0 => ... fun(xn : Tn => body)) over
-    f32 arrays; one thread per output scalar."""
+    f32 arrays (see the module docstring for the two thread mappings)."""
     s = S()
     ir, tc = s.ir, s.typecheck
     try:
@@ -311,40 +576,78 @@ def compile_term(term) -> Compiled:
         params.append((body.param, _type_shape(t.arg)))
         t, body = t.res, body.body
     out_shape = _type_shape(t)
+    if not out_shape:
+        raise CodegenError("the program's result is not an array of scalars")
+    g = _per_scalar_kernel(body, params, out_shape)
+    if g.materialised:
+        # a reduce with a non-elementwise array accumulator: computing one output
+        # scalar per thread would rebuild that accumulator per scalar, so write
+        # the result in the term's own structure instead (destination passing)
+        g = _dps_kernel(body, params, out_shape)
+    name = "elv_generated"
+    args = ", ".join([f"const float* __restrict__ in{i}" for i in range(len(params))] +
+                     ["float* __restrict__ out"])
+    src = "\n".join([f'extern "C" __global__ void __launch_bounds__(128) {name}({args}) {{'] + g.head +
+                    g.consts + g.lines + ["}"])
+    return Compiled(name, src, tuple(shp for _, shp in params), out_shape, g.threads, g.mode)
+
+
+def _inputs_env(g: Gen, params) -> dict:
+    env = {}
+    for idx, (p, shp) in enumerate(params):
+        env[p] = _buffer_view(g, f"in{idx}", shp) if shp else Scal(f"in{idx}[0]")
+    return env
+
+
+def _per_scalar_kernel(body, params, out_shape) -> Gen:
+    """Mode A: one thread per output scalar; lifted (elementwise) array
+    reduces are folded per demanded element, so nothing is recomputed."""
     g = Gen()
+    env = _inputs_env(g, params)
     total = 1
     for d in out_shape:
         total *= d
-    # index decomposition of the thread's output element
-    head = [f"  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;",
-            f"  if (t >= {total}LL) return;"]
-    rem = "t"
-    idx_names = []
+    g.head = [f"  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;",
+              f"  if (t >= {total}LL) return;"]
+    rem, names = "t", []
     for level, d in enumerate(out_shape):
         stride = 1
         for dd in out_shape[level + 1:]:
             stride *= dd
-        nm = f"o{level}"
-        head.append(f"  const int {nm} = (int)(({rem}) / {stride}LL);")
-        head.append(f"  const long long r{level} = ({rem}) % {stride}LL;")
+        g.head.append(f"  const int o{level} = (int)(({rem}) / {stride}LL);")
+        g.head.append(f"  const long long r{level} = ({rem}) % {stride}LL;")
         rem = f"r{level}"
-        idx_names.append(nm)
-    env = {}
-    for idx, (p, shp) in enumerate(params):
-        env[p] = _buffer_view(g, f"in{idx}", shp) if shp else Scal(f"in{idx}[0]")
-    result = _compile(g, body, env)
-    v = result
-    for nm in idx_names:
+        names.append(f"o{level}")
+    v = _compile(g, body, env)
+    for nm in names:
+        if not isinstance(v, Arr):
+            raise CodegenError("the program's result is not an array of scalars")
         v = v.elem(nm)
     if not isinstance(v, Scal):
         raise CodegenError("the program's result is not an array of scalars")
     g.emit(f"out[t] = {v.code};")
-    name = "elv_generated"
-    args = ", ".join([f"const float* __restrict__ in{i}" for i in range(len(params))] +
-                     ["float* __restrict__ out"])
-    src = "\n".join([f'extern "C" __global__ void __launch_bounds__(128) {name}({args}) {{'] + head +
-                    g.consts + g.lines + ["}"])
-    return Compiled(name, src, tuple(shp for _, shp in params), out_shape)
+    g.threads, g.mode = total, "per-scalar"
+    return g
+
+
+def _dps_kernel(body, params, out_shape) -> Gen:
+    """Mode B: destination passing; the outermost PAR_LEVELS maps are the
+    thread index, small computing maps are materialised per thread."""
+    g = Gen()
+    g.strict_maps = True
+    env = _inputs_env(g, params)
+    _accept(g, body, env, _out_buffer("out", out_shape), PAR_LEVELS)
+    total = 1
+    for d in g.par_sizes:
+        total *= d
+    g.head = [f"  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;",
+              f"  if (t >= {total}LL) return;"]
+    stride = total
+    for lvl, d in enumerate(g.par_sizes):
+        stride //= d
+        g.head.append(f"  const int par{lvl} = (int)((t / {stride}LL) % {d}LL);")
+    g.threads, g.mode = total, "destination-passing"
+    return g
 
 
 def _type_shape(t) -> tuple:
@@ -359,6 +662,32 @@ def _type_shape(t) -> tuple:
     if t != ir.F32:
         raise CodegenError(f"inputs/outputs must be f32 arrays, got {ir.format_type(t)}")
     return tuple(dims)
+
+
+def cpu_source(c: Compiled) -> str:
+    """The generated kernel wrapped as plain C++ (thread loop on the host), so
+    tests can check code generation against the reference interpreter
+    without a GPU.  Compiled with -ffp-contract=off it performs the same fp32
+    operations in the same order as the NVRTC (--fmad=false) build."""
+    n = len(c.in_shapes)
+    call = ", ".join([f"ins[{i}]" for i in range(n)] + ["out"])
+    return "\n".join([
+        "#include <algorithm>",
+        "using std::min; using std::max;",
+        "struct elv_dim3 { unsigned x, y, z; };",
+        "static elv_dim3 blockIdx, threadIdx, blockDim;",
+        "#define __global__",
+        "#define __launch_bounds__(x)",
+        "#define __restrict__",
+        c.source,
+        'extern "C" void elv_run_cpu(const float* const* ins, float* out, long long threads) {',
+        "  blockDim.x = 128;",
+        "  for (long long t = 0; t < threads; ++t) {",
+        "    blockIdx.x = (unsigned)(t / 128); threadIdx.x = (unsigned)(t % 128);",
+        f"    {c.name}({call});",
+        "  }",
+        "}",
+    ])
 
 
 # ----------------------------------------------------------------------------
@@ -397,9 +726,7 @@ class Kernel:
         import ctypes
         import numpy as np
         d = self.driver
-        total = 1
-        for x in self.c.out_shape:
-            total *= x
+        total = self.c.threads
         ptrs = [ctypes.c_void_p(t.data_ptr()) for t in list(inputs) + [out]]
         arg_ptrs = np.array([ctypes.addressof(p) for p in ptrs], dtype=np.uint64)
         block = 128

@@ -17,8 +17,8 @@ pytestmark = pytest.mark.gpu
 
 def _inputs(term, seed=3):
     c = codegen.compile_term(term)
-    return [synth.matrix(*shp, seed, i) if len(shp) == 2 else synth.uniform(shp[0], seed, i)
-            for i, shp in enumerate(c.in_shapes)]
+    return [synth.matrix(*shp, seed, i) if len(shp) == 2 else
+            synth.uniform(int(np.prod(shp)), seed, i).reshape(shp) for i, shp in enumerate(c.in_shapes)]
 
 
 @pytest.mark.parametrize("name,term", list(corpus().items()))
