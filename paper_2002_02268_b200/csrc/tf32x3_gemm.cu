@@ -44,16 +44,16 @@ constexpr int TMEM_COLS = 512;                    // pair kernel: D_big + D_smal
 // The 1-CTA kernel is templated on its N tile (256, 128 or 64): narrow tiles
 // give small problems (e.g. 1024^3: 32 tiles of 128x256 for 148 SMs) more
 // CTAs.  Per-element arithmetic does not depend on the tile shape.
-template <int TBN> struct OneCfg {
-  static constexpr int B_TILE = TBN * BK * 4;
-  static constexpr int STAGE = 2 * A_TILE_BYTES + 2 * B_TILE;
+template <int TBN, int TBK = BK> struct OneCfg {
+  static constexpr int A_TILE = BM * TBK * 4;
+  static constexpr int B_TILE = TBN * TBK * 4;
+  static constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;
   static constexpr int NST = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
   static constexpr int TMEM = 2 * TBN;             // D_big | D_small
   static constexpr int SMEM = NST * STAGE + 256 + 1024;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
                                     ((uint32_t)(BM >> 4) << 24);
 };
-
 inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
 // ----------------------------------------------------------------------------
@@ -194,17 +194,20 @@ struct TileSched {
   }
 };
 
-template <int TBN>
+template <int TBN, int TBK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
           float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
           unsigned int* __restrict__ wave_ctr) {
-  constexpr int STAGES = OneCfg<TBN>::NST;
-  constexpr int STAGE_BYTES = OneCfg<TBN>::STAGE;
-  constexpr int B_TILE_BYTES = OneCfg<TBN>::B_TILE;
+  using Cfg = OneCfg<TBN, TBK>;
+  constexpr int STAGES = Cfg::NST;
+  constexpr int STAGE_BYTES = Cfg::STAGE;
+  constexpr int B_TILE_BYTES = Cfg::B_TILE;
+  constexpr int A_TILE_BYTES = Cfg::A_TILE;
+  constexpr int BK = TBK;
   constexpr int BN = TBN;
-  constexpr uint32_t kIdesc = OneCfg<TBN>::IDESC;
+  constexpr uint32_t kIdesc = Cfg::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -228,7 +231,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)), "r"(OneCfg<TBN>::TMEM));
+                     smem_u32(tmem_holder)), "r"(Cfg::TMEM));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -277,10 +280,10 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          const uint64_t ahi = umma_desc_sw64(st);
-          const uint64_t alo = umma_desc_sw64(st + A_TILE_BYTES);
-          const uint64_t bhi = umma_desc_sw64(st + 2 * A_TILE_BYTES);
-          const uint64_t blo = umma_desc_sw64(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+          const uint64_t ahi = umma_desc_k<TBK>(st);
+          const uint64_t alo = umma_desc_k<TBK>(st + A_TILE_BYTES);
+          const uint64_t bhi = umma_desc_k<TBK>(st + 2 * A_TILE_BYTES);
+          const uint64_t blo = umma_desc_k<TBK>(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t koff = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along the row
@@ -341,7 +344,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(OneCfg<TBN>::TMEM));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM));
   }
 }
 
@@ -907,28 +910,42 @@ static int one_cta_bn(int M, int N) {
   return best;
 }
 
-template <int TBN>
+template <int TBN, int TBK>
 static int launch_one(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo, float* C,
                       int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st) {
+  using Cfg = OneCfg<TBN, TBK>;
   CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
-  int rc = make_map(&m_ahi, a_hi, M, Kp, BM);
-  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM);
-  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, TBN);
-  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, TBN);
+  int rc = make_map(&m_ahi, a_hi, M, Kp, BM, TBK);
+  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM, TBK);
+  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, TBN, TBK);
+  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, TBN, TBK);
   if (rc) return rc;
   static int attr_dev = -1;
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3<TBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         OneCfg<TBN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3<TBN, TBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
     attr_dev = dev;
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + TBN - 1) / TBN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   unsigned int* ctr = tiles > grid ? wave_counter(dev, st) : nullptr;
-  k7_tf32x3<TBN><<<grid, NUM_THREADS, OneCfg<TBN>::SMEM, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc,
-                                                                Kp / BK, with_lolo(K), tile_group(16), ctr);
+  k7_tf32x3<TBN, TBK><<<grid, NUM_THREADS, Cfg::SMEM, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc,
+                                                             Kp / TBK, with_lolo(K), tile_group(16), ctr);
   return check_launch("gemm_parallel_tf32x3");
+}
+
+// K depth of a stage: 32 (128 B rows, 128B swizzle) for the narrow tiles --
+// measured 1024^3 BN=64: 26.6 us vs 30.7 us at BK=16 -- but 16 for BN=256,
+// whose 96 KB BK=32 stage would leave only two stages.  ELV_TF32X3_BK forces.
+static int one_cta_bk(int bn) {
+  static int forced = -2;
+  if (forced == -2) {
+    forced = env_int("ELV_TF32X3_BK", -1);
+    if (forced != 16 && forced != 32) forced = -1;
+  }
+  if (forced > 0) return forced;
+  return bn == 256 ? 16 : 32;
 }
 
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
@@ -944,9 +961,14 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   if (pm == 16) return launch_pair<16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   if (pm == 32) return launch_pair<32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   const int bn = one_cta_bn(M, N);
-  if (bn == 64) return launch_one<64>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  if (bn == 128) return launch_one<128>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  return launch_one<256>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (one_cta_bk(bn) == 32) {
+    if (bn == 64) return launch_one<64, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+    if (bn == 128) return launch_one<128, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+    return launch_one<256, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  }
+  if (bn == 64) return launch_one<64, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (bn == 128) return launch_one<128, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  return launch_one<256, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
 }
 
 // elv_gemm workspace for variant 7 = [A planes | B planes]
