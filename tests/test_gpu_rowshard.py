@@ -176,3 +176,26 @@ def test_c_abi_rowshard_single_process(cuda):
         assert torch.equal(C, ref)
     finally:
         lib.elv_nccl_destroy()
+
+
+def test_bench_two_ranks_sharing_one_gpu(cuda, tmp_path):
+    """bench.py's N>1 path (torchrun, PipelinedRowShardGemm, barriers,
+    max-over-ranks timing, rank-0 JSON line) with two ranks sharing cuda:0
+    over gloo (ELV_BENCH_SHARE_GPU=1, test-only); NCCL itself needs one GPU
+    per rank."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ELV_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(repo, "bench.py"),
+           "--gpus", "2", "--M", "2048", "--N", "2048", "--K", "1024", "--steps", "3", "--warmup", "3",
+           "--no-cpu-baseline"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=repo)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"] == "rowshard2"
