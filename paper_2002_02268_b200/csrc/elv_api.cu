@@ -25,6 +25,15 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ELV_PDL");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v != 0;
+}
+
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -220,12 +229,11 @@ int elv_gemm_prepare(int variant, const float* A, const float* B, int M, int N, 
     case ELV_ARRAYPACKING:
     case ELV_CACHEBLOCKS:
       return launch_pack_b(B, static_cast<float*>(workspace), K, N, ldb, st);
-    case ELV_PARALLEL: {
-      int rc2 = launch_pack_b(B, static_cast<float*>(workspace), K, N, ldb, st);
-      if (rc2 || !parallel_uses_packed_a(M, N)) return rc2;
-      return launch_pack_a(A, reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + elv_pack_b_bytes(K, N)),
-                           M, K, lda, st);
-    }
+    case ELV_PARALLEL:
+      if (!parallel_uses_packed_a(M, N)) return launch_pack_b(B, static_cast<float*>(workspace), K, N, ldb, st);
+      return launch_pack_ab(B, static_cast<float*>(workspace), K, N, ldb, A,
+                            reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + elv_pack_b_bytes(K, N)), M,
+                            lda, st);
     case ELV_PARALLEL_TF32X3:
       return tf32x3_prepare(A, B, M, N, K, lda, ldb, workspace, workspace_bytes, st);
     default:

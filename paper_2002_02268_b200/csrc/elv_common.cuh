@@ -6,6 +6,9 @@
 #include <stddef.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/elevate_b200.h"
 
@@ -13,6 +16,33 @@ namespace elv {
 
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
+
+// Programmatic dependent launch: a GEMM that follows its operand-preparation
+// kernel on the stream is launched with programmatic stream serialization,
+// so its prologue (TMEM allocation, barrier init, descriptor prefetch) runs
+// while the preparation drains; griddep_wait() then blocks until the
+// preceding grid has completed and its writes are visible.  Without the
+// attribute (or ELV_PDL=0) the wait is a no-op and ordering is the stream's.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 constexpr int kPanel = 32;          // packB block (rules.py:516 default 32)
 constexpr int kPackAlign = 256;     // packed column count padded to 8 panels (widest SIMT tile)
@@ -36,6 +66,8 @@ int launch_simt(int variant, const float* A, const float* B, const float* packed
 int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStream_t st);
 size_t pack_a_bytes(int M, int K);
 int launch_pack_a(const float* A, float* packedA, int M, int K, int lda, cudaStream_t st);
+int launch_pack_ab(const float* B, float* packedB, int K, int N, int ldb, const float* A, float* packedA, int M,
+                   int lda, cudaStream_t st);
 int launch_parallel_packed(const float* packedA, const float* packedB, float* C, int M, int N, int K, int ldc,
                            cudaStream_t st);
 bool parallel_uses_packed_a(int M, int N);

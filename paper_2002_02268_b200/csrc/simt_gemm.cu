@@ -714,6 +714,7 @@ k6_sgemm_cp(const float* __restrict__ PA, const float* __restrict__ PB, float* _
   const int num_tiles = tiles_m * tiles_n;
   const int nkb = (K + CP_BK - 1) / CP_BK;
 
+  griddep_wait();                                   // packed operands from k_pack_ab
   for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     const TileCoord tc = tile_of(t, tiles_m, tiles_n);
     const int row0 = tc.m * BM, col0 = tc.n * BN;
@@ -836,6 +837,7 @@ k6_sgemm_ffma2(const float* __restrict__ PA, const float* __restrict__ PB, float
   const int num_tiles = tiles_m * tiles_n;
   const int nkb = (K + CP_BK - 1) / CP_BK;
 
+  griddep_wait();                                   // packed operands from k_pack_ab
   for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     const TileCoord tc = tile_of(t, tiles_m, tiles_n);
     const int row0 = tc.m * BM, col0 = tc.n * BN;
@@ -949,6 +951,7 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
   const int num_tiles = tiles_m * tiles_n;
   const int nkb = (K + SM_BK - 1) / SM_BK;
 
+  griddep_wait();                                   // packed operands from k_pack_ab
   for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     const int tm = t % tiles_m, tn = t / tiles_m;      // column-major: neighbours share B panels
     const int row0 = tm * SM_BM, col0 = tn * SM_BN;
@@ -1042,10 +1045,10 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
 
 // packA: packedA[p][k][r] = A[128p + r][k], zero past M.  32x32 tiles through
 // SMEM so both the row reads of A and the panel-row writes coalesce.
-__global__ void __launch_bounds__(256)
-k_pack_a(const float* __restrict__ A, float* __restrict__ PA, int M, int K, int lda) {
+__device__ __forceinline__ void pack_a_block(const float* __restrict__ A, float* __restrict__ PA, int M, int K,
+                                             int lda, int bx, int by) {
   __shared__ float tt[32][33];
-  const int k0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int k0 = bx * 32, r0 = by * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -1058,6 +1061,10 @@ k_pack_a(const float* __restrict__ A, float* __restrict__ PA, int M, int K, int 
     const int k = k0 + ty + 8 * i, r = r0 + tx;
     if (k < K) PA[((size_t)(r >> 7) * K + k) * 128 + (r & 127)] = tt[tx][ty + 8 * i];
   }
+}
+__global__ void __launch_bounds__(256)
+k_pack_a(const float* __restrict__ A, float* __restrict__ PA, int M, int K, int lda) {
+  pack_a_block(A, PA, M, K, lda, blockIdx.x, blockIdx.y);
 }
 
 struct SgemmCfg { void (*fn)(const float*, const float*, float*, int, int, int, int, int); int minb, bm, bn; };
@@ -1081,12 +1088,11 @@ static int sgemm_cfg() {
 // TVM packedB PAPER.md:49-50).  Pure layout transform, HBM-bound: every
 // thread moves one float4; reads are coalesced along B's rows, writes along
 // the panel rows.
-__global__ void __launch_bounds__(256)
-k_pack_b(const float* __restrict__ B, float* __restrict__ P, int K, int N, int ldb,
-         int panels, bool vecB) {
+__device__ __forceinline__ void pack_b_part(const float* __restrict__ B, float* __restrict__ P, int K, int N,
+                                            int ldb, int panels, bool vecB, int bx, int gx) {
   const long long total4 = (long long)panels * K * (kPanel / 4);
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total4;
-       q += (long long)gridDim.x * blockDim.x) {
+  for (long long q = bx * (long long)blockDim.x + threadIdx.x; q < total4;
+       q += (long long)gx * blockDim.x) {
     // q enumerates (k, p, c4) with c4 fastest so reads of a B row coalesce
     const int c4 = (int)(q & 7) * 4;
     const long long kp = q >> 3;
@@ -1104,6 +1110,22 @@ k_pack_b(const float* __restrict__ B, float* __restrict__ P, int K, int N, int l
     }
     *reinterpret_cast<float4*>(P + ((size_t)p * K + k) * kPanel + c4) = v;
   }
+}
+__global__ void __launch_bounds__(256)
+k_pack_b(const float* __restrict__ B, float* __restrict__ P, int K, int N, int ldb,
+         int panels, bool vecB) {
+  pack_b_part(B, P, K, N, ldb, panels, vecB, blockIdx.x, gridDim.x);
+}
+
+// the parallel variant's prepare in one launch: blocks [0, gb) pack B
+// (grid-stride), the rest pack A in 32x32 tiles (independent work)
+__global__ void __launch_bounds__(256)
+k_pack_ab(const float* __restrict__ B, float* __restrict__ P, int K, int N, int ldb, int panels, bool vecB,
+          int gb, const float* __restrict__ A, float* __restrict__ PA, int M, int lda, int gxa) {
+  griddep_launch_dependents();
+  const int b = blockIdx.x;
+  if (b < gb) pack_b_part(B, P, K, N, ldb, panels, vecB, b, gb);
+  else pack_a_block(A, PA, M, K, lda, (b - gb) % gxa, (b - gb) / gxa);
 }
 
 }  // namespace
@@ -1140,6 +1162,22 @@ bool parallel_uses_packed_a(int M, int N) {
 
 size_t pack_a_bytes(int M, int K) { return (size_t)((M + 127) / 128) * 128 * (size_t)K * sizeof(float); }
 
+int launch_pack_ab(const float* B, float* packedB, int K, int N, int ldb, const float* A, float* packedA, int M,
+                   int lda, cudaStream_t st) {
+  const int panels = (int)(packed_cols(N) / kPanel);
+  const bool vecB = ((reinterpret_cast<uintptr_t>(B) & 15u) == 0) && (ldb & 3) == 0;
+  const long long total4 = (long long)panels * K * (kPanel / 4);
+  long long gb = (total4 + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  if (gb > cap) gb = cap;
+  if (gb < 1) gb = 1;
+  const int gxa = (K + 31) / 32, gya = (M + 127) / 128 * 4;
+  const long long blocks = gb + (long long)gxa * gya;
+  if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "pack_ab: problem too large for one launch");
+  k_pack_ab<<<(unsigned)blocks, 256, 0, st>>>(B, packedB, K, N, ldb, panels, vecB, (int)gb, A, packedA, M, lda, gxa);
+  return check_launch("pack_ab");
+}
+
 int launch_pack_a(const float* A, float* packedA, int M, int K, int lda, cudaStream_t st) {
   dim3 grid((K + 31) / 32, (M + 127) / 128 * 4);
   k_pack_a<<<grid, 256, 0, st>>>(A, packedA, M, K, lda);
@@ -1160,7 +1198,9 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
     const long long tiles = (long long)((M + SM_BM - 1) / SM_BM) * ((N + SM_BN - 1) / SM_BN);
     long long grid = (long long)num_sms() * 4;
     if (grid > tiles) grid = tiles;
-    k6_sgemm_small<<<(unsigned)grid, 64, SM_SMEM, st>>>(packedA, packedB, C, M, N, K, ldc);
+    cudaError_t e = launch_pdl(k6_sgemm_small, dim3((unsigned)grid), dim3(64), (size_t)SM_SMEM, st, packedA, packedB,
+                               C, M, N, K, ldc);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_small: %s", cudaGetErrorString(e));
     return check_launch("gemm_parallel_small");
   }
   static int order = -1;
@@ -1182,7 +1222,9 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
   const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
   long long grid = num_sms();
   if (grid > tiles) grid = tiles;
-  fn<<<(unsigned)grid, 256, CP_SMEM, st>>>(packedA, packedB, C, M, N, K, ldc);
+  cudaError_t e = launch_pdl(fn, dim3((unsigned)grid), dim3(256), (size_t)CP_SMEM, st, packedA, packedB, C, M, N, K,
+                             ldc);
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel");
 }
 

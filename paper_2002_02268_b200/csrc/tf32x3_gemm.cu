@@ -238,6 +238,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  griddep_wait();                                   // operand planes from the preceding split kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -474,6 +475,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  griddep_wait();                                   // operand planes from the preceding split kernel
 
   // tile t: rows [mt*256, +256) (this CTA: + rank*128), cols [nt*256, +256) (this CTA stages + rank*128)
   auto coords = [&](int t, int& m0, int& n0) {
@@ -713,6 +715,7 @@ __global__ void __launch_bounds__(256)
 k_split_ab(const float* __restrict__ A, float* __restrict__ ahi, float* __restrict__ alo, int M, int lda,
            bool vecA, int gxa, int gya, const float* __restrict__ B, float* __restrict__ bhi,
            float* __restrict__ blo, int N, int ldb, int gxb, int K, int Kp) {
+  griddep_launch_dependents();
   const int b = blockIdx.x, ga = gxa * gya;
   if (b < ga) split_a_block(A, ahi, alo, M, K, lda, Kp, vecA, b % gxa, b / gxa, gya);
   else split_transpose_b_block<false>(B, bhi, blo, K, N, ldb, Kp, (b - ga) % gxb, (b - ga) / gxb);
@@ -838,8 +841,10 @@ static int launch_pair(const float* a_hi, const float* a_lo, const float* b_hi,
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
   unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;   // one wave: nothing to sync
-  k7_tf32x3_pair<BKT><<<2 * clusters, P_NUM_THREADS, PairCfg<BKT>::SMEM_BYTES, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT, with_lolo(K), tile_group(8), ctr);
+  cudaError_t e = launch_pdl(k7_tf32x3_pair<BKT>, dim3(2 * clusters), dim3(P_NUM_THREADS),
+                             (size_t)PairCfg<BKT>::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc,
+                             Kp / BKT, with_lolo(K), tile_group(8), ctr);
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3_pair");
 }
 static inline size_t planes_bytes(int rows, int K) {
@@ -930,8 +935,9 @@ static int launch_one(const float* a_hi, const float* a_lo, const float* b_hi, c
   const int tiles = ((M + BM - 1) / BM) * ((N + TBN - 1) / TBN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   unsigned int* ctr = tiles > grid ? wave_counter(dev, st) : nullptr;
-  k7_tf32x3<TBN, TBK><<<grid, NUM_THREADS, Cfg::SMEM, st>>>(m_ahi, m_alo, m_bhi, m_blo, C, M, N, ldc,
-                                                             Kp / TBK, with_lolo(K), tile_group(16), ctr);
+  cudaError_t e = launch_pdl(k7_tf32x3<TBN, TBK>, dim3(grid), dim3(NUM_THREADS), (size_t)Cfg::SMEM, st, m_ahi,
+                             m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / TBK, with_lolo(K), tile_group(16), ctr);
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3");
 }
 

@@ -97,8 +97,8 @@ class GemmCall:
     """A bound kernel call with its workspace, split into the two C-ABI
     phases (elv_gemm_prepare: operand layout transform; elv_gemm_compute:
     the GEMM kernel) so callers can time or overlap them separately.
-    Launches per call: prepare 0 (variants 0-3), 1 (4, 5), 1-2 (6: packB, and
-    packA when the workspace holds it), 1 (7: fused hi/lo split of A and B); compute 1."""
+    Launches per call: prepare 0 (variants 0-3), 1 (4, 5: packB; 6: packB, or
+    packA+packB fused; 7: fused hi/lo split of A and B); compute 1."""
 
     PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1}
 
@@ -110,8 +110,6 @@ class GemmCall:
         self.ws = (torch.empty(self.ws_bytes, device=A.device, dtype=torch.uint8)
                    if self.ws_bytes else None)
         self.launches = self.PREPARE_LAUNCHES[p.variant] + 1
-        if p.variant == 6 and self.ws_bytes > self.lib.elv_pack_b_bytes(p.K, p.N):
-            self.launches += 1                      # packA (large and small problems)
 
     def _args(self):
         return (self.ws.data_ptr() if self.ws is not None else None, self.ws_bytes,
