@@ -80,19 +80,26 @@ class RowShardGemm:
         return self.compute(A_shard, B, C_shard)
 
 
-def column_chunks(N: int, chunks: int, align: int = 256):
+def column_chunks(N: int, chunks: int, align: int = 256, first_weight: float = 1.0):
     """Split [0, N) into <= `chunks` column blocks, each a multiple of `align`
-    (the 3xTF32 tile width and the 256-column packB padding unit)."""
+    (the 3xTF32 tile width and the 256-column packB padding unit).  With
+    first_weight < 1 the first block is that fraction of the others: it is
+    the one whose broadcast nothing overlaps, so it should arrive early."""
     units = (N + align - 1) // align
     chunks = max(1, min(chunks, units))
-    base, extra = divmod(units, chunks)
-    out, u = [], 0
-    for c in range(chunks):
-        nu = base + (1 if c < extra else 0)
-        n0, n1 = u * align, min((u + nu) * align, N)
+    w = [first_weight] + [1.0] * (chunks - 1)
+    tot = sum(w)
+    bounds, acc = [0], 0.0
+    for x in w[:-1]:
+        acc += x
+        b = int(round(units * acc / tot))
+        bounds.append(min(max(b, bounds[-1] + 1), units - (chunks - len(bounds))))
+    bounds.append(units)
+    out = []
+    for u0, u1 in zip(bounds[:-1], bounds[1:]):
+        n0, n1 = u0 * align, min(u1 * align, N)
         if n1 > n0:
             out.append((n0, n1))
-        u += nu
     return out
 
 
@@ -105,10 +112,16 @@ class PipelinedRowShardGemm:
       all      : broadcast(P_c) on NCCL's stream (async, issued in order)
       all      : wait(P_c) -> C[:, chunk c] = A_shard . B[:, chunk c]
                  SIMT (variant 6): elv_gemm_prepacked on the packed chunk
-                 3xTF32 (variant 7): split_b_packed(P_c) + gemm_planes, with
-                 A's hi/lo planes made once per step while chunk 0 is in flight
-    Column blocks of C are independent, so the result is bit-identical to
-    the unchunked kernel's for the same per-tile arithmetic.
+                 3xTF32 (variant 7): split_b_packed(P_c) on a side stream as
+                 soon as P_c lands (overlapping the GEMM of chunk c-1), then
+                 gemm_planes; A's hi/lo planes are made once per step while
+                 chunk 0 is in flight
+    The first chunk is half the size of the others (nothing hides its
+    broadcast); with 4 chunks and N = 32768 the rest are 37 units of 256
+    columns, i.e. 16*37 = 592 = 8 full waves of 74 pair tiles per GEMM at 8
+    ranks (4096 rows each).  Column blocks of C are independent, so the
+    result is bit-identical to the unchunked kernel's for the same per-tile
+    arithmetic.
     """
 
     def __init__(self, plan, N: int, K: int, device, group=None, src: int = 0, chunks: int = 4,
@@ -124,7 +137,8 @@ class PipelinedRowShardGemm:
         self.stream = stream or torch.cuda.current_stream(device)
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.chunks = column_chunks(N, chunks)
+        self.chunks = column_chunks(N, chunks, first_weight=0.5 if chunks > 1 else 1.0)
+        self.prep = torch.cuda.Stream(device) if plan.variant == 7 else None
         self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
         M = plan.M
         if self.variant == 7:
@@ -161,23 +175,34 @@ class PipelinedRowShardGemm:
                         w.wait()
                 return C_shard
             if self.variant == 7:
+                # side stream: split each packed chunk as soon as it lands (after
+                # the previous step's GEMMs are done with the plane buffers)
+                self.prep.wait_stream(self.stream)
+                ready = []
+                with torch.cuda.stream(self.prep):
+                    pst = self.prep.cuda_stream
+                    for (n0, n1), w, bp in zip(self.chunks, works, self.b_planes):
+                        if w is not None:
+                            w.wait()                # the prep stream waits for chunk c
+                        self._check(lib.elv_tf32x3_split_b_packed(self._panel(n0).data_ptr(), K, n1 - n0,
+                                                                  bp.data_ptr(), pst), "split_b_packed")
+                        ev = torch.cuda.Event()
+                        ev.record(self.prep)
+                        ready.append(ev)
                 self._check(lib.elv_tf32x3_split_a(A_shard.data_ptr(), M, K, A_shard.stride(0),
                                                    self.a_planes.data_ptr(), st), "split_a")
-            for (n0, n1), w, bp in zip(self.chunks, works,
-                                      self.b_planes if self.variant == 7 else [None] * len(works)):
+                for (n0, n1), bp, ev in zip(self.chunks, self.b_planes, ready):
+                    self.stream.wait_event(ev)
+                    self._check(lib.elv_tf32x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(),
+                                                           C_shard.data_ptr() + 4 * n0, M, n1 - n0, K,
+                                                           C_shard.stride(0), st), "gemm_planes")
+                return C_shard
+            for (n0, n1), w in zip(self.chunks, works):
                 if w is not None:
                     w.wait()                        # compute stream waits for chunk c only
-                Pc = self._panel(n0)
-                Cc = C_shard.data_ptr() + 4 * n0
-                if self.variant == 7:
-                    self._check(lib.elv_tf32x3_split_b_packed(Pc.data_ptr(), K, n1 - n0, bp.data_ptr(), st),
-                                "split_b_packed")
-                    self._check(lib.elv_tf32x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(), Cc, M,
-                                                           n1 - n0, K, C_shard.stride(0), st), "gemm_planes")
-                else:
-                    self._check(lib.elv_gemm_prepacked(self.variant, A_shard.data_ptr(), Pc.data_ptr(), Cc, M,
-                                                       n1 - n0, K, A_shard.stride(0), C_shard.stride(0), st),
-                                "elv_gemm_prepacked")
+                self._check(lib.elv_gemm_prepacked(self.variant, A_shard.data_ptr(), self._panel(n0).data_ptr(),
+                                                   C_shard.data_ptr() + 4 * n0, M, n1 - n0, K, A_shard.stride(0),
+                                                   C_shard.stride(0), st), "elv_gemm_prepacked")
         return C_shard
 
 

@@ -76,3 +76,15 @@ def test_rowshard_gloo_world2(M, N, K):
     A = synth.matrix(M, K, 0, 0).astype(np.float64)
     B = synth.matrix(K, N, 0, 1).astype(np.float64)
     assert np.array_equal(C, (A @ B).astype(np.float32))
+
+
+@pytest.mark.parametrize("N,chunks", [(32768, 4), (2048, 4), (1000, 3), (256, 8), (300, 4), (4096, 1)])
+def test_column_chunks_partition(N, chunks):
+    """Broadcast chunks: a partition of [0, N) into 256-aligned blocks (but the
+    tail), at most `chunks` of them, the first about half the others."""
+    cs = D.column_chunks(N, chunks, first_weight=0.5)
+    assert cs[0][0] == 0 and cs[-1][1] == N and len(cs) <= chunks
+    assert all(a[1] == b[0] for a, b in zip(cs, cs[1:]))
+    assert all(n0 % 256 == 0 and n1 > n0 for n0, n1 in cs)
+    if N == 32768 and chunks == 4:
+        assert [(n1 - n0) // 256 for n0, n1 in cs] == [18, 37, 36, 37]
