@@ -253,3 +253,23 @@ def test_tf32x3_tile_widths_bitwise_identical(cuda, tmp_path, shape):
     A, B = synth.matrix(M, K, 11, 0), synth.matrix(K, N, 11, 1)
     ok, worst = oracle.check(outs[64], oracle.mm_f64(A, B), oracle.absprod_np(A, B), K)
     assert ok, worst
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3"])
+def test_output_beyond_2_pow_31_elements(cuda, variant):
+    """Maximum-size edge: C with more than 2^31 elements (8.6 GB), so every
+    row/column offset must be computed in 64 bits; rows at the far end
+    checked against the f64 oracle."""
+    M, N, K = 65536 + 128, 32768, 32
+    assert M * N > 2 ** 31
+    sched, tf = _sched(variant)
+    A, B = _device_inputs(M, N, K, 12, cuda)
+    term = schedules.apply_padded(sched, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf)
+    torch.cuda.synchronize()
+    rows = [0, 65535, 65536, M - 1]
+    Ah, Bh = A[rows].cpu().numpy(), B.cpu().numpy()
+    ok, worst = oracle.check(C[rows].cpu().numpy(), oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
+    assert ok, worst
+    del C
+    torch.cuda.empty_cache()
