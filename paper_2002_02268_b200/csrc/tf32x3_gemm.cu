@@ -38,7 +38,6 @@ namespace {
 
 constexpr int BM = 128, BK = 16;                  // BK fp32 = 64 B rows (SWIZZLE_64B)
 constexpr int NUM_THREADS = 192;
-constexpr int A_TILE_BYTES = BM * BK * 4;         // 8 KB
 constexpr int TMEM_COLS = 512;                    // pair kernel: D_big + D_small, 256 columns each
 
 // The 1-CTA kernel is templated on its N tile (256, 128 or 64): narrow tiles
