@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 import weakref
 
 import numpy as np
@@ -176,6 +177,10 @@ class HostPipeline:
         _lib.check(self.lib.elv_gemm_host_tiles(p.variant, p.M, p.N, p.K, ctypes.byref(r),
                                                 ctypes.byref(c)), "elv_gemm_host_tiles")
         self.tile = (r.value, c.value)
+        # one call at a time per workspace: concurrent callers (threads on
+        # other streams) would otherwise share A/B/C staging buffers
+        self._lock = threading.Lock()
+        self._done = None           # event: the previous call's work has drained
 
     def __call__(self, A_h: torch.Tensor, B_h: torch.Tensor, out_h: torch.Tensor,
                  sync: bool = True) -> torch.Tensor:
@@ -184,11 +189,16 @@ class HostPipeline:
             if t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != shape or t.stride(-1) != 1:
                 raise EvalError(f"host pipeline expects row-major fp32 host matrices {shape}")
         st = torch.cuda.current_stream(self.device)
-        with torch.cuda.device(self.device):
-            rc = self.lib.elv_gemm_host(p.variant, A_h.data_ptr(), B_h.data_ptr(), out_h.data_ptr(),
-                                        p.M, p.N, p.K, A_h.stride(0), B_h.stride(0), out_h.stride(0),
-                                        self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
-        _lib.check(rc, f"elv_gemm_host[{p.variant_name}]")
+        with self._lock:
+            if self._done is not None:
+                st.wait_event(self._done)     # previous call (maybe another stream) done with the workspace
+            with torch.cuda.device(self.device):
+                rc = self.lib.elv_gemm_host(p.variant, A_h.data_ptr(), B_h.data_ptr(), out_h.data_ptr(),
+                                            p.M, p.N, p.K, A_h.stride(0), B_h.stride(0), out_h.stride(0),
+                                            self.ws.data_ptr(), self.ws_bytes, st.cuda_stream)
+            _lib.check(rc, f"elv_gemm_host[{p.variant_name}]")
+            self._done = torch.cuda.Event()
+            self._done.record(st)
         if sync:
             st.synchronize()
         return out_h

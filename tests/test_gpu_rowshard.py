@@ -199,3 +199,38 @@ def test_bench_two_ranks_sharing_one_gpu(cuda, tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["config"]["parallelism"] == "rowshard2"
+
+
+def test_host_pipeline_concurrent_callers(cuda):
+    """Two Python threads on two streams sharing one cached host pipeline
+    (same plan -> same workspace): calls are serialised on the workspace, and
+    both results are exact."""
+    import threading
+    from paper_2002_02268_b200 import interp as I
+    M, N, K = 1024, 2048, 512
+    term = schedules.apply("parallel", M, N, K).term
+    ins = [(torch.from_numpy(synth.matrix(M, K, s, 0)).pin_memory(),
+            torch.from_numpy(synth.matrix(K, N, s, 1)).pin_memory()) for s in (21, 22)]
+    p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=True)
+    refs = [I.gemm(p, A.to(cuda), B.to(cuda)).cpu() for A, B in ins]
+    hp = I.host_pipeline(p, cuda)
+    outs = [torch.empty((M, N), pin_memory=True) for _ in ins]
+    errs = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream(cuda)
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    hp(ins[i][0], ins[i][1], outs[i])
+        except Exception as e:      # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
