@@ -129,6 +129,10 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h,
                   void* workspace, size_t workspace_bytes, void* stream);
 /* The tile shape elv_gemm_host uses (rows x cols). */
 int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols);
+/* Diagnostics: with ELV_HOST_TRACE=1 set, after the last elv_gemm_host on
+ * this thread completed, write up to `cap` (kind, ms since entry) float pairs
+ * (kind 0 = H2D item landed, 1 = tile GEMM done, 2 = tile D2H done). */
+int elv_gemm_host_trace(float* out, int cap);
 
 /* Synthetic inputs: X[i] = U(-1,1) with 24-bit resolution from
  * splitmix64((seed << 48) ^ (tensor_id << 40) ^ (offset + i)); bit-identical

@@ -36,12 +36,13 @@ struct HostPlan {
 
 // Tile sizes.  Small problems: one tile (plain H2D -> GEMM -> D2H).  Large:
 // 8-16 row blocks (multiples of the 256-row pair tile) x column chunks of
-// about 8192 columns (multiples of 256), so the first C tile is ready after
+// about 16384 columns (multiples of 256), so the first C tile is ready after
 // a small slice of A and one chunk of B have crossed PCIe and each GEMM
-// launch still fills several waves of the persistent grid.  Measured at
-// 32768 x 32768 x 8192 (3xTF32, gpurun_out/s2d): 2048x8192 and 4096x4096
-// tiles 97.6-98.1 ms, 4096x8192 100.6 ms, 8192x8192 102.1 ms; the D2H of C
-// (4 GiB at ~50 GB/s while H2D runs) is the bound.
+// launch still fills several waves of the persistent grid.  The D2H of C is
+// the bound, and a 2D copy's throughput grows with its row segment (32 KB
+// rows ~46-51 GB/s, contiguous 57 GB/s).  Measured at 32768 x 32768 x 8192
+// (3xTF32, gpurun_out/s2aa): 2048x16384 tiles 91.7 ms, 4096x16384 94.3,
+// 2048x8192 96.7, 2048x32768 101.5 (full rows start the D2H too late).
 HostPlan make_plan(int v, int M, int N, int K) {
   HostPlan p{};
   const double bytes = 4.0 * ((double)M * K + (double)K * N + (double)M * N);
@@ -55,8 +56,11 @@ HostPlan make_plan(int v, int M, int N, int K) {
     const int row_blocks = M >= 8192 ? fine : (M >= 2048 ? 8 : (M >= 512 ? 2 : 1));
     p.R = (int)up((size_t)ceil_div(M, row_blocks), 256);
     if (p.R > M) p.R = M;
-    if (N >= 16384) {
-      const int chunks = ceil_div(N, 8192);
+    // 3xTF32 (D2H-bound): 16384-column chunks (64 KB copy rows); SIMT
+    // (GEMM-bound): 8192, so the first B chunk lands sooner
+    const int cw = v == ELV_PARALLEL_TF32X3 ? 16384 : 8192;
+    if (N >= 2 * cw) {
+      const int chunks = ceil_div(N, cw);
       p.Nc = (int)up((size_t)ceil_div(N, chunks), 256);
       if (p.Nc > N) p.Nc = N;
     }
@@ -89,11 +93,18 @@ HostPlan make_plan(int v, int M, int N, int K) {
 }
 
 // Per-device copy streams and an event pool (library-internal, created once).
+// With ELV_HOST_TRACE=1 a second pool of timing events records when every
+// H2D item, tile GEMM and D2H copy finished (elv_gemm_host_trace reads them).
 struct DeviceRes {
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t d2h_extra[3] = {nullptr, nullptr, nullptr};   // more copy engines for D2H
+  cudaEvent_t end_extra[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> events;
+  std::vector<cudaEvent_t> tev;          // trace: [0] entry, then (kind, event) records
+  std::vector<int> tkind;                // 0 h2d, 1 tile, 2 d2h
   std::mutex mu;
 };
+thread_local int g_trace_dev = -1;
 DeviceRes g_res[64];
 
 int get_events(DeviceRes& r, size_t n) {
@@ -153,7 +164,17 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   if (r.h2d == nullptr) {
     CK(cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking), "create h2d stream");
     CK(cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking), "create d2h stream");
+    for (int q = 0; q < 3; ++q) {
+      CK(cudaStreamCreateWithFlags(&r.d2h_extra[q], cudaStreamNonBlocking), "create d2h stream");
+      CK(cudaEventCreateWithFlags(&r.end_extra[q], cudaEventDisableTiming), "create event");
+    }
   }
+  // D2H copies of a tile are split by rows over `nd` streams (copy engines)
+  int nd = 1;        // measured: 2-3 streams do not raise D2H throughput (gpurun_out/s2aa)
+  if (const char* e = getenv("ELV_HOST_D2H_STREAMS")) nd = atoi(e);
+  if (nd < 1) nd = 1;
+  if (nd > 4) nd = 4;
+  cudaStream_t d2hs[4] = {r.d2h, r.d2h_extra[0], r.d2h_extra[1], r.d2h_extra[2]};
   const int ntiles = p.nrb * p.ncb;
   // events: [0] entry, [1] h2d done, [2 .. 2+nrb) A blocks, [.. +ncb) B chunks, [.. +ntiles) tiles
   int rc = get_events(r, 2 + p.nrb + p.ncb + ntiles);
@@ -165,6 +186,21 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   cudaEvent_t* ev_t = ev_b + p.ncb;
 
   cudaStream_t st = (cudaStream_t)stream;
+  const bool trace = getenv("ELV_HOST_TRACE") && atoi(getenv("ELV_HOST_TRACE")) != 0;
+  size_t ntr = 0;
+  auto trace_rec = [&](int kind, cudaStream_t s2) -> int {
+    if (!trace) return ELV_OK;
+    if (r.tev.size() <= ntr) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return set_error(ELV_ECUDA, "gemm_host: trace event");
+      r.tev.push_back(e);
+      r.tkind.push_back(0);
+    }
+    r.tkind[ntr] = kind;
+    if (cudaEventRecord(r.tev[ntr++], s2) != cudaSuccess) return set_error(ELV_ECUDA, "gemm_host: trace record");
+    return ELV_OK;
+  };
+  if (trace) g_trace_dev = dev;
   uint8_t* base = reinterpret_cast<uint8_t*>(up(reinterpret_cast<uintptr_t>(workspace), kAlign));
   float* A_d = reinterpret_cast<float*>(base + p.off_a);
   float* B_d = reinterpret_cast<float*>(base + p.off_b);
@@ -174,8 +210,9 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
 
   // the copy streams start after everything already queued on the caller's stream
   CK(cudaEventRecord(ev_entry, st), "record entry");
+  if ((rc = trace_rec(-1, st))) return rc;
   CK(cudaStreamWaitEvent(r.h2d, ev_entry, 0), "h2d wait entry");
-  CK(cudaStreamWaitEvent(r.d2h, ev_entry, 0), "d2h wait entry");
+  for (int q = 0; q < nd; ++q) CK(cudaStreamWaitEvent(d2hs[q], ev_entry, 0), "d2h wait entry");
 
   // H2D order: start with B chunk 0 and A block 0, then repeatedly bring
   // whichever operand enables more new C tiles per byte (an A block enables
@@ -204,11 +241,13 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
       CK(cudaMemcpy2DAsync(B_d + c0, (size_t)N * 4, B_h + c0, (size_t)ldb * 4, (size_t)nc * 4, K,
                            cudaMemcpyHostToDevice, r.h2d), "H2D B chunk");
       CK(cudaEventRecord(ev_b[it.idx], r.h2d), "record B chunk");
+      if ((rc = trace_rec(0, r.h2d))) return rc;
     } else {
       const int r0 = it.idx * p.R, nr = M - r0 < p.R ? M - r0 : p.R;
       CK(cudaMemcpy2DAsync(A_d + (size_t)r0 * K, (size_t)K * 4, A_h + (size_t)r0 * lda, (size_t)lda * 4,
                            (size_t)K * 4, nr, cudaMemcpyHostToDevice, r.h2d), "H2D A block");
       CK(cudaEventRecord(ev_a[it.idx], r.h2d), "record A block");
+      if ((rc = trace_rec(0, r.h2d))) return rc;
     }
   }
 
@@ -256,20 +295,51 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
     }
     if (rc) return rc;
     CK(cudaEventRecord(ev_t[t], st), "record tile");
+    if ((rc = trace_rec(1, st))) return rc;
   }
 
-  // D2H each tile as soon as it is written
+  // D2H each tile as soon as it is written (row slices over nd streams)
   for (int t : tiles) {
     const int i = t / p.ncb, j = t % p.ncb;
     const int r0 = i * p.R, nr = M - r0 < p.R ? M - r0 : p.R;
     const int c0 = j * p.Nc, nc = N - c0 < p.Nc ? N - c0 : p.Nc;
-    CK(cudaStreamWaitEvent(r.d2h, ev_t[t], 0), "d2h wait tile");
-    CK(cudaMemcpy2DAsync(C_h + (size_t)r0 * ldc + c0, (size_t)ldc * 4, C_d + (size_t)r0 * N + c0,
-                         (size_t)N * 4, (size_t)nc * 4, nr, cudaMemcpyDeviceToHost, r.d2h), "D2H C tile");
+    const int per = (nr + nd - 1) / nd;
+    for (int q = 0; q < nd; ++q) {
+      const int a0 = q * per, a1 = nr < a0 + per ? nr : a0 + per;
+      if (a1 <= a0) continue;
+      CK(cudaStreamWaitEvent(d2hs[q], ev_t[t], 0), "d2h wait tile");
+      CK(cudaMemcpy2DAsync(C_h + (size_t)(r0 + a0) * ldc + c0, (size_t)ldc * 4, C_d + (size_t)(r0 + a0) * N + c0,
+                           (size_t)N * 4, (size_t)nc * 4, a1 - a0, cudaMemcpyDeviceToHost, d2hs[q]),
+         "D2H C tile");
+    }
+    if ((rc = trace_rec(2, d2hs[nd - 1]))) return rc;
   }
   CK(cudaEventRecord(ev_end, r.d2h), "record end");
+  if (trace) r.tkind.resize(ntr);
   CK(cudaStreamWaitEvent(st, ev_end, 0), "join d2h");
+  for (int q = 1; q < nd; ++q) {
+    CK(cudaEventRecord(r.end_extra[q - 1], d2hs[q]), "record end");
+    CK(cudaStreamWaitEvent(st, r.end_extra[q - 1], 0), "join d2h");
+  }
   return ELV_OK;
+}
+
+/* Diagnostics (ELV_HOST_TRACE=1): after the last elv_gemm_host on this
+ * thread has completed, write up to `cap` (kind, ms-since-entry) pairs --
+ * kind 0 = an H2D item landed, 1 = a tile's GEMM finished, 2 = a tile's D2H
+ * finished -- and return how many. */
+int elv_gemm_host_trace(float* out, int cap) {
+  if (g_trace_dev < 0) return 0;
+  DeviceRes& r = g_res[g_trace_dev];
+  std::lock_guard<std::mutex> lk(r.mu);
+  int n = 0;
+  for (size_t i = 1; i < r.tkind.size() && n < cap; ++i, ++n) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.tev[0], r.tev[i]);
+    out[2 * n] = (float)r.tkind[i];
+    out[2 * n + 1] = ms;
+  }
+  return n;
 }
 
 }  // extern "C"

@@ -47,8 +47,12 @@ def main():
     del Cd
     print(json.dumps(res), flush=True)
 
-    tiles = [None, "4096,4096", "2048,8192", "8192,4096", "2048,4096", "4096,16384", "8192,8192"]
-    for t in tiles:
+    tiles = os.environ.get("SWEEP_TILES", "None,4096:4096,2048:8192,8192:4096,2048:4096,4096:16384,8192:8192").split(",")
+    tiles = [None if t == "None" else t.replace(":", ",") for t in tiles]
+    nds = os.environ.get("SWEEP_D2H", "").split(",") if os.environ.get("SWEEP_D2H") else [None]
+    for nd, t in [(nd, t) for nd in nds for t in tiles]:
+        if nd:
+            os.environ["ELV_HOST_D2H_STREAMS"] = nd
         if t:
             os.environ["ELV_HOST_TILES"] = t
         else:
@@ -62,7 +66,7 @@ def main():
             t0 = time.perf_counter()
             hp(A, B, C)
             best = min(best, time.perf_counter() - t0)
-        print(json.dumps({"tiles": hp.tile, "ms": best * 1e3,
+        print(json.dumps({"tiles": hp.tile, "d2h_streams": nd, "ms": best * 1e3,
                           "TFLOP/s": 2.0 * M * N * K / best / 1e12}), flush=True)
         del hp
 

@@ -128,8 +128,8 @@ def test_host_pipeline_bitwise_equals_device_path(cuda, variant, tiles, monkeypa
 
 
 def test_host_pipeline_large_default_tiling(cuda):
-    """The default tiling at a bench-like shape (8 row blocks x 8192-column
-    chunks) and repeated calls reusing the cached workspace: row samples
+    """The default tiling at a bench-like shape (8 row blocks; N < 32768, so
+    one column chunk) and repeated calls reusing the cached workspace: row samples
     against the f64 oracle, and call 2 == call 1."""
     from paper_2002_02268_b200 import interp as I
     M, N, K = 4096, 16384, 1024
@@ -139,7 +139,7 @@ def test_host_pipeline_large_default_tiling(cuda):
     C1 = torch.empty((M, N), pin_memory=True)
     I.run(term, [A, B], tf32x3=True, out=C1)
     hp = I._host_pipes[(7, M, N, K, str(torch.device("cuda", torch.cuda.current_device())))]
-    assert hp.tile == (512, 8192)
+    assert hp.tile == (512, 16384)
     C2 = torch.empty((M, N), pin_memory=True)
     I.run(term, [A, B], tf32x3=True, out=C2)
     assert torch.equal(C1, C2)
