@@ -298,7 +298,9 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
     if ((rc = trace_rec(1, st))) return rc;
   }
 
-  // D2H each tile as soon as it is written (row slices over nd streams)
+  // D2H each tile as soon as it is written (row slices over nd streams).
+  // Copying whole row blocks instead (longer copy rows, but each waits for
+  // its last tile) measured slower: 99.7 vs 94.8 ms (gpurun_out/s2ac).
   for (int t : tiles) {
     const int i = t / p.ncb, j = t % p.ncb;
     const int r0 = i * p.R, nr = M - r0 < p.R ? M - r0 : p.R;
