@@ -508,13 +508,21 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           PROF_T(e1);
           PROF_ADD(3, e1 - e0);
           uint8_t* st = smem + s * P_STAGE_BYTES;
-          if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
           const uint32_t bar = full0 + (uint32_t)(s * 8);
           const int k0 = kb * BKT;
+#ifdef ELV_K7_EXPERIMENT_NOLO
+          // tuning experiment only (wrong results): load the hi planes only, to
+          // measure how power-capped throughput responds to L2->SMEM traffic
+          if (leader) mbar_expect_tx(&full[s], P_STAGE_BYTES);
+          tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
+          tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
+#else
+          if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
           tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
           tma_load_2d_pair(&map_alo, bar, st + P_A_TILE, k0, ma);
           tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
           tma_load_2d_pair(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb);
+#endif
           if (++s == P_STAGES) { s = 0; ph ^= 1; }
         }
         if (wave_ctr != nullptr) atomicAdd(wave_ctr, 1u);
