@@ -83,7 +83,7 @@ def features(term) -> dict:
 
 def _guess(f: dict) -> list:
     """Schedules consistent with the feature scan, most likely first."""
-    if f["mapPar"]:
+    if f["mapPar"] >= 2:                     # parallelizeCopy's + the row-block loop's
         return ["parallel"]
     if f["toMem"] >= 2:                      # packedB + the cache_write accumulator
         return ["cacheBlocks"]

@@ -16,7 +16,7 @@ The output terms are the inputs of the hot path:
   blocking      tile(32,32) ;; split(4) ;; reorder_blocking       xo,yo,ko,ki,xi,yi  (26-30, 280-283)
   vectorized    blocking ;; vectorize(32) [lands on yi]           + vectorize(yi)    (33)
   loopPerm      tile ;; split(4) ;; reorder_loopperm ;; vec(32)   xo,yo,ko,xi,ki,yi  (37-42, 293-297)
-  arrayPacking  packB ;; loopPerm                                 + packedB          (49-63, 303-306)
+  arrayPacking  packB ;; loopPerm ;; parallelizeCopy              + packedB          (49-63, 303-306)
   cacheBlocks   arrayPacking ;; topDown(isReduce;toMemAfter)
                 ;; bottomUp(isAppliedReduce;unroll)               + cache_write, unroll(ki) (65-79)
   parallel      arrayPacking ;; topDown(parallel)
@@ -132,7 +132,16 @@ def _prefixes():
     blocking = dseq(dseq(tiled, lift_inner), lift_inner)     # ki above yi and xi
     vectorized = dseq(blocking, vec32)
     loop_perm = dseq(dseq(tiled, lift_inner), vec32)          # ki above yi only
-    array_packing = dseq(tv.top_down(rules.make_pack_b(32)), loop_perm)
+    # parallelizeCopy (undefined in paper and reference; TVM
+    # s[packedB].parallel(x)): the outermost loop of the
+    # packing copy inside toMem becomes mapPar.  The paper's extra
+    # topDown(vectorize(32)) is meant for the copy's inner loop (TVM
+    # s[packedB].vectorize(z)), but the shipped vectorize rule cannot type the
+    # copy's identity function (rules.py:408-431 needs f : f32 -> f32 and the
+    # identity is polymorphic), and a plain topDown lands on the k-products
+    # map instead; the copy kernel (k_pack_b) moves 128-bit vectors anyway.
+    parallelize_copy = tv.top_down(tv.argument_of("toMem", tv.top_down(rules.parallel)))
+    array_packing = dseq(dseq(tv.top_down(rules.make_pack_b(32)), loop_perm), parallelize_copy)
     unroll_ki = tv.bottom_up(st.seq(is_applied_reduce(), rules.unroll))
     cache_blocks = dseq(dseq(array_packing,
                              tv.top_down(st.seq(tv.is_reduce, rules.to_mem_after))),

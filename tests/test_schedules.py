@@ -59,8 +59,12 @@ def test_structural_witnesses(terms):
         assert f[n]["toMem"] == 1, n                      # packedB
     assert f["cacheBlocks"]["toMem"] == 2                 # + the block accumulator (cache_write)
     assert f["cacheBlocks"]["reduceSeqUnroll"] == 1       # unroll(ki)
-    assert f["parallel"]["mapPar"] == 1 and f["parallel"]["reduceSeqUnroll"] == 1
-    assert all(f[n]["mapPar"] == 0 for n in NAMES[:-1])
+    # parallelizeCopy: the packing copy's outer loop is mapPar (TVM
+    # s[packedB].parallel(x)); parallel adds the row-block loop (parallel(xo))
+    for n in ("arrayPacking", "cacheBlocks"):
+        assert f[n]["mapPar"] == 1, n
+    assert f["parallel"]["mapPar"] == 2 and f["parallel"]["reduceSeqUnroll"] == 1
+    assert all(f[n]["mapPar"] == 0 for n in NAMES[:4])
     assert all(f[n]["high_level"] == 0 for n in NAMES)
 
 
