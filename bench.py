@@ -410,16 +410,14 @@ def main():
         C_h = torch.empty((sh.rows, N), dtype=torch.float32, pin_memory=True)
         shard_term = term if world == 1 else None
 
+        if world > 1:
+            host_pipe = D.HostRowShardPipeline(pipe)
+
         def e2e_step():
             if world == 1:
                 interp.run(shard_term, [A_h, B_h], out=C_h, tf32x3=tf32x3)
-            else:
-                if rank == 0:
-                    B.copy_(B_h, non_blocking=True)
-                A.copy_(A_h, non_blocking=True)
-                pipe.step(A, B, C)
-                C_h.copy_(C, non_blocking=True)
-                torch.cuda.current_stream(dev).synchronize()
+                return
+            host_pipe(A_h, B_h, C_h, A, B, C)
 
         e2e_step()
         barrier()
@@ -438,8 +436,9 @@ def main():
         e2e = {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "api": "interp.run(term, [A_host_pinned, B_host_pinned], out=C_host_pinned)"
-               if world == 1 else ("H2D A-shard (+B on rank 0), PipelinedRowShardGemm.step "
-                                   "(chunked packedB NCCL broadcast + GEMM), D2H C-shard")}
+               if world == 1 else ("per rank: H2D of the A shard and (rank 0) of B by column chunk, "
+                                   "PipelinedRowShardGemm.step (each chunk packed + NCCL-broadcast as it "
+                                   "lands, GEMM per chunk), D2H of each C-shard chunk as its GEMM ends")}
 
     if rank != 0:
         if world > 1:

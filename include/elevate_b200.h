@@ -129,6 +129,11 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h,
                   void* workspace, size_t workspace_bytes, void* stream);
 /* The tile shape elv_gemm_host uses (rows x cols). */
 int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols);
+/* Pitched copy (cudaMemcpy2DAsync): kind 1 = host->device, 2 = device->host,
+ * 3 = device->device.  Used by the multi-GPU end-to-end path to move column
+ * chunks of a row-major matrix. */
+int elv_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+               int kind, void* stream);
 /* Diagnostics: with ELV_HOST_TRACE=1 set, after the last elv_gemm_host on
  * this thread completed, write up to `cap` (kind, ms since entry) float pairs
  * (kind 0 = H2D item landed, 1 = tile GEMM done, 2 = tile D2H done). */

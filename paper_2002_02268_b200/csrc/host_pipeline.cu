@@ -326,6 +326,17 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   return ELV_OK;
 }
 
+int elv_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height, int kind,
+               void* stream) {
+  if (dst == nullptr || src == nullptr || width > dpitch || width > spitch)
+    return set_error(ELV_EINVAL, "copy2d: bad arguments");
+  if (width == 0 || height == 0) return ELV_OK;
+  const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost
+                                                                          : cudaMemcpyDeviceToDevice;
+  CK(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, k, (cudaStream_t)stream), "copy2d");
+  return ELV_OK;
+}
+
 /* Diagnostics (ELV_HOST_TRACE=1): after the last elv_gemm_host on this
  * thread has completed, write up to `cap` (kind, ms-since-entry) pairs --
  * kind 0 = an H2D item landed, 1 = a tile's GEMM finished, 2 = a tile's D2H

@@ -154,14 +154,22 @@ class PipelinedRowShardGemm:
     def _panel(self, n0: int) -> torch.Tensor:
         return self.P[(n0 // 32) * self.K * 32:]
 
-    def step(self, A_shard: torch.Tensor, B: torch.Tensor | None, C_shard: torch.Tensor):
+    def step(self, A_shard: torch.Tensor, B: torch.Tensor | None, C_shard: torch.Tensor,
+             b_ready=None, a_ready=None, chunk_done=None):
+        """One step.  Optional hooks for the end-to-end path (host operands):
+        b_ready[c] -- event after which B's columns of chunk c are on the
+        device (rank src); a_ready -- event for A_shard; chunk_done(c, n0, n1,
+        event) is called after chunk c's GEMM is enqueued, with an event
+        recorded after it (to start that chunk's D2H)."""
         lib, K, N, st = self.lib, self.K, self.N, self.stream.cuda_stream
         M = A_shard.shape[0]
         works = []
         with torch.cuda.stream(self.stream):
-            for n0, n1 in self.chunks:
+            for c, (n0, n1) in enumerate(self.chunks):
                 Pc = self._panel(n0)
                 count = ((n1 - n0 + 255) // 256) * 256 * K     # packB writes whole 256-col groups
+                if self.rank == self.src and b_ready is not None:
+                    self.stream.wait_event(b_ready[c])
                 if self.rank == self.src:
                     self._check(lib.elv_pack_b(B.data_ptr() + 4 * n0, Pc.data_ptr(), K, n1 - n0, B.stride(0),
                                                32, st), "elv_pack_b")
@@ -189,23 +197,85 @@ class PipelinedRowShardGemm:
                         ev = torch.cuda.Event()
                         ev.record(self.prep)
                         ready.append(ev)
+                if a_ready is not None:
+                    self.stream.wait_event(a_ready)
                 self._check(lib.elv_tf32x3_split_a(A_shard.data_ptr(), M, K, A_shard.stride(0),
                                                    self.a_planes.data_ptr(), st), "split_a")
-                for (n0, n1), bp, ev in zip(self.chunks, self.b_planes, ready):
+                for c, ((n0, n1), bp, ev) in enumerate(zip(self.chunks, self.b_planes, ready)):
                     self.stream.wait_event(ev)
                     self._check(lib.elv_tf32x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(),
                                                            C_shard.data_ptr() + 4 * n0, M, n1 - n0, K,
                                                            C_shard.stride(0), st), "gemm_planes")
+                    self._done(chunk_done, c, n0, n1)
                 return C_shard
-            for (n0, n1), w in zip(self.chunks, works):
+            if a_ready is not None:
+                self.stream.wait_event(a_ready)
+            for c, ((n0, n1), w) in enumerate(zip(self.chunks, works)):
                 if w is not None:
                     w.wait()                        # compute stream waits for chunk c only
                 self._check(lib.elv_gemm_prepacked(self.variant, A_shard.data_ptr(), self._panel(n0).data_ptr(),
                                                    C_shard.data_ptr() + 4 * n0, M, n1 - n0, K, A_shard.stride(0),
                                                    C_shard.stride(0), st), "elv_gemm_prepacked")
+                self._done(chunk_done, c, n0, n1)
         return C_shard
 
+    def _done(self, chunk_done, c, n0, n1):
+        if chunk_done is not None:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            chunk_done(c, n0, n1, ev)
 
+
+
+class HostRowShardPipeline:
+    """End to end from host buffers on N GPUs (one process per GPU): rank
+    `src` streams B to its device column chunk by column chunk (each chunk is
+    packed and NCCL-broadcast as soon as it lands), every rank streams in its
+    A shard, and each column chunk of the C shard goes back to the host as
+    soon as its GEMM is done -- PCIe in, NVLink and PCIe out overlap the
+    GEMMs.  Wraps a PipelinedRowShardGemm; A_dev/B_dev/C_dev are its device
+    buffers (B_dev only on `src`)."""
+
+    def __init__(self, pipe: PipelinedRowShardGemm):
+        self.pipe = pipe
+        self.lib = pipe.lib
+        self.s_in = torch.cuda.Stream(pipe.device)
+        self.s_out = torch.cuda.Stream(pipe.device)
+
+    def __call__(self, A_h, B_h, C_h, A_dev, B_dev, C_dev, sync: bool = True):
+        pipe, lib, st = self.pipe, self.lib, self.pipe.stream
+        N, K, rows = pipe.N, pipe.K, A_dev.shape[0]
+        for t, shape in ((A_h, (rows, K)), (C_h, (rows, N))):
+            if t.is_cuda or tuple(t.shape) != shape or t.stride(-1) != 1 or t.stride(0) != shape[1]:
+                raise ValueError(f"host buffers must be contiguous row-major {shape}")
+        self.s_in.wait_stream(st)
+        self.s_out.wait_stream(st)
+        src = pipe.rank == pipe.src
+        b_evs = [] if src else None
+        a_ev = torch.cuda.Event()
+        with torch.cuda.stream(self.s_in):
+            for c, (n0, n1) in enumerate(pipe.chunks):
+                if src:
+                    pipe._check(lib.elv_copy2d(B_dev.data_ptr() + 4 * n0, B_dev.stride(0) * 4,
+                                               B_h.data_ptr() + 4 * n0, B_h.stride(0) * 4, (n1 - n0) * 4, K, 1,
+                                               self.s_in.cuda_stream), "elv_copy2d")
+                    b_evs.append(torch.cuda.Event())
+                    b_evs[-1].record(self.s_in)
+                if c == 0 and rows:
+                    A_dev.copy_(A_h, non_blocking=True)
+            a_ev.record(self.s_in)
+
+        def chunk_done(c, n0, n1, ev):
+            self.s_out.wait_event(ev)
+            pipe._check(lib.elv_copy2d(C_h.data_ptr() + 4 * n0, C_h.stride(0) * 4, C_dev.data_ptr() + 4 * n0,
+                                       C_dev.stride(0) * 4, (n1 - n0) * 4, rows, 2, self.s_out.cuda_stream),
+                        "elv_copy2d")
+
+        pipe.step(A_dev, B_dev, C_dev, b_ready=b_evs, a_ready=a_ev, chunk_done=chunk_done)
+        st.wait_stream(self.s_out)
+        if sync:
+            st.synchronize()
+        return C_h
 
 
 def gather_rows(C_shard: torch.Tensor, M: int, group=None, align: int = ROW_ALIGN) -> torch.Tensor:

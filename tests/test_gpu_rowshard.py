@@ -234,3 +234,51 @@ def test_host_pipeline_concurrent_callers(cuda):
     assert not errs
     for o, r in zip(outs, refs):
         assert torch.equal(o, r)
+
+
+def _worker_host(rank, world, port, variant, M, N, K, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        sh = D.shard_rows(M, world, rank)
+        import dataclasses
+        p = dataclasses.replace(_plan(variant, M, N, K), M=sh.rows)
+        A_h = torch.from_numpy(synth.matrix(sh.rows, K, 5, 0, row0=sh.row0)).pin_memory()
+        B_h = torch.from_numpy(synth.matrix(K, N, 5, 1)).pin_memory() if rank == 0 else None
+        C_h = torch.full((sh.rows, N), float("nan")).pin_memory()
+        A = torch.empty((sh.rows, K), device=dev)
+        B = torch.empty((K, N), device=dev) if rank == 0 else None
+        C = torch.empty((sh.rows, N), device=dev)
+        pipe = D.PipelinedRowShardGemm(p, N, K, dev, chunks=3)
+        hp = D.HostRowShardPipeline(pipe)
+        for _ in range(2):                              # reuse of every buffer
+            hp(A_h, B_h, C_h, A, B, C)
+        q.put((rank, sh.row0, C_h.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("variant", [6, 7])
+def test_host_row_shard_pipeline_two_ranks(cuda, variant):
+    """The multi-GPU end-to-end path from host buffers (B streamed to rank 0 by
+    column chunk and broadcast chunk by chunk, C chunks streamed back) with
+    two ranks sharing cuda:0 over gloo: the gathered C equals one unsharded
+    launch bit for bit."""
+    M, N, K = 384, 1280, 256
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_host, args=(r, 2, port, variant, M, N, K, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    parts = sorted([q.get(timeout=240) for _ in range(2)])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    C = np.concatenate([c for _, _, c in parts], 0)
+    p = _plan(variant, M, N, K)
+    A = torch.from_numpy(synth.matrix(M, K, 5, 0)).to(cuda)
+    B = torch.from_numpy(synth.matrix(K, N, 5, 1)).to(cuda)
+    assert np.array_equal(C, interp.gemm(p, A, B).cpu().numpy())
