@@ -273,3 +273,41 @@ def test_output_beyond_2_pow_31_elements(cuda, variant):
     assert ok, worst
     del C
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3"])
+def test_bench_shape_checksums_cover_every_element(cuda, variant):
+    """configs[3] at full size, every element accounted for: the column sums
+    e^T C must match (e^T A) B and the row sums C e must match A (B e) in
+    f64.  Per-element errors are independent and centred, so a column sum's
+    error is compared with the root-sum-square of its elements' bounds
+    b_ij = tau sqrt(K) 2^-24 (|A||B|)_ij (correct kernels sit at ~4 % of b,
+    a dropped 3xTF32 correction at 7-29x b); the linear sum of the bounds is
+    asserted too.  A checksum of checksums: size-independent, so it runs at
+    32768^2 x 8192 where the element-wise oracle cannot (torch f64 on the
+    GPU is the checker here)."""
+    name, tf = _sched(variant)
+    M, N, K = 32768, 32768, 8192
+    A, B = _device_inputs(M, N, K, 1, cuda)
+    C = interp.run_tensor(schedules.apply(name, M, N, K).term, A, B, tf32x3=tf)
+    torch.cuda.synchronize()
+    col = C.double().sum(0)
+    row = C.double().sum(1)
+    del C
+    torch.cuda.empty_cache()
+    Ad, Bd = A.double(), B.double()
+    del A, B
+    col_ref, row_ref = Ad.sum(0) @ Bd, Ad @ Bd.sum(1)
+    b = Ad.abs() @ Bd.abs()                              # (|A||B|), f64
+    b *= oracle.default_tau(K) * K ** 0.5 * 2.0 ** -24
+    col_lin, row_lin = b.sum(0), b.sum(1)
+    b.square_()
+    col_rss, row_rss = b.sum(0).sqrt(), b.sum(1).sqrt()
+    del b
+    torch.cuda.empty_cache()
+    ce, re = (col - col_ref).abs(), (row - row_ref).abs()
+    assert (ce / col_lin).max().item() <= 1.0 and (re / row_lin).max().item() <= 1.0
+    col_ratio, row_ratio = (ce / col_rss).max().item(), (re / row_rss).max().item()
+    print(f"{variant}: checksum err / rss-bound: columns {col_ratio:.3g}, rows {row_ratio:.3g}")
+    assert col_ratio <= 1.0, f"{variant}: column checksum err/rss-bound {col_ratio:.3g}"
+    assert row_ratio <= 1.0, f"{variant}: row checksum err/rss-bound {row_ratio:.3g}"
