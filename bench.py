@@ -102,6 +102,11 @@ def roofline_peak(variant: str, peaks: dict, n_sms: int, cublas: dict | None = N
     if cublas:
         lib = "; cuBLAS in this run: " + ", ".join(
             f"{k.replace('cublas_', '')} {v:.0f} TF" for k, v in cublas.items() if v)
+    if variant == "parallel_fp16x3":
+        tf16 = peaks["bf16_tflops"]
+        return tf16 / 3.0, "tensor", (
+            f"MEASURED_PEAKS bf16_tflops {tf16:.0f} (burst) = the f16 dense rate; 3xFP16 issues 3 MMAs per "
+            f"useful MAC, so the useful-fp32 ceiling is that / 3{lib}")
     if variant == "parallel_tf32x3":
         tf32 = peaks["bf16_tflops"] / 2.0
         alt = peaks.get("bf16_tflops_sustained", 0) / 2.0 / 3.0
@@ -322,9 +327,10 @@ def main():
         return
 
     M, N, K = args.M, args.N, args.K
-    sched, tf32x3 = ("parallel", True) if args.variant == "parallel_tf32x3" else (args.variant, False)
+    sched, tf32x3 = ("parallel", True) if args.variant.startswith("parallel_") else (args.variant, False)
+    enc = "fp16" if args.variant == "parallel_fp16x3" else "tf32"
     term = schedules.apply(sched, M, N, K).term
-    full_plan = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf32x3)
+    full_plan = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf32x3, tc_encoding=enc)
     sh = D.shard_rows(M, world, rank)
     import dataclasses
     plan = dataclasses.replace(full_plan, M=sh.rows)
@@ -415,7 +421,7 @@ def main():
 
         def e2e_step():
             if world == 1:
-                interp.run(shard_term, [A_h, B_h], out=C_h, tf32x3=tf32x3)
+                interp.run(shard_term, [A_h, B_h], out=C_h, tf32x3=tf32x3, tc_encoding=enc)
                 return
             host_pipe(A_h, B_h, C_h, A, B, C)
 
@@ -453,7 +459,8 @@ def main():
         cublas = None
     peak, bound, note = roofline_peak(args.variant, peaks, n_sms, cublas)
     achieved = 2.0 * sh.rows * N * K / (comp_ms * 1e-3) / 1e12
-    kernel = {"parallel_tf32x3": "k7_tf32x3_pair<32>", "parallel": "k6_sgemm_cp<2>"}.get(args.variant, args.variant)
+    kernel = {"parallel_tf32x3": "k7_tf32x3_pair<32>", "parallel_fp16x3": "k7_tf32x3_pair<64, true>",
+              "parallel": "k6_sgemm_ffma2"}.get(args.variant, args.variant)
     roof = {"bound": "tensor" if bound == "tensor" else "fp32-simt", "achieved": achieved,
             "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic_from_profiles(f"{kernel}@{sh.rows}x{N}x{K}"),
@@ -462,7 +469,7 @@ def main():
             "algorithmic_flops_per_launch": 2.0 * sh.rows * N * K, "library_reference": cublas}
     # compulsory bytes of one launch: operand planes (3xTF32: hi+lo, 8 B per
     # element; SIMT: packed fp32, 4 B) read once + C written once
-    ob = 8 if args.variant == "parallel_tf32x3" else 4
+    ob = {"parallel_tf32x3": 8, "parallel_fp16x3": 4}.get(args.variant, 4)
     roof["algorithmic_bytes_per_launch"] = float(ob * (sh.rows * K + K * N) + 4 * sh.rows * N)
     roof["traffic_note"] = (
         "traffic = ncu dram read+write of the same launch (profiles/ncu_traffic.json). It exceeds the "
@@ -496,12 +503,13 @@ def run_ladder(args, dev):
     cublas = measure_cublas(dev)
     print(json.dumps({"workload": "library reference points (not our path)", **cublas}), flush=True)
     cases = [(v, 1024) for v in list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]]
-    cases += [(v, 8192) for v in ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3")]
+    cases += [(v, 8192) for v in ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3", "parallel_fp16x3")]
     stream = torch.cuda.current_stream(dev)
     for v, n in cases:
-        sched, tf = ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+        sched, tf = ("parallel", True) if v.startswith("parallel_") else (v, False)
         term = schedules.apply(sched, n, n, n).term
-        p = dispatch.decode(term, [(n, n), (n, n)], tf32x3=tf)
+        p = dispatch.decode(term, [(n, n), (n, n)], tf32x3=tf,
+                            tc_encoding="fp16" if v == "parallel_fp16x3" else "tf32")
         A = torch.empty((n, n), device=dev); synth.fill_device(A, 0, 0)
         B = torch.empty((n, n), device=dev); synth.fill_device(B, 0, 1)
         C = torch.empty((n, n), device=dev)

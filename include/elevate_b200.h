@@ -56,7 +56,10 @@ enum {
   ELV_CACHEBLOCKS = 5,     /* + toMem(acc) + unroll: 8x8 register accumulators*/
   ELV_PARALLEL = 6,        /* + mapPar: persistent, double-buffered, 148 SMs  */
   ELV_PARALLEL_TF32X3 = 7, /* parallel term on tcgen05: 3xTF32, TMEM accum    */
-  ELV_NUM_VARIANTS = 8
+  ELV_PARALLEL_FP16X3 = 8, /* same three products on scaled fp16 hi/lo planes:
+                              half the bytes, kind::f16 (falls back to 7 for
+                              K < 512 or fewer pair tiles than SMs)          */
+  ELV_NUM_VARIANTS = 9
 };
 
 /* C = A . B with the kernel of `variant`.

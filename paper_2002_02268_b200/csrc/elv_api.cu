@@ -142,7 +142,7 @@ int elv_abi_version(void) { return ELV_ABI_VERSION; }
 const char* elv_variant_name(int v) {
   static const char* names[ELV_NUM_VARIANTS] = {
       "baseline", "blocking", "vectorized", "loopPerm", "arrayPacking",
-      "cacheBlocks", "parallel", "parallel_tf32x3"};
+      "cacheBlocks", "parallel", "parallel_tf32x3", "parallel_fp16x3"};
   return (v >= 0 && v < ELV_NUM_VARIANTS) ? names[v] : "unknown";
 }
 
@@ -159,6 +159,7 @@ size_t elv_gemm_workspace_bytes(int variant, int M, int N, int K) {
     case ELV_PARALLEL:
       return elv_pack_b_bytes(K, N) + (parallel_uses_packed_a(M, N) ? pack_a_bytes(M, K) : 0);
     case ELV_PARALLEL_TF32X3: return tf32x3_workspace_bytes(M, N, K);
+    case ELV_PARALLEL_FP16X3: return fp16x3_workspace_bytes(M, N, K);
     default: return 0;
   }
 }
@@ -236,6 +237,8 @@ int elv_gemm_prepare(int variant, const float* A, const float* B, int M, int N, 
                             lda, st);
     case ELV_PARALLEL_TF32X3:
       return tf32x3_prepare(A, B, M, N, K, lda, ldb, workspace, workspace_bytes, st);
+    case ELV_PARALLEL_FP16X3:
+      return fp16x3_prepare(A, B, M, N, K, lda, ldb, workspace, workspace_bytes, st);
     default:
       return ELV_OK;   // 0..3 read A and B in place
   }
@@ -266,6 +269,8 @@ int elv_gemm_compute(int variant, const float* A, const float* B, float* C, int 
                          ldc, st);
     case ELV_PARALLEL_TF32X3:
       return tf32x3_compute(C, M, N, K, ldc, workspace, workspace_bytes, st);
+    case ELV_PARALLEL_FP16X3:
+      return fp16x3_compute(C, M, N, K, ldc, workspace, workspace_bytes, st);
   }
   return set_error(ELV_EVARIANT, "unknown variant %d", variant);
 }

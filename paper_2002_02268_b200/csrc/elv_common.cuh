@@ -84,6 +84,12 @@ int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_p
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                        cudaStream_t st);
 int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st);
+// 3xFP16 encoding of the parallel schedule's tcgen05 kernel (tf32x3_gemm.cu)
+bool fp16x3_applicable(int M, int N, int K);
+size_t fp16x3_workspace_bytes(int M, int N, int K);
+int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
+int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
 
 // binomial filter (stencil.cu)
 int launch_binomial(int variant, const float* img, float* out, int H, int W, int ldi, int ldo,

@@ -132,12 +132,14 @@ extern "C" {
 
 size_t elv_gemm_host_workspace_bytes(int variant, int M, int N, int K) {
   if (M < 1 || N < 1 || K < 1 || variant < 0 || variant >= ELV_NUM_VARIANTS) return 0;
+  if (variant == ELV_PARALLEL_FP16X3) variant = ELV_PARALLEL_TF32X3;
   return make_plan(variant, M, N, K).total;
 }
 
 int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols) {
   if (M < 1 || N < 1 || K < 1 || variant < 0 || variant >= ELV_NUM_VARIANTS)
     return set_error(ELV_EINVAL, "gemm_host_tiles: bad arguments");
+  if (variant == ELV_PARALLEL_FP16X3) variant = ELV_PARALLEL_TF32X3;
   const HostPlan p = make_plan(variant, M, N, K);
   if (rows) *rows = p.R;
   if (cols) *cols = p.Nc;
@@ -153,6 +155,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   if (lda < K || ldb < N || ldc < N)
     return set_error(ELV_EINVAL, "gemm_host: leading dimension too small (lda=%d ldb=%d ldc=%d)", lda, ldb, ldc);
   if (variant < 0 || variant >= ELV_NUM_VARIANTS) return set_error(ELV_EVARIANT, "unknown variant %d", variant);
+  if (variant == ELV_PARALLEL_FP16X3) variant = ELV_PARALLEL_TF32X3;   // per-tile prepare is tf32-encoded
   const HostPlan p = make_plan(variant, M, N, K);
   if (workspace == nullptr || workspace_bytes < p.total)
     return set_error(ELV_EWORKSPACE, "gemm_host: needs %zu workspace bytes, got %zu", p.total, workspace_bytes);

@@ -30,6 +30,7 @@
 #include "elv_common.cuh"
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <mutex>
 #include <stdlib.h>
 
@@ -376,15 +377,21 @@ constexpr int P_BM = 128;                          // rows per CTA (pair: 256)
 constexpr int P_NUM_THREADS = 320;
 constexpr int P_EPI_WARPS = 8;
 constexpr int P_BN = 256;                          // columns per pair tile (128 per CTA staged)
-template <int BKT> struct PairCfg {
-  static constexpr int STAGES = BKT == 32 ? 3 : 6;
-  static constexpr int A_TILE = P_BM * BKT * 4;            // 8 / 16 KB
-  static constexpr int B_TILE = (P_BN / 2) * BKT * 4;      // this CTA's half of Bt
+// BKT = K elements per stage; F16: operands are scaled fp16 hi/lo planes
+// (2 B per element, kind::f16, 16 K per MMA) instead of tf32 (4 B, 8 K).
+template <int BKT, bool F16 = false> struct PairCfg {
+  static constexpr int EB = F16 ? 2 : 4;                   // bytes per element
+  static constexpr int ROW_BYTES = BKT * EB;                // 64 or 128 (swizzle width)
+  static constexpr int STAGES = ROW_BYTES == 128 ? 3 : 6;
+  static constexpr int A_TILE = P_BM * ROW_BYTES;           // 8 / 16 KB
+  static constexpr int B_TILE = (P_BN / 2) * ROW_BYTES;     // this CTA's half of Bt
   static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+  static constexpr int KSUB = BKT / (F16 ? 16 : 8);         // MMAs per product per stage
+  // idesc: D f32; A/B type tf32 (2) or f16 (0); K-major both; N, M
+  static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
+                                    ((uint32_t)(P_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 };
-constexpr uint32_t kIdescPair = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
-                                ((uint32_t)(256 >> 4) << 24);
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -410,16 +417,28 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                                 uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
+template <bool F16>
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  if (F16) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -428,16 +447,19 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BKT>
+template <int BKT, bool F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
-               unsigned int* __restrict__ wave_ctr) {
-  constexpr int P_STAGES = PairCfg<BKT>::STAGES;
-  constexpr int P_A_TILE = PairCfg<BKT>::A_TILE;
-  constexpr int P_B_TILE = PairCfg<BKT>::B_TILE;
-  constexpr int P_STAGE_BYTES = PairCfg<BKT>::STAGE_BYTES;
+               unsigned int* __restrict__ wave_ctr, const float* __restrict__ inv_s,
+               const float* __restrict__ inv_t) {
+  using Cfg = PairCfg<BKT, F16>;
+  constexpr int P_STAGES = Cfg::STAGES;
+  constexpr int P_A_TILE = Cfg::A_TILE;
+  constexpr int P_B_TILE = Cfg::B_TILE;
+  constexpr int P_STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr uint32_t kIdescPair = Cfg::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
@@ -549,18 +571,19 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           PROF_ADD(1, f1 - f0);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * P_STAGE_BYTES);
-          const uint64_t ahi = umma_desc_k<BKT>(st);
-          const uint64_t alo = umma_desc_k<BKT>(st + P_A_TILE);
-          const uint64_t bhi = umma_desc_k<BKT>(st + 2 * P_A_TILE);
-          const uint64_t blo = umma_desc_k<BKT>(st + 2 * P_A_TILE + P_B_TILE);
+          // 128 B rows (tf32 BK=32 / f16 BK=64): 128B swizzle; 64 B rows: 64B
+          const uint64_t ahi = umma_desc_k<Cfg::ROW_BYTES / 4>(st);
+          const uint64_t alo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + P_A_TILE);
+          const uint64_t bhi = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE);
+          const uint64_t blo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE + P_B_TILE);
 #pragma unroll
-          for (int k = 0; k < BKT / 8; ++k) {
-            const uint64_t koff = (uint64_t)((k * 32) >> 4);
+          for (int k = 0; k < Cfg::KSUB; ++k) {
+            const uint64_t koff = (uint64_t)((k * 32) >> 4);      // 32 B of K per MMA
             const uint32_t acc = (kb | k) != 0;
-            tc_mma_tf32_pair(d_small, ahi + koff, blo + koff, kIdescPair, acc);
-            tc_mma_tf32_pair(d_small, alo + koff, bhi + koff, kIdescPair, 1u);
-            if (with_lolo) tc_mma_tf32_pair(d_small, alo + koff, blo + koff, kIdescPair, 1u);
-            tc_mma_tf32_pair(d_big, ahi + koff, bhi + koff, kIdescPair, acc);
+            tc_mma_pair<F16>(d_small, ahi + koff, blo + koff, kIdescPair, acc);
+            tc_mma_pair<F16>(d_small, alo + koff, bhi + koff, kIdescPair, 1u);
+            if (!F16 && with_lolo) tc_mma_pair<F16>(d_small, alo + koff, blo + koff, kIdescPair, 1u);
+            tc_mma_pair<F16>(d_big, ahi + koff, bhi + koff, kIdescPair, acc);
           }
           tc_commit_pair(&empty[s]);            // frees slot s in both CTAs
           if (++s == P_STAGES) { s = 0; ph ^= 1; }
@@ -604,9 +627,20 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           if (lane == 0) mbar_arrive_cluster(tempty0);
         }
         float v[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
         const int col = n0 + cc * 32;
+        if (F16) {
+          // planes were scaled by s_i * t_j (powers of two) and lo by 2^11:
+          // C = (big + small * 2^-11) / (s_i t_j), every scaling exact
+          const float rs_i = row < M ? __ldg(inv_s + row) : 0.f;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float tj = col + q < N ? __ldg(inv_t + col + q) : 0.f;
+            v[q] = (__uint_as_float(rb[q]) + __uint_as_float(rs[q]) * 0x1p-11f) * rs_i * tj;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
+        }
         if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
@@ -746,16 +780,18 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-int make_map(CUtensorMap* map, const float* base, int rows, int kp, int box_rows, int box_k = BK) {
+int make_map(CUtensorMap* map, const void* base, int rows, int kp, int box_rows, int box_k = BK,
+             bool f16 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const size_t eb = f16 ? 2 : 4;
   const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
+  const cuuint64_t strides[1] = {(cuuint64_t)kp * eb};
   const cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+  CUresult r = enc(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_k * eb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return ELV_OK;
@@ -828,19 +864,21 @@ static int tile_group(int dflt) {
   return v > 0 ? v : dflt;
 }
 
-template <int BKT>
-static int launch_pair(const float* a_hi, const float* a_lo, const float* b_hi,
-                       const float* b_lo, float* C, int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st) {
+template <int BKT, bool F16 = false>
+static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C, int M,
+                       int N, int K, int Kp, int ldc, int dev, cudaStream_t st, const float* inv_s = nullptr,
+                       const float* inv_t = nullptr) {
+  using Cfg = PairCfg<BKT, F16>;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
-  int rc = make_map(&ma_hi, a_hi, M, Kp, P_BM, BKT);
-  if (!rc) rc = make_map(&ma_lo, a_lo, M, Kp, P_BM, BKT);
-  if (!rc) rc = make_map(&mb_hi, b_hi, N, Kp, P_BN / 2, BKT);
-  if (!rc) rc = make_map(&mb_lo, b_lo, N, Kp, P_BN / 2, BKT);
+  int rc = make_map(&ma_hi, a_hi, M, Kp, P_BM, BKT, F16);
+  if (!rc) rc = make_map(&ma_lo, a_lo, M, Kp, P_BM, BKT, F16);
+  if (!rc) rc = make_map(&mb_hi, b_hi, N, Kp, P_BN / 2, BKT, F16);
+  if (!rc) rc = make_map(&mb_lo, b_lo, N, Kp, P_BN / 2, BKT, F16);
   if (rc) return rc;
   static int attr_dev = -1;
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3_pair<BKT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PairCfg<BKT>::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3_pair<BKT, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 pair smem attribute: %s", cudaGetErrorString(e));
     attr_dev = dev;
   }
@@ -848,9 +886,9 @@ static int launch_pair(const float* a_hi, const float* a_lo, const float* b_hi,
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
   unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;   // one wave: nothing to sync
-  cudaError_t e = launch_pdl(k7_tf32x3_pair<BKT>, dim3(2 * clusters), dim3(P_NUM_THREADS),
-                             (size_t)PairCfg<BKT>::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc,
-                             Kp / BKT, with_lolo(K), tile_group(8), ctr);
+  cudaError_t e = launch_pdl(k7_tf32x3_pair<BKT, F16>, dim3(2 * clusters), dim3(P_NUM_THREADS),
+                             (size_t)Cfg::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT,
+                             F16 ? 0 : with_lolo(K), tile_group(8), ctr, inv_s, inv_t);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3_pair");
 }
@@ -1008,6 +1046,176 @@ int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_b
   if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
   return tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
+}
+
+// ---------------------------------------------------------------------------
+// 3xFP16 encoding (variant 8): the same three-product scheme as 3xTF32 with
+// fp16 hi/lo planes -- fp16 keeps 11 significant bits like tf32, so the
+// split is exact to 2^-22 -- at half the bytes per element and twice the
+// tensor rate (kind::f16).  fp16's exponent range is restored by power-of-two
+// scaling (Ootomo & Yokota's FP16 error correction with exponent handling):
+// row i of A by s_i and column j of B by t_j so each row / column maximum
+// lands in [2^14, 2^15), and lo by 2^11 so it does not underflow:
+//   a s_i = hi + lo / 2^11 (+ 2^-22 |a s_i|),  hi, lo in fp16
+//   C_ij = (hi.hi + 2^-11 (hi.lo + lo.hi)) / (s_i t_j)       (exact scalings)
+// Elements more than ~2^28 below their row / column maximum lose relative
+// precision to fp16 subnormals; against the per-element bound (which sums
+// |a||b| over the row) that is below 2^-50 of the bound's scale.
+constexpr int K16_ALIGN = 64;                     // 128 B rows of fp16 per stage
+static inline long long kpad16(int K) { return round_up(K, K16_ALIGN); }
+
+__device__ __forceinline__ void pow2_scale(float m, float* s, float* inv) {
+  if (!(m > 0.f) || !isfinite(m)) { *s = 1.f; *inv = 1.f; return; }
+  int e;
+  frexpf(m, &e);                                  // m = f 2^e, f in [0.5, 1)
+  e = max(-100, min(100, e));
+  *s = ldexpf(1.f, 15 - e);                        // m s in [2^14, 2^15)
+  *inv = ldexpf(1.f, e - 15);
+}
+
+// one warp per row of A: row maximum -> s_i, 1/s_i
+__global__ void __launch_bounds__(256)
+k16_row_scale(const float* __restrict__ A, int M, int K, int lda, float* __restrict__ s, float* __restrict__ inv) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const float* row = A + (size_t)r * lda;
+  float m = 0.f;
+  for (int k = lane; k < K; k += 32) m = fmaxf(m, fabsf(__ldg(row + k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) pow2_scale(m, s + r, inv + r);
+}
+
+// column maxima of B (K x N row-major): a 256-row slab per block, one column
+// per thread, combined with an integer atomicMax on the (non-negative) bits
+__global__ void __launch_bounds__(256)
+k16_col_max(const float* __restrict__ B, int K, int N, int ldb, unsigned int* __restrict__ maxbits) {
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= N) return;
+  const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
+  float m = 0.f;
+  for (int k = k0; k < k1; ++k) m = fmaxf(m, fabsf(__ldg(B + (size_t)k * ldb + j)));
+  atomicMax(maxbits + j, __float_as_uint(m));
+}
+
+__device__ __forceinline__ void split16(float x, __half* hi, __half* lo) {
+  const __half h = __float2half_rn(x);
+  *hi = h;
+  *lo = __float2half_rn((x - __half2float(h)) * 2048.f);
+}
+
+// A planes: [M][Kp] hi and lo, K-major (A is already K-major), 4 k per thread
+__global__ void __launch_bounds__(256)
+k16_split_a(const float* __restrict__ A, int M, int K, int lda, int Kp, const float* __restrict__ s,
+            __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int k = (blockIdx.x * 256 + threadIdx.x) * 4;
+  if (k >= Kp) return;
+  for (int r = blockIdx.y; r < M; r += gridDim.y) {
+    const float sc = s[r];
+    const float* src = A + (size_t)r * lda;
+    __align__(8) __half h[4], l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) split16(k + u < K ? __ldg(src + k + u) * sc : 0.f, &h[u], &l[u]);
+    const size_t o = (size_t)r * Kp + k;
+    *reinterpret_cast<uint2*>(hi + o) = *reinterpret_cast<const uint2*>(h);
+    *reinterpret_cast<uint2*>(lo + o) = *reinterpret_cast<const uint2*>(l);
+  }
+}
+
+// B planes: [N][Kp] (B transposed to K-major) through 32 x 32 SMEM tiles,
+// scaled by t_j from the column maxima; blocks with k0 == 0 also publish 1/t_j
+__global__ void __launch_bounds__(256)
+k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp,
+                      const unsigned int* __restrict__ maxbits, __half* __restrict__ hi, __half* __restrict__ lo,
+                      float* __restrict__ inv_t) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int k = k0 + ty + 8 * r, n = n0 + tx;
+    t[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int n = n0 + ty + 8 * r, k = k0 + tx;
+    if (n < N && k < Kp) {
+      float sc, inv;
+      pow2_scale(__uint_as_float(maxbits[n]), &sc, &inv);
+      if (k0 == 0 && tx == 0) inv_t[n] = inv;
+      __half h, l;
+      split16(t[tx][ty + 8 * r] * sc, &h, &l);
+      hi[(size_t)n * Kp + k] = h;
+      lo[(size_t)n * Kp + k] = l;
+    }
+  }
+}
+
+struct F16Layout {
+  size_t a_hi, a_lo, b_hi, b_lo, s, inv_s, tmax, inv_t, total;
+};
+static F16Layout f16_layout(int M, int N, int K) {
+  const size_t Kp = (size_t)kpad16(K);
+  F16Layout L{};
+  size_t o = 128;                                   // slack for aligning the base
+  auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 127) / 128 * 128; return at; };
+  L.a_hi = take((size_t)M * Kp * 2);
+  L.a_lo = take((size_t)M * Kp * 2);
+  L.b_hi = take((size_t)N * Kp * 2);
+  L.b_lo = take((size_t)N * Kp * 2);
+  L.s = take((size_t)M * 4);
+  L.inv_s = take((size_t)M * 4);
+  L.tmax = take((size_t)N * 4);
+  L.inv_t = take((size_t)N * 4);
+  L.total = o;
+  return L;
+}
+
+// The fp16 encoding runs on the cta_group::2 kernel (>= one wave of pair
+// tiles) for K >= 512 (no lo.lo term); anything else uses the tf32 encoding.
+bool fp16x3_applicable(int M, int N, int K) {
+  const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
+  return K >= 512 && pair_tiles >= num_sms();
+}
+
+size_t fp16x3_workspace_bytes(int M, int N, int K) {
+  return fp16x3_applicable(M, N, K) ? f16_layout(M, N, K).total : tf32x3_workspace_bytes(M, N, K);
+}
+
+int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (!fp16x3_applicable(M, N, K)) return tf32x3_prepare(A, B, M, N, K, lda, ldb, ws, ws_bytes, st);
+  const F16Layout L = f16_layout(M, N, K);
+  if (ws == nullptr || ws_bytes < L.total) return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127)) - 128;
+  const int Kp = (int)kpad16(K);
+  float* s = reinterpret_cast<float*>(base + L.s);
+  unsigned int* tmax = reinterpret_cast<unsigned int*>(base + L.tmax);
+  k16_row_scale<<<(M + 7) / 8, 256, 0, st>>>(A, M, K, lda, s, reinterpret_cast<float*>(base + L.inv_s));
+  if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess)
+    return set_error(ELV_ECUDA, "fp16x3: memset");
+  k16_col_max<<<dim3((N + 255) / 256, (K + 255) / 256), 256, 0, st>>>(B, K, N, ldb, tmax);
+  int gx, gy;
+  split_a_grid(M, Kp, &gx, &gy);
+  k16_split_a<<<dim3(gx, gy), 256, 0, st>>>(A, M, K, lda, Kp, s, reinterpret_cast<__half*>(base + L.a_hi),
+                                            reinterpret_cast<__half*>(base + L.a_lo));
+  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 31) / 32), 256, 0, st>>>(
+      B, K, N, ldb, Kp, tmax, reinterpret_cast<__half*>(base + L.b_hi), reinterpret_cast<__half*>(base + L.b_lo),
+      reinterpret_cast<float*>(base + L.inv_t));
+  return check_launch("fp16x3_prepare");
+}
+
+int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!fp16x3_applicable(M, N, K)) return tf32x3_compute(C, M, N, K, ldc, ws, ws_bytes, st);
+  const F16Layout L = f16_layout(M, N, K);
+  if (ws == nullptr || ws_bytes < L.total) return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127)) - 128;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return launch_pair<64, true>(base + L.a_hi, base + L.a_lo, base + L.b_hi, base + L.b_lo, C, M, N, K,
+                               (int)kpad16(K), ldc, dev, st, reinterpret_cast<const float*>(base + L.inv_s),
+                               reinterpret_cast<const float*>(base + L.inv_t));
 }
 
 }  // namespace elv

@@ -33,7 +33,7 @@ from ._ref import S
 
 VARIANTS = {
     "baseline": 0, "blocking": 1, "vectorized": 2, "loopPerm": 3,
-    "arrayPacking": 4, "cacheBlocks": 5, "parallel": 6, "parallel_tf32x3": 7,
+    "arrayPacking": 4, "cacheBlocks": 5, "parallel": 6, "parallel_tf32x3": 7, "parallel_fp16x3": 8,
 }
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
@@ -126,7 +126,7 @@ def term_shape(term):
     return da[0], db[1], da[1]
 
 
-def decode(term, arg_shapes=None, tf32x3: bool = False) -> KernelPlan:
+def decode(term, arg_shapes=None, tf32x3: bool = False, tc_encoding: str = "tf32") -> KernelPlan:
     """Map a lowered term (and the argument shapes) to a kernel plan."""
     nf = S().normal_forms
     Mt, Nt, Kt = term_shape(term)
@@ -159,6 +159,8 @@ def decode(term, arg_shapes=None, tf32x3: bool = False) -> KernelPlan:
     if tf32x3:
         if name != "parallel":
             raise EvalError("the 3xTF32 tcgen05 variant is attached to the parallel schedule")
-        variant = VARIANTS["parallel_tf32x3"]
+        if tc_encoding not in ("tf32", "fp16"):
+            raise EvalError(f"unknown tensor-core encoding {tc_encoding!r} (tf32 | fp16)")
+        variant = VARIANTS["parallel_tf32x3" if tc_encoding == "tf32" else "parallel_fp16x3"]
     return KernelPlan(name, variant, M, N, K, (Mt, Nt, Kt),
                       (M, N, K) != (Mt, Nt, Kt), f)

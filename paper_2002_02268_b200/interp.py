@@ -43,10 +43,15 @@ def _default_tf32x3() -> bool:
     return os.environ.get("ELV_TF32X3", "0") not in ("", "0", "false", "False")
 
 
-def plan(e, arg_shapes, tf32x3: bool | None = None) -> dispatch.KernelPlan:
+def _default_encoding() -> str:
+    return os.environ.get("ELV_TC_ENCODING", "tf32")
+
+
+def plan(e, arg_shapes, tf32x3: bool | None = None, tc_encoding: str | None = None) -> dispatch.KernelPlan:
     """Decode (cached per term object) and bind to the argument shapes."""
     tf32x3 = _default_tf32x3() if tf32x3 is None else tf32x3
-    key = (tuple(map(tuple, arg_shapes)), bool(tf32x3))
+    tc_encoding = _default_encoding() if tc_encoding is None else tc_encoding
+    key = (tuple(map(tuple, arg_shapes)), bool(tf32x3), tc_encoding)
     per_term = _plan_cache.get(e)
     if per_term is None:
         per_term = {}
@@ -56,7 +61,7 @@ def plan(e, arg_shapes, tf32x3: bool | None = None) -> dispatch.KernelPlan:
             pass
     p = per_term.get(key)
     if p is None:
-        p = dispatch.decode(e, arg_shapes, tf32x3=tf32x3)
+        p = dispatch.decode(e, arg_shapes, tf32x3=tf32x3, tc_encoding=tc_encoding)
         per_term[key] = p
     return p
 
@@ -101,7 +106,7 @@ class GemmCall:
     Launches per call: prepare 0 (variants 0-3), 1 (4, 5: packB; 6: packB, or
     packA+packB fused; 7: fused hi/lo split of A and B); compute 1."""
 
-    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1}
+    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 4}
 
     def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
         self.lib = _lib.load()
@@ -136,9 +141,9 @@ class GemmCall:
 
 
 def run_tensor(e, A: torch.Tensor, B: torch.Tensor, out=None, stream=None,
-               tf32x3: bool | None = None) -> torch.Tensor:
+               tf32x3: bool | None = None, tc_encoding: str | None = None) -> torch.Tensor:
     """Tensor-returning variant of `run`: device in, device out, async."""
-    p = plan(e, [tuple(A.shape), tuple(B.shape)], tf32x3)
+    p = plan(e, [tuple(A.shape), tuple(B.shape)], tf32x3, tc_encoding)
     return gemm(p, A, B, out=out, stream=stream)
 
 
@@ -265,7 +270,7 @@ def _run_generic(e, args, device=None):
     return out if (ts and ts[0].is_cuda) else out.cpu()
 
 
-def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
+def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None, tc_encoding: str | None = None):
     """Evaluate the program `e` applied to `args` on a B200.
 
     Mirrors stratir.interp.run (interp.py:157-162).  The seven GEMM schedules
@@ -278,14 +283,15 @@ def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
     the result is written into and returned.  Large host-resident GEMMs go
     through `HostPipeline` (transfers overlapped with the kernel)."""
     try:
-        return _run_template(e, args, device=device, tf32x3=tf32x3, out=out)
+        return _run_template(e, args, device=device, tf32x3=tf32x3, out=out, tc_encoding=tc_encoding)
     except S().interp.EvalError as err:
         if not _no_template(err):
             raise
         return _run_generic(e, args, device)
 
 
-def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out=None):
+def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out=None,
+                  tc_encoding: str | None = None):
     if len(args) == 1:
         return _run_binomial(e, args[0], device)
     if len(args) != 2:
@@ -295,7 +301,7 @@ def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out
     for t in ts:
         if t.dim() != 2:
             raise EvalError("map expects an array of arrays")
-    p = plan(e, [tuple(t.shape) for t in ts], tf32x3)
+    p = plan(e, [tuple(t.shape) for t in ts], tf32x3, tc_encoding)
     if device is None:
         device = ts[0].device if ts[0].is_cuda else torch.device("cuda", torch.cuda.current_device())
     on_host = not ts[0].is_cuda
