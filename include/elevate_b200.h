@@ -142,6 +142,19 @@ int elv_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t 
  * (kind 0 = H2D item landed, 1 = tile GEMM done, 2 = tile D2H done). */
 int elv_gemm_host_trace(float* out, int cap);
 
+/* 3xFP16 building blocks (variant 8 in pieces, like the 3xTF32 ones above).
+ * Planes = [hi | lo] fp16 rows x Kp (Kp = K rounded up to 64, K-major) plus
+ * the per-row (A) / per-column (B) power-of-two scales.  split_b takes
+ * row-major B (K x N, ldb) and writes B transposed.  gemm_planes requires
+ * elv_fp16x3_applicable(M, N, K) (K >= 512, >= 148 256x256 tiles). */
+size_t elv_fp16x3_a_planes_bytes(int M, int K);
+size_t elv_fp16x3_b_planes_bytes(int N, int K);
+int elv_fp16x3_applicable(int M, int N, int K);
+int elv_fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, void* stream);
+int elv_fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, void* stream);
+int elv_fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
+                           int M, int N, int K, int ldc, void* stream);
+
 /* Synthetic inputs: X[i] = U(-1,1) with 24-bit resolution from
  * splitmix64((seed << 48) ^ (tensor_id << 40) ^ (offset + i)); bit-identical
  * to paper_2002_02268_b200.synth.uniform() on the host. */

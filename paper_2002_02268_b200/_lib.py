@@ -25,6 +25,8 @@ EXPORTS = (
     "elv_tf32x3_split_a", "elv_tf32x3_split_b", "elv_tf32x3_split_b_packed",
     "elv_tf32x3_gemm_planes", "elv_binomial", "elv_binomial_variant_name",
     "elv_gemm_host", "elv_gemm_host_workspace_bytes", "elv_gemm_host_tiles", "elv_gemm_host_trace", "elv_copy2d",
+    "elv_fp16x3_a_planes_bytes", "elv_fp16x3_b_planes_bytes", "elv_fp16x3_applicable", "elv_fp16x3_split_a",
+    "elv_fp16x3_split_b", "elv_fp16x3_gemm_planes",
 )
 
 _lib = None
@@ -72,6 +74,12 @@ def load():
                                         ctypes.POINTER(c_int)]),
         "elv_gemm_host_trace": (c_int, [c_vp, c_int]),
         "elv_copy2d": (c_int, [c_vp, c_size, c_vp, c_size, c_size, c_size, c_int, c_vp]),
+        "elv_fp16x3_a_planes_bytes": (c_size, [c_int, c_int]),
+        "elv_fp16x3_b_planes_bytes": (c_size, [c_int, c_int]),
+        "elv_fp16x3_applicable": (c_int, [c_int, c_int, c_int]),
+        "elv_fp16x3_split_a": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
+        "elv_fp16x3_split_b": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
+        "elv_fp16x3_gemm_planes": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
         "elv_binomial": (c_int, [c_int, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
         "elv_binomial_variant_name": (ctypes.c_char_p, [c_int]),
         "elv_last_error": (ctypes.c_char_p, []),

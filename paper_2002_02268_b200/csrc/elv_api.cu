@@ -316,6 +316,29 @@ int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
   return tf32x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
 }
 
+size_t elv_fp16x3_a_planes_bytes(int M, int K) { return (M < 1 || K < 1) ? 0 : fp16x3_a_planes_bytes(M, K); }
+size_t elv_fp16x3_b_planes_bytes(int N, int K) { return (N < 1 || K < 1) ? 0 : fp16x3_b_planes_bytes(N, K); }
+int elv_fp16x3_applicable(int M, int N, int K) { return (M > 0 && N > 0 && K > 0) ? fp16x3_applicable(M, N, K) : 0; }
+
+int elv_fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, void* stream) {
+  if (bad_ptr(A) || bad_ptr(a_planes) || M < 1 || K < 1 || lda < K)
+    return set_error(ELV_EINVAL, "fp16x3_split_a: bad arguments");
+  return fp16x3_split_a(A, M, K, lda, a_planes, (cudaStream_t)stream);
+}
+
+int elv_fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, void* stream) {
+  if (bad_ptr(B) || bad_ptr(b_planes) || N < 1 || K < 1 || ldb < N)
+    return set_error(ELV_EINVAL, "fp16x3_split_b: bad arguments");
+  return fp16x3_split_b(B, K, N, ldb, b_planes, (cudaStream_t)stream);
+}
+
+int elv_fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
+                           void* stream) {
+  if (bad_ptr(a_planes) || bad_ptr(b_planes) || bad_ptr(C) || M < 1 || N < 1 || K < 1 || ldc < N)
+    return set_error(ELV_EINVAL, "fp16x3_gemm_planes: bad arguments");
+  return fp16x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
+}
+
 const char* elv_binomial_variant_name(int v) {
   static const char* names[ELV_BF_NUM_VARIANTS] = {"naive", "naivePar", "separated", "separatedPar"};
   return (v >= 0 && v < ELV_BF_NUM_VARIANTS) ? names[v] : "unknown";

@@ -90,6 +90,12 @@ size_t fp16x3_workspace_bytes(int M, int N, int K);
 int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
                    size_t ws_bytes, cudaStream_t st);
 int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t fp16x3_a_planes_bytes(int M, int K);
+size_t fp16x3_b_planes_bytes(int N, int K);
+int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st);
+int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st);
+int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
+                       cudaStream_t st);
 
 // binomial filter (stencil.cu)
 int launch_binomial(int variant, const float* img, float* out, int H, int W, int ldi, int ldo,

@@ -52,13 +52,14 @@ HostPlan make_plan(int v, int M, int N, int K) {
     // 3xTF32 is PCIe-bound (GEMM ~ D2H time): finer row blocks start the D2H
     // stream sooner.  The SIMT variants are GEMM-bound (~4.6x the PCIe time):
     // 8 row blocks keep each launch at >= 6 waves of 128x256 tiles.
-    const int fine = v == ELV_PARALLEL_TF32X3 ? 16 : 8;
+    const bool tc = v == ELV_PARALLEL_TF32X3 || v == ELV_PARALLEL_FP16X3;
+    const int fine = tc ? 16 : 8;
     const int row_blocks = M >= 8192 ? fine : (M >= 2048 ? 8 : (M >= 512 ? 2 : 1));
     p.R = (int)up((size_t)ceil_div(M, row_blocks), 256);
     if (p.R > M) p.R = M;
     // 3xTF32 (D2H-bound): 16384-column chunks (64 KB copy rows); SIMT
     // (GEMM-bound): 8192, so the first B chunk lands sooner
-    const int cw = v == ELV_PARALLEL_TF32X3 ? 16384 : 8192;
+    const int cw = tc ? 16384 : 8192;
     if (N >= 2 * cw) {
       const int chunks = ceil_div(N, cw);
       p.Nc = (int)up((size_t)ceil_div(N, chunks), 256);
@@ -82,14 +83,27 @@ HostPlan make_plan(int v, int M, int N, int K) {
   p.off_c = o;  o = up(o + (size_t)M * N * 4, kAlign);
   p.stride_pa = 0;
   if (v == ELV_PARALLEL_TF32X3) p.stride_pa = up(tf32x3_a_planes_bytes(p.R, K), kAlign);
+  else if (v == ELV_PARALLEL_FP16X3) p.stride_pa = up(fp16x3_a_planes_bytes(p.R, K), kAlign);
   else if (p.packed_a) p.stride_pa = up(pack_a_bytes(p.R, K), kAlign);
   p.off_pa = o;  o += p.stride_pa * p.nrb;
   p.stride_pb = 0;
   if (v == ELV_PARALLEL_TF32X3) p.stride_pb = up(tf32x3_b_planes_bytes(p.Nc, K), kAlign);
+  else if (v == ELV_PARALLEL_FP16X3) p.stride_pb = up(fp16x3_b_planes_bytes(p.Nc, K), kAlign);
   else if (v >= ELV_ARRAYPACKING) p.stride_pb = up(elv_pack_b_bytes(K, p.Nc), kAlign);
   p.off_pb = o;  o += p.stride_pb * p.ncb;
   p.total = o + kAlign;   // slack for aligning the caller's base pointer
   return p;
+}
+
+// The fp16 encoding needs every tile GEMM to qualify (K >= 512, a wave of
+// pair tiles); otherwise the whole call uses the tf32 encoding.
+int host_variant(int v, int M, int N, int K) {
+  if (v != ELV_PARALLEL_FP16X3) return v;
+  const HostPlan p = make_plan(ELV_PARALLEL_TF32X3, M, N, K);
+  const int rl = M - (p.nrb - 1) * p.R, cl = N - (p.ncb - 1) * p.Nc;
+  const bool ok = fp16x3_applicable(p.R, p.Nc, K) && fp16x3_applicable(rl, p.Nc, K) &&
+                  fp16x3_applicable(p.R, cl, K) && fp16x3_applicable(rl, cl, K);
+  return ok ? v : ELV_PARALLEL_TF32X3;
 }
 
 // Per-device copy streams and an event pool (library-internal, created once).
@@ -132,14 +146,14 @@ extern "C" {
 
 size_t elv_gemm_host_workspace_bytes(int variant, int M, int N, int K) {
   if (M < 1 || N < 1 || K < 1 || variant < 0 || variant >= ELV_NUM_VARIANTS) return 0;
-  if (variant == ELV_PARALLEL_FP16X3) variant = ELV_PARALLEL_TF32X3;
+  variant = host_variant(variant, M, N, K);
   return make_plan(variant, M, N, K).total;
 }
 
 int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols) {
   if (M < 1 || N < 1 || K < 1 || variant < 0 || variant >= ELV_NUM_VARIANTS)
     return set_error(ELV_EINVAL, "gemm_host_tiles: bad arguments");
-  if (variant == ELV_PARALLEL_FP16X3) variant = ELV_PARALLEL_TF32X3;
+  variant = host_variant(variant, M, N, K);
   const HostPlan p = make_plan(variant, M, N, K);
   if (rows) *rows = p.R;
   if (cols) *cols = p.Nc;
@@ -155,7 +169,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   if (lda < K || ldb < N || ldc < N)
     return set_error(ELV_EINVAL, "gemm_host: leading dimension too small (lda=%d ldb=%d ldc=%d)", lda, ldb, ldc);
   if (variant < 0 || variant >= ELV_NUM_VARIANTS) return set_error(ELV_EVARIANT, "unknown variant %d", variant);
-  if (variant == ELV_PARALLEL_FP16X3) variant = ELV_PARALLEL_TF32X3;   // per-tile prepare is tf32-encoded
+  variant = host_variant(variant, M, N, K);
   const HostPlan p = make_plan(variant, M, N, K);
   if (workspace == nullptr || workspace_bytes < p.total)
     return set_error(ELV_EWORKSPACE, "gemm_host: needs %zu workspace bytes, got %zu", p.total, workspace_bytes);
@@ -273,6 +287,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
     if (!have_b[j]) {
       CK(cudaStreamWaitEvent(st, ev_b[j], 0), "wait B chunk");
       if (variant == ELV_PARALLEL_TF32X3) rc = tf32x3_split_b(B_d + c0, K, nc, N, false, prep_b(j), st);
+      else if (variant == ELV_PARALLEL_FP16X3) rc = fp16x3_split_b(B_d + c0, K, nc, N, prep_b(j), st);
       else if (variant >= ELV_ARRAYPACKING) rc = launch_pack_b(B_d + c0, reinterpret_cast<float*>(prep_b(j)), K, nc, N, st);
       if (rc) return rc;
       have_b[j] = 1;
@@ -280,6 +295,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
     if (!have_a[i]) {
       CK(cudaStreamWaitEvent(st, ev_a[i], 0), "wait A block");
       if (variant == ELV_PARALLEL_TF32X3) rc = tf32x3_split_a(Ai, nr, K, K, prep_a(i), st);
+      else if (variant == ELV_PARALLEL_FP16X3) rc = fp16x3_split_a(Ai, nr, K, K, prep_a(i), st);
       else if (p.packed_a) rc = launch_pack_a(Ai, reinterpret_cast<float*>(prep_a(i)), nr, K, K, st);
       if (rc) return rc;
       have_a[i] = 1;
@@ -287,6 +303,8 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
     float* Cij = C_d + (size_t)r0 * N + c0;
     if (variant == ELV_PARALLEL_TF32X3) {
       rc = tf32x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st);
+    } else if (variant == ELV_PARALLEL_FP16X3) {
+      rc = fp16x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st);
     } else if (variant == ELV_PARALLEL && p.packed_a && parallel_uses_packed_a(nr, nc)) {
       rc = launch_parallel_packed(reinterpret_cast<const float*>(prep_a(i)),
                                   reinterpret_cast<const float*>(prep_b(j)), Cij, nr, nc, K, N, st);

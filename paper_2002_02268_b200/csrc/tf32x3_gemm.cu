@@ -1073,19 +1073,6 @@ __device__ __forceinline__ void pow2_scale(float m, float* s, float* inv) {
   *inv = ldexpf(1.f, e - 15);
 }
 
-// one warp per row of A: row maximum -> s_i, 1/s_i
-__global__ void __launch_bounds__(256)
-k16_row_scale(const float* __restrict__ A, int M, int K, int lda, float* __restrict__ s, float* __restrict__ inv) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (r >= M) return;
-  const float* row = A + (size_t)r * lda;
-  float m = 0.f;
-  for (int k = lane; k < K; k += 32) m = fmaxf(m, fabsf(__ldg(row + k)));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) pow2_scale(m, s + r, inv + r);
-}
-
 // column maxima of B (K x N row-major): a 256-row slab per block, one column
 // per thread, combined with an integer atomicMax on the (non-negative) bits
 __global__ void __launch_bounds__(256)
@@ -1104,72 +1091,127 @@ __device__ __forceinline__ void split16(float x, __half* hi, __half* lo) {
   *lo = __float2half_rn((x - __half2float(h)) * 2048.f);
 }
 
-// A planes: [M][Kp] hi and lo, K-major (A is already K-major), 4 k per thread
+// A planes: [M][Kp] hi and lo, K-major (A is already K-major).  One CTA per
+// row: the row is read once into registers, its maximum reduced across the
+// block, then scaled and split (row scale fused with the split).
 __global__ void __launch_bounds__(256)
-k16_split_a(const float* __restrict__ A, int M, int K, int lda, int Kp, const float* __restrict__ s,
-            __half* __restrict__ hi, __half* __restrict__ lo) {
-  const int k = (blockIdx.x * 256 + threadIdx.x) * 4;
-  if (k >= Kp) return;
-  for (int r = blockIdx.y; r < M; r += gridDim.y) {
-    const float sc = s[r];
-    const float* src = A + (size_t)r * lda;
-    __align__(8) __half h[4], l[4];
+k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
+                 float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo) {
+  __shared__ float red[8];
+  const int r = blockIdx.x;
+  const float* row = A + (size_t)r * lda;
+  float m = 0.f;
+  for (int k = threadIdx.x; k < K; k += 256) m = fmaxf(m, fabsf(__ldg(row + k)));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) split16(k + u < K ? __ldg(src + k + u) * sc : 0.f, &h[u], &l[u]);
-    const size_t o = (size_t)r * Kp + k;
-    *reinterpret_cast<uint2*>(hi + o) = *reinterpret_cast<const uint2*>(h);
-    *reinterpret_cast<uint2*>(lo + o) = *reinterpret_cast<const uint2*>(l);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+  float sc, iv;
+  pow2_scale(m, &sc, &iv);
+  if (threadIdx.x == 0) { s[r] = sc; inv[r] = iv; }
+  __half2* h2 = reinterpret_cast<__half2*>(hi + (size_t)r * Kp);
+  __half2* l2 = reinterpret_cast<__half2*>(lo + (size_t)r * Kp);
+  for (int k2 = threadIdx.x; k2 < Kp / 2; k2 += 256) {       // second read hits L1/L2
+    const int k = 2 * k2;
+    __half a0, a1, b0, b1;
+    split16(k < K ? __ldg(row + k) * sc : 0.f, &a0, &b0);
+    split16(k + 1 < K ? __ldg(row + k + 1) * sc : 0.f, &a1, &b1);
+    h2[k2] = __halves2half2(a0, a1);
+    l2[k2] = __halves2half2(b0, b1);
   }
 }
 
-// B planes: [N][Kp] (B transposed to K-major) through 32 x 32 SMEM tiles,
-// scaled by t_j from the column maxima; blocks with k0 == 0 also publish 1/t_j
+// column maxima -> per-column scale (in place over the max bits) and 1/t_j
 __global__ void __launch_bounds__(256)
-k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp,
-                      const unsigned int* __restrict__ maxbits, __half* __restrict__ hi, __half* __restrict__ lo,
-                      float* __restrict__ inv_t) {
-  __shared__ float t[32][33];
-  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+k16_col_scale(int N, float* __restrict__ s_bits, float* __restrict__ inv) {
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= N) return;
+  float sc, iv;
+  pow2_scale(__uint_as_float(reinterpret_cast<const unsigned int*>(s_bits)[j]), &sc, &iv);
+  s_bits[j] = sc;
+  inv[j] = iv;
+}
+
+// B planes: [N][Kp] (B transposed to K-major) through 64(k) x 32(n) SMEM
+// tiles: coalesced 128 B reads along B's rows, 128 B half2 writes along the
+// planes' rows; t_j from k16_col_scale.
+__global__ void __launch_bounds__(256)
+k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp, const float* __restrict__ t,
+                      __half* __restrict__ hi, __half* __restrict__ lo) {
+  __shared__ float tile[64][33];
+  const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < 8; ++r) {
     const int k = k0 + ty + 8 * r, n = n0 + tx;
-    t[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
+    tile[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const int n = n0 + ty + 8 * r, k = k0 + tx;
+    const int n = n0 + ty + 8 * r, k = k0 + 2 * tx;
     if (n < N && k < Kp) {
-      float sc, inv;
-      pow2_scale(__uint_as_float(maxbits[n]), &sc, &inv);
-      if (k0 == 0 && tx == 0) inv_t[n] = inv;
-      __half h, l;
-      split16(t[tx][ty + 8 * r] * sc, &h, &l);
-      hi[(size_t)n * Kp + k] = h;
-      lo[(size_t)n * Kp + k] = l;
+      const float sc = t[n];
+      __half a0, a1, b0, b1;
+      split16(tile[2 * tx][ty + 8 * r] * sc, &a0, &b0);
+      split16(tile[2 * tx + 1][ty + 8 * r] * sc, &a1, &b1);
+      *reinterpret_cast<__half2*>(hi + (size_t)n * Kp + k) = __halves2half2(a0, a1);
+      *reinterpret_cast<__half2*>(lo + (size_t)n * Kp + k) = __halves2half2(b0, b1);
     }
   }
 }
 
-struct F16Layout {
-  size_t a_hi, a_lo, b_hi, b_lo, s, inv_s, tmax, inv_t, total;
+// Plane buffers of the fp16 encoding (the unit the C ABI, the row-shard
+// broadcast and the host pipeline move around):
+//   A planes = [hi M x Kp | lo M x Kp] fp16 | s (M f32) | 1/s (M f32)
+//   B planes = [hi N x Kp | lo N x Kp] fp16 | t (N f32; max bits first) | 1/t (N f32)
+static inline size_t up128(size_t x) { return (x + 127) / 128 * 128; }
+size_t fp16x3_a_planes_bytes(int M, int K) {
+  return 128 + up128((size_t)M * kpad16(K) * 2) * 2 + up128((size_t)M * 4) * 2;
+}
+size_t fp16x3_b_planes_bytes(int N, int K) { return fp16x3_a_planes_bytes(N, K); }
+struct Planes16 {
+  __half *hi, *lo;
+  float* s;            // A: s_i ; B: max bits (as u32)
+  float* inv;          // 1/s_i or 1/t_j
 };
-static F16Layout f16_layout(int M, int N, int K) {
-  const size_t Kp = (size_t)kpad16(K);
-  F16Layout L{};
-  size_t o = 128;                                   // slack for aligning the base
-  auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 127) / 128 * 128; return at; };
-  L.a_hi = take((size_t)M * Kp * 2);
-  L.a_lo = take((size_t)M * Kp * 2);
-  L.b_hi = take((size_t)N * Kp * 2);
-  L.b_lo = take((size_t)N * Kp * 2);
-  L.s = take((size_t)M * 4);
-  L.inv_s = take((size_t)M * 4);
-  L.tmax = take((size_t)N * 4);
-  L.inv_t = take((size_t)N * 4);
-  L.total = o;
-  return L;
+static Planes16 planes16(const void* buf, int rows, int K) {
+  uint8_t* b = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
+  const size_t plane = up128((size_t)rows * kpad16(K) * 2), vec = up128((size_t)rows * 4);
+  return {reinterpret_cast<__half*>(b), reinterpret_cast<__half*>(b + plane),
+          reinterpret_cast<float*>(b + 2 * plane), reinterpret_cast<float*>(b + 2 * plane + vec)};
+}
+
+int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st) {
+  const Planes16 P = planes16(a_planes, M, K);
+  const int Kp = (int)kpad16(K);
+  k16_split_a_rows<<<M, 256, 0, st>>>(A, M, K, lda, Kp, P.s, P.inv, P.hi, P.lo);
+  return check_launch("fp16x3_split_a");
+}
+
+int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st) {
+  const Planes16 P = planes16(b_planes, N, K);
+  const int Kp = (int)kpad16(K);
+  unsigned int* tmax = reinterpret_cast<unsigned int*>(P.s);
+  if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
+  k16_col_max<<<dim3((N + 255) / 256, (K + 255) / 256), 256, 0, st>>>(B, K, N, ldb, tmax);
+  k16_col_scale<<<(N + 255) / 256, 256, 0, st>>>(N, P.s, P.inv);
+  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, P.s, P.hi, P.lo);
+  return check_launch("fp16x3_split_b");
+}
+
+int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
+                       cudaStream_t st) {
+  if (!fp16x3_applicable(M, N, K))
+    return set_error(ELV_EINVAL, "fp16x3: needs K >= 512 and >= %d 256x256 tiles (got %dx%dx%d)", num_sms(), M, N,
+                     K);
+  const Planes16 A = planes16(a_planes, M, K), B = planes16(b_planes, N, K);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return launch_pair<64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, (int)kpad16(K), ldc, dev, st, A.inv, B.inv);
 }
 
 // The fp16 encoding runs on the cta_group::2 kernel (>= one wave of pair
@@ -1179,43 +1221,27 @@ bool fp16x3_applicable(int M, int N, int K) {
   return K >= 512 && pair_tiles >= num_sms();
 }
 
+// elv_gemm workspace for variant 8 = [A planes | B planes] (or variant 7's)
 size_t fp16x3_workspace_bytes(int M, int N, int K) {
-  return fp16x3_applicable(M, N, K) ? f16_layout(M, N, K).total : tf32x3_workspace_bytes(M, N, K);
+  return fp16x3_applicable(M, N, K) ? fp16x3_a_planes_bytes(M, K) + fp16x3_b_planes_bytes(N, K)
+                                    : tf32x3_workspace_bytes(M, N, K);
 }
 
 int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
   if (!fp16x3_applicable(M, N, K)) return tf32x3_prepare(A, B, M, N, K, lda, ldb, ws, ws_bytes, st);
-  const F16Layout L = f16_layout(M, N, K);
-  if (ws == nullptr || ws_bytes < L.total) return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127)) - 128;
-  const int Kp = (int)kpad16(K);
-  float* s = reinterpret_cast<float*>(base + L.s);
-  unsigned int* tmax = reinterpret_cast<unsigned int*>(base + L.tmax);
-  k16_row_scale<<<(M + 7) / 8, 256, 0, st>>>(A, M, K, lda, s, reinterpret_cast<float*>(base + L.inv_s));
-  if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess)
-    return set_error(ELV_ECUDA, "fp16x3: memset");
-  k16_col_max<<<dim3((N + 255) / 256, (K + 255) / 256), 256, 0, st>>>(B, K, N, ldb, tmax);
-  int gx, gy;
-  split_a_grid(M, Kp, &gx, &gy);
-  k16_split_a<<<dim3(gx, gy), 256, 0, st>>>(A, M, K, lda, Kp, s, reinterpret_cast<__half*>(base + L.a_hi),
-                                            reinterpret_cast<__half*>(base + L.a_lo));
-  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 31) / 32), 256, 0, st>>>(
-      B, K, N, ldb, Kp, tmax, reinterpret_cast<__half*>(base + L.b_hi), reinterpret_cast<__half*>(base + L.b_lo),
-      reinterpret_cast<float*>(base + L.inv_t));
-  return check_launch("fp16x3_prepare");
+  if (ws == nullptr || ws_bytes < fp16x3_workspace_bytes(M, N, K))
+    return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
+  int rc = fp16x3_split_a(A, M, K, lda, ws, st);
+  if (rc) return rc;
+  return fp16x3_split_b(B, K, N, ldb, static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K), st);
 }
 
 int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (!fp16x3_applicable(M, N, K)) return tf32x3_compute(C, M, N, K, ldc, ws, ws_bytes, st);
-  const F16Layout L = f16_layout(M, N, K);
-  if (ws == nullptr || ws_bytes < L.total) return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 127) & ~uintptr_t(127)) - 128;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return launch_pair<64, true>(base + L.a_hi, base + L.a_lo, base + L.b_hi, base + L.b_lo, C, M, N, K,
-                               (int)kpad16(K), ldc, dev, st, reinterpret_cast<const float*>(base + L.inv_s),
-                               reinterpret_cast<const float*>(base + L.inv_t));
+  if (ws == nullptr || ws_bytes < fp16x3_workspace_bytes(M, N, K))
+    return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
+  return fp16x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
 }
 
 }  // namespace elv

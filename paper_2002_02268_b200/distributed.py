@@ -131,16 +131,30 @@ class PipelinedRowShardGemm:
         self._check = _lib.check
         self.plan, self.N, self.K, self.group, self.src = plan, N, K, group, src
         self.variant = plan.variant
-        if self.variant not in (4, 5, 6, 7):
-            raise ValueError("the pipelined row shard runs the packed variants (4..7)")
+        if self.variant not in (4, 5, 6, 7, 8):
+            raise ValueError("the pipelined row shard runs the packed / tensor-core variants (4..8)")
         self.device = device
         self.stream = stream or torch.cuda.current_stream(device)
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.chunks = column_chunks(N, chunks, first_weight=0.5 if chunks > 1 else 1.0)
-        self.prep = torch.cuda.Stream(device) if plan.variant == 7 else None
-        self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
         M = plan.M
+        if self.variant == 8 and not all(self.lib.elv_fp16x3_applicable(max(M, 1), n1 - n0, K)
+                                         for n0, n1 in self.chunks):
+            self.variant = 7                        # chunk GEMMs too small for the fp16 encoding
+        self.prep = torch.cuda.Stream(device) if self.variant == 7 else None
+        if self.variant == 8:
+            # rank src prepares each chunk's scaled fp16 planes and broadcasts
+            # them (4 B per element, as packed fp32 would be): no split on the
+            # receivers
+            self.a_planes = torch.empty(self.lib.elv_fp16x3_a_planes_bytes(max(M, 1), K), device=device,
+                                        dtype=torch.uint8)
+            self.b_planes = [torch.empty(self.lib.elv_fp16x3_b_planes_bytes(n1 - n0, K), device=device,
+                                         dtype=torch.uint8) for n0, n1 in self.chunks]
+            # per step: (src) column max, scale, split per chunk; A split; one GEMM per chunk
+            self.launches = (3 * len(self.chunks) if self.rank == src else 0) + 1 + len(self.chunks)
+            return
+        self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
         if self.variant == 7:
             self.a_planes = torch.empty(self.lib.elv_tf32x3_a_planes_bytes(max(M, 1), K),
                                         device=device, dtype=torch.uint8)
@@ -163,6 +177,8 @@ class PipelinedRowShardGemm:
         recorded after it (to start that chunk's D2H)."""
         lib, K, N, st = self.lib, self.K, self.N, self.stream.cuda_stream
         M = A_shard.shape[0]
+        if self.variant == 8:
+            return self._step_fp16(A_shard, B, C_shard, b_ready, a_ready, chunk_done)
         works = []
         with torch.cuda.stream(self.stream):
             for c, (n0, n1) in enumerate(self.chunks):
@@ -216,6 +232,37 @@ class PipelinedRowShardGemm:
                 self._check(lib.elv_gemm_prepacked(self.variant, A_shard.data_ptr(), self._panel(n0).data_ptr(),
                                                    C_shard.data_ptr() + 4 * n0, M, n1 - n0, K, A_shard.stride(0),
                                                    C_shard.stride(0), st), "elv_gemm_prepacked")
+                self._done(chunk_done, c, n0, n1)
+        return C_shard
+
+    def _step_fp16(self, A_shard, B, C_shard, b_ready, a_ready, chunk_done):
+        lib, K, st = self.lib, self.K, self.stream.cuda_stream
+        M = A_shard.shape[0]
+        works = []
+        with torch.cuda.stream(self.stream):
+            for c, ((n0, n1), bp) in enumerate(zip(self.chunks, self.b_planes)):
+                if self.rank == self.src:
+                    if b_ready is not None:
+                        self.stream.wait_event(b_ready[c])
+                    self._check(lib.elv_fp16x3_split_b(B.data_ptr() + 4 * n0, K, n1 - n0, B.stride(0),
+                                                       bp.data_ptr(), st), "elv_fp16x3_split_b")
+                works.append(dist.broadcast(bp, src=self.src, group=self.group, async_op=True)
+                             if self.world > 1 else None)
+            if M == 0:
+                for w in works:
+                    if w is not None:
+                        w.wait()
+                return C_shard
+            if a_ready is not None:
+                self.stream.wait_event(a_ready)
+            self._check(lib.elv_fp16x3_split_a(A_shard.data_ptr(), M, K, A_shard.stride(0),
+                                               self.a_planes.data_ptr(), st), "elv_fp16x3_split_a")
+            for c, ((n0, n1), bp, w) in enumerate(zip(self.chunks, self.b_planes, works)):
+                if w is not None:
+                    w.wait()
+                self._check(lib.elv_fp16x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(),
+                                                       C_shard.data_ptr() + 4 * n0, M, n1 - n0, K,
+                                                       C_shard.stride(0), st), "elv_fp16x3_gemm_planes")
                 self._done(chunk_done, c, n0, n1)
         return C_shard
 

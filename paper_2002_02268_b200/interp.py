@@ -44,7 +44,11 @@ def _default_tf32x3() -> bool:
 
 
 def _default_encoding() -> str:
-    return os.environ.get("ELV_TC_ENCODING", "tf32")
+    """Operand encoding of the tcgen05 kernel when tf32x3 is requested:
+    "fp16" (3xFP16, scaled planes: 1.8x the throughput and half the error of
+    3xTF32 in every measured input class; falls back to tf32 for K < 512 or
+    fewer pair tiles than SMs) or "tf32" (the 3xTF32 split)."""
+    return os.environ.get("ELV_TC_ENCODING", "fp16")
 
 
 def plan(e, arg_shapes, tf32x3: bool | None = None, tc_encoding: str | None = None) -> dispatch.KernelPlan:
@@ -106,7 +110,7 @@ class GemmCall:
     Launches per call: prepare 0 (variants 0-3), 1 (4, 5: packB; 6: packB, or
     packA+packB fused; 7: fused hi/lo split of A and B); compute 1."""
 
-    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 4}
+    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 4}   # 8: A rows; B max, scale, split
 
     def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
         self.lib = _lib.load()

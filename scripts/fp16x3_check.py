@@ -28,7 +28,7 @@ def run_case(M, N, K, kind, enc, dev):
         A *= torch.pow(2.0, torch.randint(-20, 21, (M, K), generator=g).float()).to(dev)
         B *= torch.pow(2.0, torch.randint(-20, 21, (K, N), generator=g).float()).to(dev)
     term = schedules.apply_padded("parallel", M, N, K).term
-    C = interp.run_tensor(term, A, B, tf32x3=True, tc_encoding=enc)
+    C = interp.run_tensor(term, A, B, tf32x3=enc != "simt", tc_encoding="tf32" if enc == "simt" else enc)
     torch.cuda.synchronize()
     rows = np.r_[0:3, M // 2, M - 2:M]
     Ah, Bh = A[torch.from_numpy(rows).to(dev)].double().cpu().numpy(), B.double().cpu().numpy()
@@ -36,15 +36,19 @@ def run_case(M, N, K, kind, enc, dev):
     bnd = oracle.bound(K, ab)
     err = np.abs(C[torch.from_numpy(rows).to(dev)].cpu().numpy().astype(np.float64) - ref)
     r = err / np.maximum(bnd, 1e-300)
+    # the deterministic (worst-case) fp32 bound: gamma_K = K u / (1 - K u), u = 2^-24
+    u = 2.0 ** -24
+    rd = err / np.maximum(K * u / (1 - K * u) * ab, 1e-300)
     return {"M": M, "N": N, "K": K, "inputs": kind, "encoding": enc, "worst": float(r.max()),
-            "mean": float(r.mean()), "finite": bool(np.isfinite(C.cpu().numpy()).all())}
+            "mean": float(r.mean()), "worst_vs_gammaK": float(rd.max()),
+            "finite": bool(np.isfinite(C.cpu().numpy()).all())}
 
 
 def main():
     dev = torch.device("cuda", 0)
     for (M, N, K) in [(4096, 4096, 512), (4096, 4096, 1024), (4096, 8192, 8192), (8192, 8192, 4096)]:
         for kind in ("uniform", "scaled", "dynamic"):
-            for enc in ("tf32", "fp16"):
+            for enc in ("tf32", "fp16", "simt"):
                 print(json.dumps(run_case(M, N, K, kind, enc, dev)), flush=True)
 
 

@@ -24,10 +24,11 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     M, N, K = a.M or a.n, a.N or a.n, a.K or a.n
-    sched, tf = ("parallel", True) if a.variant == "parallel_tf32x3" else (a.variant, False)
+    sched, tf = ("parallel", True) if a.variant.startswith("parallel_") else (a.variant, False)
+    enc = "fp16" if a.variant == "parallel_fp16x3" else "tf32"
     dev = torch.device("cuda", 0)
     term = schedules.apply_padded(sched, M, N, K).term
-    p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf)
+    p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf, tc_encoding=enc)
     A = torch.empty((M, K), device=dev); synth.fill_device(A, 0, 0)
     B = torch.empty((K, N), device=dev); synth.fill_device(B, 0, 1)
     C = torch.empty((M, N), device=dev)

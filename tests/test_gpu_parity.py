@@ -23,7 +23,12 @@ VARIANTS = list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]
 
 
 def _sched(v):
-    return ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+    return ("parallel", True) if v.startswith("parallel_") else (v, False)
+
+
+def _enc(v):
+    """tc_encoding of a variant name (the library default is fp16)."""
+    return "fp16" if v == "parallel_fp16x3" else "tf32"
 
 
 def _device_inputs(M, N, K, seed, dev):
@@ -80,7 +85,7 @@ def test_1024_cubed_vs_interpreter_arithmetic(cuda, variant):
     M = N = K = 1024
     A, B = _device_inputs(M, N, K, 0, cuda)
     term = schedules.apply(name, M, N, K).term
-    C = interp.run_tensor(term, A, B, tf32x3=tf).cpu().numpy()
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant)).cpu().numpy()
     Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
     ref = oracle.mm_interp_f64(Ah, Bh, name)
     ok, worst = oracle.check(C, ref, oracle.absprod_np(Ah, Bh), K)
@@ -100,7 +105,7 @@ def test_odd_shapes_split_tails(cuda, shape, variant):
     M, N, K = shape
     A, B = _device_inputs(M, N, K, 11, cuda)
     term = schedules.apply_padded(name, M, N, K).term
-    C = interp.run_tensor(term, A, B, tf32x3=tf).cpu().numpy()
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant)).cpu().numpy()
     Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
     ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
     assert ok, f"{variant} {shape}: worst err/bound = {worst:.3g}"
@@ -116,7 +121,7 @@ def test_strided_and_misaligned_operands(cuda, variant):
     big_b = torch.empty((K, N + 5), device=cuda); synth.fill_device(big_b, 5, 1)
     A = big_a[:, 1:K + 1]          # base misaligned by 4 bytes, lda = K + 3
     B = big_b[:, 3:N + 3]
-    p = dispatch.decode(schedules.apply(name, M, N, K).term, [(M, K), (K, N)], tf32x3=tf)
+    p = dispatch.decode(schedules.apply(name, M, N, K).term, [(M, K), (K, N)], tf32x3=tf, tc_encoding=_enc(variant))
     out_big = torch.zeros((M, N + 1), device=cuda)
     C = interp.gemm(p, A, B, out=out_big[:, :N])
     Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
@@ -125,14 +130,14 @@ def test_strided_and_misaligned_operands(cuda, variant):
     assert torch.all(out_big[:, N] == 0)          # nothing written past the view
 
 
-@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "cacheBlocks"])
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "parallel_fp16x3", "cacheBlocks"])
 def test_8192_cubed_row_sample(cuda, variant):
     """configs[2] roofline shape: sampled rows against the f64 oracle."""
     name, tf = _sched(variant)
     M = N = K = 8192
     A, B = _device_inputs(M, N, K, 2, cuda)
     term = schedules.apply(name, M, N, K).term
-    C = interp.run_tensor(term, A, B, tf32x3=tf)
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant))
     rows = torch.tensor([0, 1, 127, 128, 4095, 4096, 8190, 8191] + list(range(1000, 8000, 1111)),
                         device=cuda)
     Cs = C[rows].cpu().numpy()
@@ -191,13 +196,13 @@ def test_error_vs_k_sweep(cuda, variant):
         M = N = 128
         A, B = _device_inputs(M, N, K, 21, cuda)
         term = schedules.apply_padded(name, M, N, K).term
-        C = interp.run_tensor(term, A, B, tf32x3=tf).cpu().numpy()
+        C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant)).cpu().numpy()
         Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
         ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
         assert ok, f"{variant} K={K}: worst err/bound = {worst:.3g}"
 
 
-@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3"])
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "parallel_fp16x3"])
 def test_bench_shape_row_sample(cuda, variant):
     """configs[3] maximum size (32768 x 32768 x 8192, the bench workload):
     sampled rows and a column sample against the f64 oracle."""
@@ -205,7 +210,7 @@ def test_bench_shape_row_sample(cuda, variant):
     M, N, K = 32768, 32768, 8192
     A, B = _device_inputs(M, N, K, 0, cuda)
     term = schedules.apply(name, M, N, K).term
-    C = interp.run_tensor(term, A, B, tf32x3=tf)
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant))
     rows = torch.tensor([0, 255, 256, 16383, 16384, 32511, 32767], device=cuda)
     cols = torch.tensor([0, 1, 255, 256, 20000, 32767], device=cuda)
     Bh = B.cpu().numpy()
@@ -255,7 +260,7 @@ def test_tf32x3_tile_widths_bitwise_identical(cuda, tmp_path, shape):
     assert ok, worst
 
 
-@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3"])
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "parallel_fp16x3"])
 def test_output_beyond_2_pow_31_elements(cuda, variant):
     """Maximum-size edge: C with more than 2^31 elements (8.6 GB), so every
     row/column offset must be computed in 64 bits; rows at the far end
@@ -265,7 +270,7 @@ def test_output_beyond_2_pow_31_elements(cuda, variant):
     sched, tf = _sched(variant)
     A, B = _device_inputs(M, N, K, 12, cuda)
     term = schedules.apply_padded(sched, M, N, K).term
-    C = interp.run_tensor(term, A, B, tf32x3=tf)
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant))
     torch.cuda.synchronize()
     rows = [0, 65535, 65536, M - 1]
     Ah, Bh = A[rows].cpu().numpy(), B.cpu().numpy()
@@ -275,7 +280,7 @@ def test_output_beyond_2_pow_31_elements(cuda, variant):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3"])
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "parallel_fp16x3"])
 def test_bench_shape_checksums_cover_every_element(cuda, variant):
     """configs[3] at full size, every element accounted for: the column sums
     e^T C must match (e^T A) B and the row sums C e must match A (B e) in
@@ -289,7 +294,8 @@ def test_bench_shape_checksums_cover_every_element(cuda, variant):
     name, tf = _sched(variant)
     M, N, K = 32768, 32768, 8192
     A, B = _device_inputs(M, N, K, 1, cuda)
-    C = interp.run_tensor(schedules.apply(name, M, N, K).term, A, B, tf32x3=tf)
+    C = interp.run_tensor(schedules.apply(name, M, N, K).term, A, B, tf32x3=tf,
+                          tc_encoding="fp16" if variant == "parallel_fp16x3" else "tf32")
     torch.cuda.synchronize()
     col = C.double().sum(0)
     row = C.double().sum(1)
@@ -311,3 +317,52 @@ def test_bench_shape_checksums_cover_every_element(cuda, variant):
     print(f"{variant}: checksum err / rss-bound: columns {col_ratio:.3g}, rows {row_ratio:.3g}")
     assert col_ratio <= 1.0, f"{variant}: column checksum err/rss-bound {col_ratio:.3g}"
     assert row_ratio <= 1.0, f"{variant}: row checksum err/rss-bound {row_ratio:.3g}"
+
+
+FP16X3_SHAPES = [(4096, 4096, 512), (3200, 5000, 1000), (4100, 4700, 2049), (8192, 8192, 8192)]
+
+
+@pytest.mark.parametrize("shape", FP16X3_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_fp16x3_vs_oracle(cuda, shape):
+    """The 3xFP16 encoding (variant 8) where it applies (>= one wave of pair
+    tiles, K >= 512), including ragged M/N/K: sampled rows and columns
+    against the f64 oracle, same tau as every other kernel."""
+    M, N, K = shape
+    A, B = _device_inputs(M, N, K, 13, cuda)
+    term = schedules.apply_padded("parallel", M, N, K).term
+    p = interp.plan(term, [(M, K), (K, N)], True, "fp16")
+    assert p.variant == 8
+    C = interp.run_tensor(term, A, B, tf32x3=True, tc_encoding="fp16")
+    rows = torch.tensor([0, 1, 255, 256, M // 2, M - 1], device=cuda)
+    As, Bh = A[rows].cpu().numpy(), B.cpu().numpy()
+    ok, worst = oracle.check(C[rows].cpu().numpy(), oracle.mm_f64(As, Bh), oracle.absprod_np(As, Bh), K)
+    assert ok, f"rows: worst {worst:.3g}"
+    cols = torch.tensor([0, 255, 256, N - 1], device=cuda)
+    Ah, Bc = A.cpu().numpy(), Bh[:, cols.cpu().numpy()]
+    ok, worst = oracle.check(C[:, cols].cpu().numpy(), oracle.mm_f64(Ah, Bc), oracle.absprod_np(Ah, Bc), K)
+    assert ok, f"cols: worst {worst:.3g}"
+
+
+def test_fp16x3_scaled_and_special_rows(cuda):
+    """Per-row / per-column power-of-two scaling: rows and columns scaled by
+    2^-60 .. 2^60 stay within the bound, an all-zero row gives exact zeros,
+    and shapes below the applicability threshold fall back to 3xTF32."""
+    M, N, K = 4096, 4096, 1024
+    A, B = _device_inputs(M, N, K, 14, cuda)
+    g = torch.Generator().manual_seed(3)
+    A *= torch.pow(2.0, torch.randint(-60, 61, (M, 1), generator=g).float()).to(cuda)
+    B *= torch.pow(2.0, torch.randint(-60, 61, (1, N), generator=g).float()).to(cuda)
+    A[7] = 0.0
+    term = schedules.apply("parallel", M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=True, tc_encoding="fp16")
+    assert torch.all(C[7] == 0)
+    rows = torch.tensor([0, 5, 1000, M - 1], device=cuda)
+    As, Bh = A[rows].double().cpu().numpy(), B.double().cpu().numpy()
+    ok, worst = oracle.check(C[rows].cpu().numpy(), oracle.mm_f64(As, Bh), oracle.absprod_np(As, Bh), K)
+    assert ok, worst
+    small = schedules.apply("parallel", 256, 256, 256).term
+    assert interp.plan(small, [(256, 256), (256, 256)], True, "fp16").variant == 8
+    A2, B2 = _device_inputs(256, 256, 256, 15, cuda)
+    ref = interp.run_tensor(small, A2, B2, tf32x3=True)                  # variant 7
+    got = interp.run_tensor(small, A2, B2, tf32x3=True, tc_encoding="fp16")
+    assert torch.equal(got, ref)                                        # same kernel below the threshold

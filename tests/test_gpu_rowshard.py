@@ -133,12 +133,13 @@ def test_host_pipeline_large_default_tiling(cuda):
     against the f64 oracle, and call 2 == call 1."""
     from paper_2002_02268_b200 import interp as I
     M, N, K = 4096, 16384, 1024
+    I._host_pipes.clear()
     term = schedules.apply("parallel", M, N, K).term
     A = torch.from_numpy(synth.matrix(M, K, 9, 0)).pin_memory()
     B = torch.from_numpy(synth.matrix(K, N, 9, 1)).pin_memory()
     C1 = torch.empty((M, N), pin_memory=True)
     I.run(term, [A, B], tf32x3=True, out=C1)
-    hp = I._host_pipes[(7, M, N, K, str(torch.device("cuda", torch.cuda.current_device())))]
+    (hp,) = [h for k, h in I._host_pipes.items() if k[1:4] == (M, N, K)]
     assert hp.tile == (512, 16384)
     C2 = torch.empty((M, N), pin_memory=True)
     I.run(term, [A, B], tf32x3=True, out=C2)
@@ -282,3 +283,36 @@ def test_host_row_shard_pipeline_two_ranks(cuda, variant):
     A = torch.from_numpy(synth.matrix(M, K, 5, 0)).to(cuda)
     B = torch.from_numpy(synth.matrix(K, N, 5, 1)).to(cuda)
     assert np.array_equal(C, interp.gemm(p, A, B).cpu().numpy())
+
+
+def _plan16(M, N, K):
+    return dispatch.decode(schedules.apply_padded("parallel", M, N, K).term, [(M, K), (K, N)], tf32x3=True,
+                           tc_encoding="fp16")
+
+
+def test_fp16x3_pipelined_and_host_paths_bitwise(cuda, monkeypatch):
+    """The 3xFP16 encoding through the chunked row-shard pipeline (planes
+    prepared per column chunk on the source rank) and through the host
+    pipeline (planes per tile) equals the single launch bit for bit: the
+    per-row / per-column scales do not depend on the tiling."""
+    from paper_2002_02268_b200 import interp as I
+    M, N, K = 8192, 16384, 1024
+    p = _plan16(M, N, K)
+    assert p.variant == 8
+    A = torch.empty((M, K), device=cuda); synth.fill_device(A, 9, 0)
+    B = torch.empty((K, N), device=cuda); synth.fill_device(B, 9, 1)
+    direct = I.gemm(p, A, B)
+    pipe = D.PipelinedRowShardGemm(p, N, K, cuda, chunks=4)
+    assert pipe.variant == 8
+    C = torch.full((M, N), float("nan"), device=cuda)
+    pipe.step(A, B, C)
+    torch.cuda.synchronize()
+    assert torch.equal(C, direct)
+    monkeypatch.setenv("ELV_HOST_TILES", "2048,8192")
+    I._host_pipes.clear()
+    hp = I.HostPipeline(p, cuda)
+    assert hp.tile == (2048, 8192)
+    out = torch.empty((M, N), pin_memory=True)
+    hp(A.cpu().pin_memory(), B.cpu().pin_memory(), out)
+    assert torch.equal(out, direct.cpu())
+    I._host_pipes.clear()
