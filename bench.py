@@ -527,7 +527,7 @@ def run_ladder(args, dev):
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     cublas = measure_cublas(dev)
     print(json.dumps({"workload": "library reference points (not our path)", **cublas}), flush=True)
-    cases = [(v, 1024) for v in list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]]
+    cases = [(v, 1024) for v in list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3", "parallel_fp16x3"]]
     cases += [(v, 8192) for v in ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3", "parallel_fp16x3")]
     stream = torch.cuda.current_stream(dev)
     for v, n in cases:

@@ -58,7 +58,7 @@ enum {
   ELV_PARALLEL_TF32X3 = 7, /* parallel term on tcgen05: 3xTF32, TMEM accum    */
   ELV_PARALLEL_FP16X3 = 8, /* same three products on scaled fp16 hi/lo planes:
                               half the bytes, kind::f16 (falls back to 7 for
-                              K < 512 or fewer pair tiles than SMs)          */
+                              K < 512)                                       */
   ELV_NUM_VARIANTS = 9
 };
 
@@ -146,7 +146,7 @@ int elv_gemm_host_trace(float* out, int cap);
  * Planes = [hi | lo] fp16 rows x Kp (Kp = K rounded up to 64, K-major) plus
  * the per-row (A) / per-column (B) power-of-two scales.  split_b takes
  * row-major B (K x N, ldb) and writes B transposed.  gemm_planes requires
- * elv_fp16x3_applicable(M, N, K) (K >= 512, >= 148 256x256 tiles). */
+ * elv_fp16x3_applicable(M, N, K) (K >= 512). */
 size_t elv_fp16x3_a_planes_bytes(int M, int K);
 size_t elv_fp16x3_b_planes_bytes(int N, int K);
 int elv_fp16x3_applicable(int M, int N, int K);

@@ -44,15 +44,18 @@ constexpr int TMEM_COLS = 512;                    // pair kernel: D_big + D_smal
 // The 1-CTA kernel is templated on its N tile (256, 128 or 64): narrow tiles
 // give small problems (e.g. 1024^3: 32 tiles of 128x256 for 148 SMs) more
 // CTAs.  Per-element arithmetic does not depend on the tile shape.
-template <int TBN, int TBK = BK> struct OneCfg {
-  static constexpr int A_TILE = BM * TBK * 4;
-  static constexpr int B_TILE = TBN * TBK * 4;
+template <int TBN, int TBK = BK, bool F16 = false> struct OneCfg {
+  static constexpr int EB = F16 ? 2 : 4;               // bytes per operand element
+  static constexpr int ROW_BYTES = TBK * EB;            // 64 or 128 (swizzle width)
+  static constexpr int A_TILE = BM * ROW_BYTES;
+  static constexpr int B_TILE = TBN * ROW_BYTES;
   static constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;
   static constexpr int NST = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
   static constexpr int TMEM = 2 * TBN;             // D_big | D_small
   static constexpr int SMEM = NST * STAGE + 256 + 1024;
-  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
-                                    ((uint32_t)(BM >> 4) << 24);
+  static constexpr int KSUB = TBK / (F16 ? 16 : 8);     // MMAs per product per stage
+  static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
+                                    ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 };
 inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
@@ -104,16 +107,28 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
+template <bool F16>
+__device__ __forceinline__ void tc_mma_one(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  if (F16) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -194,13 +209,14 @@ struct TileSched {
   }
 };
 
-template <int TBN, int TBK>
+template <int TBN, int TBK, bool F16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
           float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
-          unsigned int* __restrict__ wave_ctr) {
-  using Cfg = OneCfg<TBN, TBK>;
+          unsigned int* __restrict__ wave_ctr, const float* __restrict__ inv_s,
+          const float* __restrict__ inv_t) {
+  using Cfg = OneCfg<TBN, TBK, F16>;
   constexpr int STAGES = Cfg::NST;
   constexpr int STAGE_BYTES = Cfg::STAGE;
   constexpr int B_TILE_BYTES = Cfg::B_TILE;
@@ -281,18 +297,18 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          const uint64_t ahi = umma_desc_k<TBK>(st);
-          const uint64_t alo = umma_desc_k<TBK>(st + A_TILE_BYTES);
-          const uint64_t bhi = umma_desc_k<TBK>(st + 2 * A_TILE_BYTES);
-          const uint64_t blo = umma_desc_k<TBK>(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+          const uint64_t ahi = umma_desc_k<Cfg::ROW_BYTES / 4>(st);
+          const uint64_t alo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + A_TILE_BYTES);
+          const uint64_t bhi = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES);
+          const uint64_t blo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
+          for (int k = 0; k < Cfg::KSUB; ++k) {
             const uint64_t koff = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along the row
             const uint32_t acc = (kb | k) != 0;                 // 0: overwrite (first k-step)
-            tc_mma_tf32(d_small, ahi + koff, blo + koff, kIdesc, acc);
-            tc_mma_tf32(d_small, alo + koff, bhi + koff, kIdesc, 1u);
-            if (with_lolo) tc_mma_tf32(d_small, alo + koff, blo + koff, kIdesc, 1u);
-            tc_mma_tf32(d_big, ahi + koff, bhi + koff, kIdesc, acc);
+            tc_mma_one<F16>(d_small, ahi + koff, blo + koff, kIdesc, acc);
+            tc_mma_one<F16>(d_small, alo + koff, bhi + koff, kIdesc, 1u);
+            if (!F16 && with_lolo) tc_mma_one<F16>(d_small, alo + koff, blo + koff, kIdesc, 1u);
+            tc_mma_one<F16>(d_big, ahi + koff, bhi + koff, kIdesc, acc);
           }
           tc_commit(&empty[s]);                 // frees the slot when these MMAs finish
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -319,9 +335,18 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
         tmem_ld_32x32b_x32(lane_base + (uint32_t)(c * 32), rb);
         tmem_ld_32x32b_x32(lane_base + (uint32_t)(BN + c * 32), rs);
         float v[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
         const int col = n0 + c * 32;
+        if (F16) {                                 // see the pair kernel: exact power-of-two unscaling
+          const float rs_i = row < M ? __ldg(inv_s + row) : 0.f;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float tj = col + q < N ? __ldg(inv_t + col + q) : 0.f;
+            v[q] = (__uint_as_float(rb[q]) + __uint_as_float(rs[q]) * 0x1p-11f) * rs_i * tj;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
+        }
         if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
@@ -960,19 +985,20 @@ static int one_cta_bn(int M, int N) {
   return best;
 }
 
-template <int TBN, int TBK>
-static int launch_one(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo, float* C,
-                      int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st) {
-  using Cfg = OneCfg<TBN, TBK>;
+template <int TBN, int TBK, bool F16 = false>
+static int launch_one(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C,
+                      int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st,
+                      const float* inv_s = nullptr, const float* inv_t = nullptr) {
+  using Cfg = OneCfg<TBN, TBK, F16>;
   CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
-  int rc = make_map(&m_ahi, a_hi, M, Kp, BM, TBK);
-  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM, TBK);
-  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, TBN, TBK);
-  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, TBN, TBK);
+  int rc = make_map(&m_ahi, a_hi, M, Kp, BM, TBK, F16);
+  if (!rc) rc = make_map(&m_alo, a_lo, M, Kp, BM, TBK, F16);
+  if (!rc) rc = make_map(&m_bhi, b_hi, N, Kp, TBN, TBK, F16);
+  if (!rc) rc = make_map(&m_blo, b_lo, N, Kp, TBN, TBK, F16);
   if (rc) return rc;
   static int attr_dev = -1;
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3<TBN, TBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3<TBN, TBK, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::SMEM);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 smem attribute: %s", cudaGetErrorString(e));
     attr_dev = dev;
@@ -980,8 +1006,9 @@ static int launch_one(const float* a_hi, const float* a_lo, const float* b_hi, c
   const int tiles = ((M + BM - 1) / BM) * ((N + TBN - 1) / TBN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   unsigned int* ctr = tiles > grid ? wave_counter(dev, st) : nullptr;
-  cudaError_t e = launch_pdl(k7_tf32x3<TBN, TBK>, dim3(grid), dim3(NUM_THREADS), (size_t)Cfg::SMEM, st, m_ahi,
-                             m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / TBK, with_lolo(K), tile_group(16), ctr);
+  cudaError_t e = launch_pdl(k7_tf32x3<TBN, TBK, F16>, dim3(grid), dim3(NUM_THREADS), (size_t)Cfg::SMEM, st, m_ahi,
+                             m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / TBK, F16 ? 0 : with_lolo(K), tile_group(16), ctr, inv_s,
+                             inv_t);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3");
 }
@@ -1073,16 +1100,21 @@ __device__ __forceinline__ void pow2_scale(float m, float* s, float* inv) {
   *inv = ldexpf(1.f, e - 15);
 }
 
-// column maxima of B (K x N row-major): a 256-row slab per block, one column
+// column maxima of B (K x N row-major): a 64-row slab per block, one column
 // per thread, combined with an integer atomicMax on the (non-negative) bits
-__global__ void __launch_bounds__(256)
-k16_col_max(const float* __restrict__ B, int K, int N, int ldb, unsigned int* __restrict__ maxbits) {
-  const int j = blockIdx.x * 256 + threadIdx.x;
+constexpr int COLMAX_SLAB = 64;
+__device__ __forceinline__ void col_max_slab(const float* __restrict__ B, int K, int N, int ldb, int bx, int by,
+                                             unsigned int* __restrict__ maxbits) {
+  const int j = bx * 256 + threadIdx.x;
   if (j >= N) return;
-  const int k0 = blockIdx.y * 256, k1 = min(K, k0 + 256);
+  const int k0 = by * COLMAX_SLAB, k1 = min(K, k0 + COLMAX_SLAB);
   float m = 0.f;
   for (int k = k0; k < k1; ++k) m = fmaxf(m, fabsf(__ldg(B + (size_t)k * ldb + j)));
   atomicMax(maxbits + j, __float_as_uint(m));
+}
+__global__ void __launch_bounds__(256)
+k16_col_max(const float* __restrict__ B, int K, int N, int ldb, unsigned int* __restrict__ maxbits) {
+  col_max_slab(B, K, N, ldb, blockIdx.x, blockIdx.y, maxbits);
 }
 
 __device__ __forceinline__ void split16(float x, __half* hi, __half* lo) {
@@ -1094,11 +1126,10 @@ __device__ __forceinline__ void split16(float x, __half* hi, __half* lo) {
 // A planes: [M][Kp] hi and lo, K-major (A is already K-major).  One CTA per
 // row: the row is read once into registers, its maximum reduced across the
 // block, then scaled and split (row scale fused with the split).
-__global__ void __launch_bounds__(256)
-k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
-                 float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo) {
+__device__ __forceinline__ void split_a_row(const float* __restrict__ A, int K, int lda, int Kp, int r,
+                                            float* __restrict__ s, float* __restrict__ inv, __half* __restrict__ hi,
+                                            __half* __restrict__ lo) {
   __shared__ float red[8];
-  const int r = blockIdx.x;
   const float* row = A + (size_t)r * lda;
   float m = 0.f;
   for (int k = threadIdx.x; k < K; k += 256) m = fmaxf(m, fabsf(__ldg(row + k)));
@@ -1123,27 +1154,41 @@ k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, flo
     l2[k2] = __halves2half2(b0, b1);
   }
 }
-
-// column maxima -> per-column scale (in place over the max bits) and 1/t_j
 __global__ void __launch_bounds__(256)
-k16_col_scale(int N, float* __restrict__ s_bits, float* __restrict__ inv) {
-  const int j = blockIdx.x * 256 + threadIdx.x;
-  if (j >= N) return;
-  float sc, iv;
-  pow2_scale(__uint_as_float(reinterpret_cast<const unsigned int*>(s_bits)[j]), &sc, &iv);
-  s_bits[j] = sc;
-  inv[j] = iv;
+k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
+                 float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo) {
+  split_a_row(A, K, lda, Kp, blockIdx.x, s, inv, hi, lo);
+}
+
+// elv_gemm's variant-8 prepare in one launch: blocks [0, M) scale and split
+// the rows of A, the rest take column-maximum slabs of B (independent work)
+__global__ void __launch_bounds__(256)
+k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
+            float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo, const float* __restrict__ B,
+            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits) {
+  const int b = blockIdx.x;
+  if (b < M) split_a_row(A, K, lda, Kp, b, s, inv, hi, lo);
+  else col_max_slab(B, K, N, ldb, (b - M) % gxb, (b - M) / gxb, maxbits);
 }
 
 // B planes: [N][Kp] (B transposed to K-major) through 64(k) x 32(n) SMEM
 // tiles: coalesced 128 B reads along B's rows, 128 B half2 writes along the
-// planes' rows; t_j from k16_col_scale.
+// planes' rows.  Each block turns its 32 columns' maxima (k16_col_max) into
+// scales once; the blocks of the first k-tile publish 1/t_j.
 __global__ void __launch_bounds__(256)
-k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp, const float* __restrict__ t,
-                      __half* __restrict__ hi, __half* __restrict__ lo) {
+k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp,
+                      const unsigned int* __restrict__ maxbits, __half* __restrict__ hi, __half* __restrict__ lo,
+                      float* __restrict__ inv_t) {
   __shared__ float tile[64][33];
+  __shared__ float scale[32];
   const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (ty == 0) {
+    float sc = 1.f, iv = 1.f;
+    if (n0 + tx < N) pow2_scale(__uint_as_float(maxbits[n0 + tx]), &sc, &iv);
+    scale[tx] = sc;
+    if (blockIdx.y == 0 && n0 + tx < N) inv_t[n0 + tx] = iv;
+  }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int k = k0 + ty + 8 * r, n = n0 + tx;
@@ -1152,12 +1197,12 @@ k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const int n = n0 + ty + 8 * r, k = k0 + 2 * tx;
+    const int nl = ty + 8 * r, n = n0 + nl, k = k0 + 2 * tx;
     if (n < N && k < Kp) {
-      const float sc = t[n];
+      const float sc = scale[nl];
       __half a0, a1, b0, b1;
-      split16(tile[2 * tx][ty + 8 * r] * sc, &a0, &b0);
-      split16(tile[2 * tx + 1][ty + 8 * r] * sc, &a1, &b1);
+      split16(tile[2 * tx][nl] * sc, &a0, &b0);
+      split16(tile[2 * tx + 1][nl] * sc, &a1, &b1);
       *reinterpret_cast<__half2*>(hi + (size_t)n * Kp + k) = __halves2half2(a0, a1);
       *reinterpret_cast<__half2*>(lo + (size_t)n * Kp + k) = __halves2half2(b0, b1);
     }
@@ -1197,28 +1242,38 @@ int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaSt
   const int Kp = (int)kpad16(K);
   unsigned int* tmax = reinterpret_cast<unsigned int*>(P.s);
   if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
-  k16_col_max<<<dim3((N + 255) / 256, (K + 255) / 256), 256, 0, st>>>(B, K, N, ldb, tmax);
-  k16_col_scale<<<(N + 255) / 256, 256, 0, st>>>(N, P.s, P.inv);
-  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, P.s, P.hi, P.lo);
+  k16_col_max<<<dim3((N + 255) / 256, (K + COLMAX_SLAB - 1) / COLMAX_SLAB), 256, 0, st>>>(B, K, N, ldb, tmax);
+  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, tmax, P.hi, P.lo,
+                                                                             P.inv);
   return check_launch("fp16x3_split_b");
 }
 
 int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                        cudaStream_t st) {
   if (!fp16x3_applicable(M, N, K))
-    return set_error(ELV_EINVAL, "fp16x3: needs K >= 512 and >= %d 256x256 tiles (got %dx%dx%d)", num_sms(), M, N,
-                     K);
+    return set_error(ELV_EINVAL, "fp16x3: needs K >= 512 (got %dx%dx%d)", M, N, K);
   const Planes16 A = planes16(a_planes, M, K), B = planes16(b_planes, N, K);
+  const int Kp = (int)kpad16(K);
   int dev = 0;
   cudaGetDevice(&dev);
-  return launch_pair<64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, (int)kpad16(K), ldc, dev, st, A.inv, B.inv);
+  if (pair_mode(M, N) != 0)
+    return launch_pair<64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
+  // fewer pair tiles than SMs: the 1-CTA kernel, 128 B stage rows for the
+  // narrow N tiles, 64 B for N = 256 (keeps 4 stages)
+  const int bn = one_cta_bn(M, N);
+  if (bn == 64) return launch_one<64, 64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
+  if (bn == 128)
+    return launch_one<128, 64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
+  return launch_one<256, 32, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
 }
 
-// The fp16 encoding runs on the cta_group::2 kernel (>= one wave of pair
-// tiles) for K >= 512 (no lo.lo term); anything else uses the tf32 encoding.
+// The fp16 encoding has no lo.lo term (lo is pre-scaled by 2^11, so lo.lo
+// would need a third accumulator scale): it serves K >= 512, where that
+// term is below the bound; shorter reductions use the tf32 encoding.
 bool fp16x3_applicable(int M, int N, int K) {
-  const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
-  return K >= 512 && pair_tiles >= num_sms();
+  (void)M;
+  (void)N;
+  return K >= 512;
 }
 
 // elv_gemm workspace for variant 8 = [A planes | B planes] (or variant 7's)
@@ -1232,9 +1287,19 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   if (!fp16x3_applicable(M, N, K)) return tf32x3_prepare(A, B, M, N, K, lda, ldb, ws, ws_bytes, st);
   if (ws == nullptr || ws_bytes < fp16x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
-  int rc = fp16x3_split_a(A, M, K, lda, ws, st);
-  if (rc) return rc;
-  return fp16x3_split_b(B, K, N, ldb, static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K), st);
+  // memset + [A rows | B column maxima] + B split-transpose: two launches
+  const Planes16 PA = planes16(ws, M, K);
+  const Planes16 PB = planes16(static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K), N, K);
+  const int Kp = (int)kpad16(K);
+  unsigned int* tmax = reinterpret_cast<unsigned int*>(PB.s);
+  if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
+  const int gxb = (N + 255) / 256, gyb = (K + COLMAX_SLAB - 1) / COLMAX_SLAB;
+  const long long blocks = (long long)M + (long long)gxb * gyb;
+  if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
+  k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax);
+  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, tmax, PB.hi, PB.lo,
+                                                                             PB.inv);
+  return check_launch("fp16x3_prepare");
 }
 
 int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {

@@ -151,8 +151,8 @@ class PipelinedRowShardGemm:
                                         dtype=torch.uint8)
             self.b_planes = [torch.empty(self.lib.elv_fp16x3_b_planes_bytes(n1 - n0, K), device=device,
                                          dtype=torch.uint8) for n0, n1 in self.chunks]
-            # per step: (src) column max, scale, split per chunk; A split; one GEMM per chunk
-            self.launches = (3 * len(self.chunks) if self.rank == src else 0) + 1 + len(self.chunks)
+            # per step: (src) column max + split per chunk; A split; one GEMM per chunk
+            self.launches = (2 * len(self.chunks) if self.rank == src else 0) + 1 + len(self.chunks)
             return
         self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
         if self.variant == 7:

@@ -110,7 +110,7 @@ class GemmCall:
     Launches per call: prepare 0 (variants 0-3), 1 (4, 5: packB; 6: packB, or
     packA+packB fused; 7: fused hi/lo split of A and B); compute 1."""
 
-    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 4}   # 8: A rows; B max, scale, split
+    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 2}   # 8: [A rows | B max], B split
 
     def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
         self.lib = _lib.load()

@@ -119,7 +119,7 @@ def test_host_pipeline_bitwise_equals_device_path(cuda, variant, tiles, monkeypa
     B = torch.from_numpy(synth.matrix(K, N, 8, 1)).pin_memory()
     C_host = I.run(term, [A, B], tf32x3=tf)
     assert not C_host.is_cuda
-    p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf)
+    p = I.plan(term, [(M, K), (K, N)], tf)         # the same plan (default encoding) run() used
     if tiles:
         assert I._host_pipes and next(iter(I._host_pipes.values())).tile == (384, 1280)
     C_dev = I.gemm(p, A.to(cuda), B.to(cuda)).cpu()
