@@ -21,16 +21,17 @@ from paper_2002_02268_b200 import binomial, interp, schedules, synth  # noqa: E4
 def main():
     dev = torch.device("cuda", 0)
     quick = "--quick" in sys.argv
-    shapes = [(129, 257, 33)] if quick else [(129, 257, 33), (257, 1031, 513)]
-    names = list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3"]
+    shapes = [(129, 257, 33), (129, 300, 520)] if quick else [(129, 257, 33), (257, 1031, 513)]
+    names = list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3", "parallel_fp16x3"]
     for (M, N, K) in shapes:
         A = synth.matrix(M, K, 5, 0)
         B = synth.matrix(K, N, 5, 1)
         ref, ab = oracle.mm_f64(A, B), oracle.absprod_np(A, B)
         for v in names:
-            sched, tf = ("parallel", True) if v == "parallel_tf32x3" else (v, False)
+            sched, tf = ("parallel", True) if v.startswith("parallel_") else (v, False)
             term = schedules.apply_padded(sched, M, N, K).term
-            C = interp.run_tensor(term, torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), tf32x3=tf)
+            C = interp.run_tensor(term, torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), tf32x3=tf,
+                                  tc_encoding="fp16" if v == "parallel_fp16x3" else "tf32")
             torch.cuda.synchronize()
             ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
             print(f"{v:16s} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
@@ -42,7 +43,7 @@ def main():
     B = torch.from_numpy(synth.matrix(K, N, 6, 1)).pin_memory()
     for v in ("parallel", "parallel_tf32x3", "loopPerm"):
         sched, tf = ("parallel", True) if v == "parallel_tf32x3" else (v, False)
-        p = interp.plan(schedules.apply_padded(sched, M, N, K).term, [(M, K), (K, N)], tf)
+        p = interp.plan(schedules.apply_padded(sched, M, N, K).term, [(M, K), (K, N)], tf, "tf32")
         out = torch.empty((M, N), pin_memory=True)
         interp.HostPipeline(p, dev)(A, B, out)
         ok, worst = oracle.check(out.numpy(), oracle.mm_f64(A.numpy(), B.numpy()),
