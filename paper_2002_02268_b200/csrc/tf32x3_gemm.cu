@@ -411,7 +411,9 @@ template <int BKT, bool F16 = false> struct PairCfg {
   static constexpr int A_TILE = P_BM * ROW_BYTES;           // 8 / 16 KB
   static constexpr int B_TILE = (P_BN / 2) * ROW_BYTES;     // this CTA's half of Bt
   static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
+  // epilogue staging for TMA stores of C: one 32 x 32 fp32 tile (4 KB) per epilogue warp
+  static constexpr int EPI_BYTES = 8 * 32 * 32 * 4;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 256 + 1024;
   static constexpr int KSUB = BKT / (F16 ? 16 : 8);         // MMAs per product per stage
   // idesc: D f32; A/B type tf32 (2) or f16 (0); K-major both; N, M
   static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
@@ -472,10 +474,11 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BKT, bool F16>
+template <int BKT, bool F16, bool TMA_C>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+               const __grid_constant__ CUtensorMap map_c,
                float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
                unsigned int* __restrict__ wave_ctr, const float* __restrict__ inv_s,
                const float* __restrict__ inv_t) {
@@ -487,7 +490,8 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   constexpr uint32_t kIdescPair = Cfg::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint8_t* epi_stage = smem + P_STAGES * P_STAGE_BYTES;      // 1 KB-aligned (stages are)
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + Cfg::EPI_BYTES);
   uint64_t* empty = full + P_STAGES;
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 1;
@@ -506,6 +510,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_ahi); tma_prefetch_desc(&map_alo);
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
+    if (TMA_C) tma_prefetch_desc(&map_c);
     for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(&tfull[0], 1);
     mbar_init(&tempty[0], 2 * P_EPI_WARPS);         // epilogue warps of both CTAs (leader's copy)
@@ -666,7 +671,27 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
 #pragma unroll
           for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
         }
-        if (row < M && col < N) {
+        if (TMA_C) {
+          // 32 x 32 chunk -> this warp's SMEM tile in the 128B-swizzled layout
+          // the tensor map expects -> one bulk tensor store (clipped at M, N)
+          uint8_t* tile = epi_stage + (warp - 2) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(tile + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&map_c)),
+                "r"(col), "r"(row - lane), "r"(smem_u32(tile))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -688,6 +713,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     for (int i = 0; i < 8; ++i) if (prof[i]) atomicAdd(&g_k7_prof[blockIdx.x][i], prof[i]);
 #endif
 
+  if (TMA_C && warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();
@@ -889,6 +915,13 @@ static int tile_group(int dflt) {
   return v > 0 ? v : dflt;
 }
 
+// ELV_TMA_STORE_C=0 selects the register-store epilogue (A/B measurements)
+static bool c_store_tma() {
+  static int v = -2;
+  if (v == -2) v = env_int("ELV_TMA_STORE_C", 1);
+  return v != 0;
+}
+
 template <int BKT, bool F16 = false>
 static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C, int M,
                        int N, int K, int Kp, int ldc, int dev, cudaStream_t st, const float* inv_s = nullptr,
@@ -900,19 +933,32 @@ static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, con
   if (!rc) rc = make_map(&mb_hi, b_hi, N, Kp, P_BN / 2, BKT, F16);
   if (!rc) rc = make_map(&mb_lo, b_lo, N, Kp, P_BN / 2, BKT, F16);
   if (rc) return rc;
-  static int attr_dev = -1;
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(k7_tf32x3_pair<BKT, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
+  // C through TMA bulk stores when it can be described by a tensor map
+  // (16 B-aligned base and pitch); otherwise the register-store epilogue
+  CUtensorMap mc{};
+  bool tma_c = c_store_tma() && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && (ldc & 3) == 0;
+  if (tma_c) {
+    EncodeTiledFn enc = get_encode();
+    const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldc * 4};
+    const cuuint32_t box[2] = {32, 32}, estr[2] = {1, 1};
+    tma_c = enc && enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  auto kern = tma_c ? k7_tf32x3_pair<BKT, F16, true> : k7_tf32x3_pair<BKT, F16, false>;
+  static int attr_dev[2] = {-1, -1};
+  if (attr_dev[tma_c] != dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 pair smem attribute: %s", cudaGetErrorString(e));
-    attr_dev = dev;
+    attr_dev[tma_c] = dev;
   }
   const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
   unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;   // one wave: nothing to sync
-  cudaError_t e = launch_pdl(k7_tf32x3_pair<BKT, F16>, dim3(2 * clusters), dim3(P_NUM_THREADS),
-                             (size_t)Cfg::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, C, M, N, ldc, Kp / BKT,
+  cudaError_t e = launch_pdl(kern, dim3(2 * clusters), dim3(P_NUM_THREADS),
+                             (size_t)Cfg::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, mc, C, M, N, ldc, Kp / BKT,
                              F16 ? 0 : with_lolo(K), tile_group(8), ctr, inv_s, inv_t);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3_pair");

@@ -30,18 +30,20 @@ def main():
     dev = torch.device("cuda", 0)
     A = torch.empty((M, K), device=dev); B = torch.empty((K, N), device=dev)
     synth.fill_device(A, 0, 0); synth.fill_device(B, 0, 1)
-    ap = torch.empty(lib.elv_tf32x3_a_planes_bytes(M, K), dtype=torch.uint8, device=dev)
-    bp = torch.empty(lib.elv_tf32x3_b_planes_bytes(N, K), dtype=torch.uint8, device=dev)
+    f16 = os.environ.get("ENC", "fp16") == "fp16"
+    pre = "elv_fp16x3_" if f16 else "elv_tf32x3_"
+    ap = torch.empty(getattr(lib, pre + "a_planes_bytes")(M, K), dtype=torch.uint8, device=dev)
+    bp = torch.empty(getattr(lib, pre + "b_planes_bytes")(N, K), dtype=torch.uint8, device=dev)
     C = torch.empty((M, N), device=dev)
     st = torch.cuda.current_stream().cuda_stream
-    _lib.check(lib.elv_tf32x3_split_a(A.data_ptr(), M, K, K, ap.data_ptr(), st), "a")
-    _lib.check(lib.elv_tf32x3_split_b(B.data_ptr(), K, N, N, bp.data_ptr(), st), "b")
+    _lib.check(getattr(lib, pre + "split_a")(A.data_ptr(), M, K, K, ap.data_ptr(), st), "a")
+    _lib.check(getattr(lib, pre + "split_b")(B.data_ptr(), K, N, N, bp.data_ptr(), st), "b")
     host = np.zeros((512, 8), np.uint64)
     for rep in range(3):
         lib.elv_debug_k7_prof(host.ctypes.data, 1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(lib.elv_tf32x3_gemm_planes(ap.data_ptr(), bp.data_ptr(), C.data_ptr(), M, N, K, N, st), "g")
+        _lib.check(getattr(lib, pre + "gemm_planes")(ap.data_ptr(), bp.data_ptr(), C.data_ptr(), M, N, K, N, st), "g")
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         lib.elv_debug_k7_prof(host.ctypes.data, 0)
