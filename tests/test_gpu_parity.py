@@ -368,3 +368,25 @@ def test_fp16x3_scaled_and_special_rows(cuda):
     ref = interp.run_tensor(small, A2, B2, tf32x3=True)                  # variant 7
     got = interp.run_tensor(small, A2, B2, tf32x3=True, tc_encoding="fp16")
     assert torch.equal(got, ref)                                        # same kernel below the threshold
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "parallel_fp16x3"])
+def test_nan_and_inf_propagate_like_ieee(cuda, variant):
+    """Special values follow the interpreter's IEEE arithmetic row/column-wise:
+    a NaN in A row r makes all of C row r NaN; +inf in B column c (with a
+    nonzero A row) makes that column non-finite; every other element is
+    unaffected and within the bound."""
+    name, tf = _sched(variant)
+    M, N, K = 512, 512, 1024
+    A, B = _device_inputs(M, N, K, 16, cuda)
+    A[3, 100] = float("nan")
+    B[200, 7] = float("inf")
+    term = schedules.apply(name, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=_enc(variant)).cpu().numpy()
+    assert np.isnan(C[3]).all()
+    assert not np.isfinite(C[:, 7]).any()
+    mask_r = np.ones(M, bool); mask_r[3] = False
+    mask_c = np.ones(N, bool); mask_c[7] = False
+    Ah, Bh = A.cpu().numpy()[mask_r], B.cpu().numpy()[:, mask_c]
+    ok, worst = oracle.check(C[mask_r][:, mask_c], oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
+    assert ok, worst
