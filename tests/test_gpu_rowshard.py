@@ -179,9 +179,11 @@ def test_c_abi_rowshard_single_process(cuda):
         lib.elv_nccl_destroy()
 
 
-def test_bench_two_ranks_sharing_one_gpu(cuda, tmp_path):
+@pytest.mark.parametrize("ranks,shape", [(2, ("2048", "2048", "1024")), (4, ("4096", "32768", "1024"))],
+                         ids=["2ranks", "4ranks-fp16"])
+def test_bench_ranks_sharing_one_gpu(cuda, tmp_path, ranks, shape):
     """bench.py's N>1 path (torchrun, PipelinedRowShardGemm, barriers,
-    max-over-ranks timing, rank-0 JSON line) with two ranks sharing cuda:0
+    max-over-ranks timing, rank-0 JSON line) with 2 and 4 ranks sharing cuda:0
     over gloo (ELV_BENCH_SHARE_GPU=1, test-only); NCCL itself needs one GPU
     per rank."""
     import json
@@ -189,17 +191,18 @@ def test_bench_two_ranks_sharing_one_gpu(cuda, tmp_path):
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, ELV_BENCH_SHARE_GPU="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    M, N, K = shape
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(ranks),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(repo, "bench.py"),
-           "--gpus", "2", "--M", "2048", "--N", "2048", "--K", "1024", "--steps", "3", "--warmup", "3",
+           "--gpus", str(ranks), "--M", M, "--N", N, "--K", K, "--steps", "3", "--warmup", "3",
            "--no-cpu-baseline"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=repo)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["parallelism"] == "rowshard2"
+    assert d["n_gpus"] == ranks and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"] == f"rowshard{ranks}"
 
 
 def test_host_pipeline_concurrent_callers(cuda):
