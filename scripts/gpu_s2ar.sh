@@ -15,3 +15,6 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "bench ref rc=$?" >> $S
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/launches_bench.log 2>&1; echo "launches rc=$?" >> $S
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_tf32x3_pair -s 1 -c 1 \
+  -o $OUT/prof_k8_bench python scripts/profile_one.py --variant parallel_fp16x3 --M 32768 --N 32768 --K 8192 --reps 2 \
+  > $OUT/prof_k8.log 2>&1; echo "ncu full rc=$?" >> $S
