@@ -130,7 +130,8 @@ size_t elv_gemm_host_workspace_bytes(int variant, int M, int N, int K);
 int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h,
                   int M, int N, int K, int lda, int ldb, int ldc,
                   void* workspace, size_t workspace_bytes, void* stream);
-/* The tile shape elv_gemm_host uses (rows x cols). */
+/* The tile shape elv_gemm_host uses (rows x cols); for the growing schedule
+ * (tensor-core variants, large outputs) the A strip rows and B strip columns. */
 int elv_gemm_host_tiles(int variant, int M, int N, int K, int* rows, int* cols);
 /* Pitched copy (cudaMemcpy2DAsync): kind 1 = host->device, 2 = device->host,
  * 3 = device->device.  Used by the multi-GPU end-to-end path to move column

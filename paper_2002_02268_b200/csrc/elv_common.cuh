@@ -79,10 +79,14 @@ int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
 int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t tf32x3_a_planes_bytes(int M, int K);
 size_t tf32x3_b_planes_bytes(int N, int K);
-int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st);
-int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st);
+// optional trailing arguments: the plane buffers hold `total` rows / columns
+// and the call covers [r0, r0 + M) / [c0, c0 + N) of them (0, 0: exactly these)
+int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st, int total = 0,
+                   int r0 = 0);
+int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st,
+                   int total = 0, int c0 = 0);
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st);
+                       cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0);
 int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st);
 // 3xFP16 encoding of the parallel schedule's tcgen05 kernel (tf32x3_gemm.cu)
 bool fp16x3_applicable(int M, int N, int K);
@@ -92,10 +96,12 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
 int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t fp16x3_a_planes_bytes(int M, int K);
 size_t fp16x3_b_planes_bytes(int N, int K);
-int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st);
-int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st);
+int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st, int total = 0,
+                   int r0 = 0);
+int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st, int total = 0,
+                   int c0 = 0);
 int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st);
+                       cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0);
 
 // binomial filter (stencil.cu)
 int launch_binomial(int variant, const float* img, float* out, int H, int W, int ldi, int ldo,

@@ -16,6 +16,7 @@
 #include "elv_common.cuh"
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <mutex>
@@ -30,6 +31,13 @@ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 struct HostPlan {
   int R, Nc, nrb, ncb;
+  // growing schedule (tensor-core variants, large C): A arrives in R-row
+  // strips and B in Nc-column strips; each landed strip is multiplied against
+  // everything of the other operand already resident (one GEMM, one D2H), so
+  // the resident rectangle grows from the corner and the D2H stream starts
+  // after a few MB instead of a whole B chunk.  Operand planes are prepared
+  // strip by strip into full-size buffers, so one GEMM reads across strips.
+  bool grow;
   bool packed_a;                 // variant 6: pack A per row block (cp.async kernel)
   size_t off_a, off_b, off_c, off_pa, stride_pa, off_pb, stride_pb, total;
 };
@@ -46,13 +54,34 @@ struct HostPlan {
 HostPlan make_plan(int v, int M, int N, int K) {
   HostPlan p{};
   const double bytes = 4.0 * ((double)M * K + (double)K * N + (double)M * N);
+  const bool tc = v == ELV_PARALLEL_TF32X3 || v == ELV_PARALLEL_FP16X3;
   p.R = M;
   p.Nc = N;
-  if (bytes >= (double)(64 << 20)) {
+  // Growing schedule for the tensor-core variants once C is large: 1024-row
+  // A strips and 4096-column B strips.  Measured (scripts/host_plan_sweep.py,
+  // profiles/r1/host_plan_sweep.jsonl, 3xFP16): 32768^2 x 8192 91-93 ms vs
+  // 94 ms for the grid, 16384^2 x 8192 29.6 vs 31.3 ms.  Narrower B strips
+  // start the D2H sooner but their C blocks are tall, narrow copies (8 KB
+  // rows over up to 4 GB of host addresses), which PCIe moves at ~34 GB/s
+  // instead of ~45-55 (the trace in profiles/r1/host_pipeline_trace_grow.json).
+  p.grow = tc && bytes >= (double)(64 << 20) && (M >= 16384 || N >= 16384);
+  if (const char* g = getenv("ELV_HOST_PLAN")) {
+    if (!strcmp(g, "grid")) p.grow = false;
+    else if (!strcmp(g, "grow")) p.grow = tc;
+  }
+  if (p.grow) {
+    p.R = 1024;
+    p.Nc = 4096;
+    if (const char* t = getenv("ELV_HOST_STRIPS")) {      // test hook: "R,Nc"
+      int r = 0, c = 0;
+      if (sscanf(t, "%d,%d", &r, &c) == 2 && r > 0 && c > 0) { p.R = r; p.Nc = c; }
+    }
+    if (p.R > M) p.R = M;
+    if (p.Nc > N) p.Nc = N;
+  } else if (bytes >= (double)(64 << 20)) {
     // 3xTF32 is PCIe-bound (GEMM ~ D2H time): finer row blocks start the D2H
     // stream sooner.  The SIMT variants are GEMM-bound (~4.6x the PCIe time):
     // 8 row blocks keep each launch at >= 6 waves of 128x256 tiles.
-    const bool tc = v == ELV_PARALLEL_TF32X3 || v == ELV_PARALLEL_FP16X3;
     const int fine = tc ? 16 : 8;
     const int row_blocks = M >= 8192 ? fine : (M >= 2048 ? 8 : (M >= 512 ? 2 : 1));
     p.R = (int)up((size_t)ceil_div(M, row_blocks), 256);
@@ -70,6 +99,7 @@ HostPlan make_plan(int v, int M, int N, int K) {
   if (const char* t = getenv("ELV_HOST_TILES")) {
     int r = 0, c = 0;
     if (sscanf(t, "%d,%d", &r, &c) == 2 && r > 0 && c > 0) {
+      p.grow = false;
       p.R = r < M ? r : M;
       p.Nc = c < N ? c : N;
     }
@@ -82,6 +112,14 @@ HostPlan make_plan(int v, int M, int N, int K) {
   p.off_b = o;  o = up(o + (size_t)K * N * 4, kAlign);
   p.off_c = o;  o = up(o + (size_t)M * N * 4, kAlign);
   p.stride_pa = 0;
+  if (p.grow) {          // full-size plane buffers, filled strip by strip
+    const size_t pa = v == ELV_PARALLEL_TF32X3 ? tf32x3_a_planes_bytes(M, K) : fp16x3_a_planes_bytes(M, K);
+    const size_t pb = v == ELV_PARALLEL_TF32X3 ? tf32x3_b_planes_bytes(N, K) : fp16x3_b_planes_bytes(N, K);
+    p.off_pa = o;  o = up(o + pa, kAlign);
+    p.off_pb = o;  o = up(o + pb, kAlign);
+    p.total = o + kAlign;
+    return p;
+  }
   if (v == ELV_PARALLEL_TF32X3) p.stride_pa = up(tf32x3_a_planes_bytes(p.R, K), kAlign);
   else if (v == ELV_PARALLEL_FP16X3) p.stride_pa = up(fp16x3_a_planes_bytes(p.R, K), kAlign);
   else if (p.packed_a) p.stride_pa = up(pack_a_bytes(p.R, K), kAlign);
@@ -192,7 +230,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   if (nd < 1) nd = 1;
   if (nd > 4) nd = 4;
   cudaStream_t d2hs[4] = {r.d2h, r.d2h_extra[0], r.d2h_extra[1], r.d2h_extra[2]};
-  const int ntiles = p.nrb * p.ncb;
+  const int ntiles = p.grow ? p.nrb + p.ncb : p.nrb * p.ncb;
   // events: [0] entry, [1] h2d done, [2 .. 2+nrb) A blocks, [.. +ncb) B chunks, [.. +ntiles) tiles
   int rc = get_events(r, 2 + p.nrb + p.ncb + ntiles);
   if (rc) return rc;
@@ -230,6 +268,83 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   if ((rc = trace_rec(-1, st))) return rc;
   CK(cudaStreamWaitEvent(r.h2d, ev_entry, 0), "h2d wait entry");
   for (int q = 0; q < nd; ++q) CK(cudaStreamWaitEvent(d2hs[q], ev_entry, 0), "d2h wait entry");
+
+  if (p.grow) {
+    // H2D: B strip 0, then always the operand with less resident (rows vs
+    // columns: both K*4 bytes each), so the resident rectangle stays square
+    struct Strip { bool is_b; int idx; };
+    std::vector<Strip> order;
+    {
+      int na = 0, nb = 0;
+      long long la = 0, lb = 0;
+      while (na < p.nrb || nb < p.ncb) {
+        const bool take_b = nb < p.ncb && (na == p.nrb || lb <= la);
+        if (take_b) { order.push_back({true, nb}); lb += std::min(p.Nc, N - nb * p.Nc); ++nb; }
+        else { order.push_back({false, na}); la += std::min(p.R, M - na * p.R); ++na; }
+      }
+    }
+    cudaEvent_t* ev_item = ev_a;            // one per strip, in H2D order
+    for (size_t k = 0; k < order.size(); ++k) {
+      const Strip& it = order[k];
+      if (it.is_b) {
+        const int c0 = it.idx * p.Nc, nc = std::min(p.Nc, N - c0);
+        CK(cudaMemcpy2DAsync(B_d + c0, (size_t)N * 4, B_h + c0, (size_t)ldb * 4, (size_t)nc * 4, K,
+                             cudaMemcpyHostToDevice, r.h2d), "H2D B strip");
+      } else {
+        const int r0 = it.idx * p.R, nr = std::min(p.R, M - r0);
+        CK(cudaMemcpy2DAsync(A_d + (size_t)r0 * K, (size_t)K * 4, A_h + (size_t)r0 * lda, (size_t)lda * 4,
+                             (size_t)K * 4, nr, cudaMemcpyHostToDevice, r.h2d), "H2D A strip");
+      }
+      CK(cudaEventRecord(ev_item[k], r.h2d), "record strip");
+      if ((rc = trace_rec(0, r.h2d))) return rc;
+    }
+    // prepare each strip as it lands, then one GEMM: the strip against the
+    // other operand's resident prefix; D2H that block of C
+    const bool f16 = variant == ELV_PARALLEL_FP16X3;
+    int d2h_rows = 1 << 30;           // rows per D2H copy (tuning hook)
+    if (const char* e = getenv("ELV_HOST_D2H_ROWS")) d2h_rows = std::max(1, atoi(e));
+    void* pa = prep_a(0);
+    void* pb = prep_b(0);
+    int rows_in = 0, cols_in = 0;
+    for (size_t k = 0; k < order.size(); ++k) {
+      const Strip& it = order[k];
+      CK(cudaStreamWaitEvent(st, ev_item[k], 0), "wait strip");
+      int r0, nr, c0, nc;
+      if (it.is_b) {
+        c0 = it.idx * p.Nc; nc = std::min(p.Nc, N - c0);
+        rc = f16 ? fp16x3_split_b(B_d + c0, K, nc, N, pb, st, N, c0)
+                 : tf32x3_split_b(B_d + c0, K, nc, N, false, pb, st, N, c0);
+        if (rc) return rc;
+        cols_in += nc;
+        r0 = 0; nr = rows_in;
+      } else {
+        r0 = it.idx * p.R; nr = std::min(p.R, M - r0);
+        rc = f16 ? fp16x3_split_a(A_d + (size_t)r0 * K, nr, K, K, pa, st, M, r0)
+                 : tf32x3_split_a(A_d + (size_t)r0 * K, nr, K, K, pa, st, M, r0);
+        if (rc) return rc;
+        rows_in += nr;
+        c0 = 0; nc = cols_in;
+      }
+      if (nr == 0 || nc == 0) continue;       // the first strip: nothing to multiply yet
+      float* Cb = C_d + (size_t)r0 * N + c0;
+      rc = f16 ? fp16x3_gemm_planes(pa, pb, Cb, nr, nc, K, N, st, M, r0, N, c0)
+               : tf32x3_gemm_planes(pa, pb, Cb, nr, nc, K, N, st, M, r0, N, c0);
+      if (rc) return rc;
+      CK(cudaEventRecord(ev_t[k], st), "record block");
+      if ((rc = trace_rec(1, st))) return rc;
+      CK(cudaStreamWaitEvent(r.d2h, ev_t[k], 0), "d2h wait block");
+      for (int a0 = 0; a0 < nr; a0 += d2h_rows) {
+        const int h = std::min(d2h_rows, nr - a0);
+        CK(cudaMemcpy2DAsync(C_h + (size_t)(r0 + a0) * ldc + c0, (size_t)ldc * 4, C_d + (size_t)(r0 + a0) * N + c0,
+                             (size_t)N * 4, (size_t)nc * 4, h, cudaMemcpyDeviceToHost, r.d2h), "D2H C block");
+      }
+      if ((rc = trace_rec(2, r.d2h))) return rc;
+    }
+    CK(cudaEventRecord(ev_end, r.d2h), "record end");
+    if (trace) r.tkind.resize(ntr);
+    CK(cudaStreamWaitEvent(st, ev_end, 0), "join d2h");
+    return ELV_OK;
+  }
 
   // H2D order: start with B chunk 0 and A block 0, then repeatedly bring
   // whichever operand enables more new C tiles per byte (an A block enables

@@ -987,10 +987,14 @@ static void split_a_grid(int M, int Kp, int* gx, int* gy) {
   *gy = y;
 }
 
-int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st) {
+// Plane buffers hold `total` rows (0: just these M); the split writes rows
+// [r0, r0 + M) of them, so strips prepared one by one form one operand that a
+// later GEMM can read across strips (the host pipeline's growing schedule).
+int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st, int total, int r0) {
   const int Kp = (int)kpad(K);
-  float* hi = align128(a_planes);
-  float* lo = hi + (size_t)M * Kp;
+  if (total <= 0) total = M;
+  float* hi = align128(a_planes) + (size_t)r0 * Kp;
+  float* lo = hi + (size_t)total * Kp;
   int gx, gy;
   split_a_grid(M, Kp, &gx, &gy);
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
@@ -998,10 +1002,12 @@ int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaSt
   return check_launch("tf32x3_split_a");
 }
 
-int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st) {
+int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st, int total,
+                   int c0) {
   const int Kp = (int)kpad(K);
-  float* hi = align128(b_planes);
-  float* lo = hi + (size_t)N * Kp;
+  if (total <= 0) total = N;
+  float* hi = align128(b_planes) + (size_t)c0 * Kp;
+  float* lo = hi + (size_t)total * Kp;
   dim3 grid((N + 31) / 32, (Kp + 31) / 32);
   if (packed) k_split_transpose_b<true><<<grid, 256, 0, st>>>(B, hi, lo, K, N, 0, Kp);
   else k_split_transpose_b<false><<<grid, 256, 0, st>>>(B, hi, lo, K, N, ldb, Kp);
@@ -1073,12 +1079,14 @@ static int one_cta_bk(int bn) {
 }
 
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st) {
+                       cudaStream_t st, int a_total, int r0, int b_total, int c0) {
   const int Kp = (int)kpad(K);
-  const float* a_hi = align128(a_planes);
-  const float* a_lo = a_hi + (size_t)M * Kp;
-  const float* b_hi = align128(b_planes);
-  const float* b_lo = b_hi + (size_t)N * Kp;
+  if (a_total <= 0) a_total = M;
+  if (b_total <= 0) b_total = N;
+  const float* a_hi = align128(a_planes) + (size_t)r0 * Kp;
+  const float* a_lo = a_hi + (size_t)a_total * Kp;
+  const float* b_hi = align128(b_planes) + (size_t)c0 * Kp;
+  const float* b_lo = b_hi + (size_t)b_total * Kp;
   int dev = 0;
   cudaGetDevice(&dev);
   const int pm = pair_mode(M, N);
@@ -1276,15 +1284,22 @@ static Planes16 planes16(const void* buf, int rows, int K) {
           reinterpret_cast<float*>(b + 2 * plane), reinterpret_cast<float*>(b + 2 * plane + vec)};
 }
 
-int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st) {
-  const Planes16 P = planes16(a_planes, M, K);
+// rows [r0, r0 + n) of plane buffers that hold `total` rows (see tf32x3_split_a)
+static Planes16 planes16_at(const void* buf, int n, int K, int total, int r0) {
+  Planes16 P = planes16(buf, total > 0 ? total : n, K);
+  const size_t off = (size_t)r0 * kpad16(K);
+  return {P.hi + off, P.lo + off, P.s + r0, P.inv + r0};
+}
+
+int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st, int total, int r0) {
+  const Planes16 P = planes16_at(a_planes, M, K, total, r0);
   const int Kp = (int)kpad16(K);
   k16_split_a_rows<<<M, 256, 0, st>>>(A, M, K, lda, Kp, P.s, P.inv, P.hi, P.lo);
   return check_launch("fp16x3_split_a");
 }
 
-int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st) {
-  const Planes16 P = planes16(b_planes, N, K);
+int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st, int total, int c0) {
+  const Planes16 P = planes16_at(b_planes, N, K, total, c0);
   const int Kp = (int)kpad16(K);
   unsigned int* tmax = reinterpret_cast<unsigned int*>(P.s);
   if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
@@ -1295,10 +1310,10 @@ int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaSt
 }
 
 int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st) {
+                       cudaStream_t st, int a_total, int r0, int b_total, int c0) {
   if (!fp16x3_applicable(M, N, K))
     return set_error(ELV_EINVAL, "fp16x3: needs K >= 512 (got %dx%dx%d)", M, N, K);
-  const Planes16 A = planes16(a_planes, M, K), B = planes16(b_planes, N, K);
+  const Planes16 A = planes16_at(a_planes, M, K, a_total, r0), B = planes16_at(b_planes, N, K, b_total, c0);
   const int Kp = (int)kpad16(K);
   int dev = 0;
   cudaGetDevice(&dev);

@@ -18,7 +18,8 @@ def main():
     M, N, K = 32768, 32768, 8192
     tf = "--simt" not in sys.argv
     dev = torch.device("cuda", 0)
-    p = dispatch.decode(schedules.apply("parallel", M, N, K).term, [(M, K), (K, N)], tf32x3=tf)
+    p = dispatch.decode(schedules.apply("parallel", M, N, K).term, [(M, K), (K, N)], tf32x3=tf,
+                        tc_encoding=os.environ.get("ENC", "fp16"))
     A = torch.empty((M, K), pin_memory=True); B = torch.empty((K, N), pin_memory=True)
     Ad = torch.empty((M, K), device=dev); synth.fill_device(Ad, 0, 0); A.copy_(Ad); del Ad
     Bd = torch.empty((K, N), device=dev); synth.fill_device(Bd, 0, 1); B.copy_(Bd); del Bd

@@ -6,15 +6,18 @@ first chunks start the D2H stream sooner but copy shorter rows).
 """
 import ctypes
 import json
+import os
+import sys
 
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2002_02268_b200 import _lib
 
 
 def main():
     dev = torch.device("cuda", 0)
-    lib = _lib.lib()
+    lib = _lib.load()
     pitch = 32768 * 4                     # a 32768-column fp32 matrix
     rows = 8192
     h = torch.empty(rows * 32768, pin_memory=True)

@@ -127,12 +127,13 @@ def test_host_pipeline_bitwise_equals_device_path(cuda, variant, tiles, monkeypa
     I._host_pipes.clear()
 
 
-def test_host_pipeline_large_default_tiling(cuda):
+def test_host_pipeline_large_default_tiling(cuda, monkeypatch):
     """The default tiling at a bench-like shape (8 row blocks; N < 32768, so
     one column chunk) and repeated calls reusing the cached workspace: row samples
     against the f64 oracle, and call 2 == call 1."""
     from paper_2002_02268_b200 import interp as I
     M, N, K = 4096, 16384, 1024
+    monkeypatch.setenv("ELV_HOST_PLAN", "grid")     # N >= 16384 would take the growing schedule
     I._host_pipes.clear()
     term = schedules.apply("parallel", M, N, K).term
     A = torch.from_numpy(synth.matrix(M, K, 9, 0)).pin_memory()
@@ -148,6 +149,7 @@ def test_host_pipeline_large_default_tiling(cuda):
     An, Bn = A.numpy(), B.numpy()
     ok, worst = oracle.check(C1.numpy()[rows], oracle.mm_f64(An[rows], Bn), oracle.absprod_np(An[rows], Bn), K)
     assert ok, worst
+    I._host_pipes.clear()
 
 
 def test_c_abi_rowshard_single_process(cuda):
@@ -318,4 +320,55 @@ def test_fp16x3_pipelined_and_host_paths_bitwise(cuda, monkeypatch):
     out = torch.empty((M, N), pin_memory=True)
     hp(A.cpu().pin_memory(), B.cpu().pin_memory(), out)
     assert torch.equal(out, direct.cpu())
+    I._host_pipes.clear()
+
+
+@pytest.mark.parametrize("enc", ["tf32", "fp16"])
+@pytest.mark.parametrize("strips", [None, "384,1280", "256,8192"])
+def test_host_pipeline_growing_schedule_bitwise(cuda, enc, strips, monkeypatch):
+    """The growing schedule (strips of A and B prepared into full-size plane
+    buffers, each landed strip multiplied against the other operand's resident
+    prefix) returns exactly the single-launch result: default strips, ragged
+    strips, and strips wider than the matrix."""
+    from paper_2002_02268_b200 import interp as I
+    M, N, K = 3000, 5000, 640
+    p = dispatch.decode(schedules.apply_padded("parallel", M, N, K).term, [(M, K), (K, N)], tf32x3=True,
+                        tc_encoding=enc)
+    monkeypatch.setenv("ELV_HOST_PLAN", "grow")
+    if strips:
+        monkeypatch.setenv("ELV_HOST_STRIPS", strips)
+    I._host_pipes.clear()
+    hp = I.HostPipeline(p, cuda)
+    if strips:
+        r, c = map(int, strips.split(","))
+        assert hp.tile == (min(r, M), min(c, N))
+    A = torch.empty((M, K), device=cuda); synth.fill_device(A, 11, 0)
+    B = torch.empty((K, N), device=cuda); synth.fill_device(B, 11, 1)
+    direct = I.gemm(p, A, B).cpu()
+    out = torch.full((M, N), float("nan")).pin_memory()
+    for _ in range(2):                      # the second call reuses the workspace
+        hp(A.cpu().pin_memory(), B.cpu().pin_memory(), out)
+        assert torch.equal(out, direct)
+    I._host_pipes.clear()
+
+
+def test_host_pipeline_grows_at_bench_scale(cuda):
+    """Large outputs take the growing schedule by default (1024-row and
+    4096-column strips) and match the f64 oracle on sampled rows."""
+    from paper_2002_02268_b200 import interp as I
+    M, N, K = 16384, 16384, 1024
+    p = _plan16(M, N, K)
+    I._host_pipes.clear()
+    hp = I.HostPipeline(p, cuda)
+    assert hp.tile == (1024, 4096)
+    A = torch.empty((M, K), device=cuda); synth.fill_device(A, 12, 0)
+    B = torch.empty((K, N), device=cuda); synth.fill_device(B, 12, 1)
+    out = torch.empty((M, N), pin_memory=True)
+    hp(A.cpu().pin_memory(), B.cpu().pin_memory(), out)
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    rows = np.array([0, 1023, 1024, 8191, 16383])
+    ref = oracle.mm_f64(Ah[rows], Bh)
+    ok, worst = oracle.check(out.numpy()[rows], ref, oracle.absprod_np(Ah[rows], Bh), K)
+    assert ok, worst
+    assert torch.equal(out, I.gemm(p, A, B).cpu())
     I._host_pipes.clear()
