@@ -1198,8 +1198,12 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
     const long long tiles = (long long)((M + SM_BM - 1) / SM_BM) * ((N + SM_BN - 1) / SM_BN);
     long long grid = (long long)num_sms() * 4;
     if (grid > tiles) grid = tiles;
-    cudaError_t e = launch_pdl(k6_sgemm_small, dim3((unsigned)grid), dim3(64), (size_t)SM_SMEM, st, packedA, packedB,
-                               C, M, N, K, ldc);
+    // no PDL here: with back-to-back calls at 1024^3 the early-resident
+    // GEMM CTAs cost 92 vs 55 us per call (scripts/small_timing.py, ELV_PDL)
+    static int pdl = -1;
+    if (pdl < 0) pdl = getenv("ELV_K6_SMALL_PDL") ? atoi(getenv("ELV_K6_SMALL_PDL")) != 0 : 0;
+    cudaError_t e = launch_pdl_if(pdl != 0, k6_sgemm_small, dim3((unsigned)grid), dim3(64), (size_t)SM_SMEM, st,
+                                  packedA, packedB, C, M, N, K, ldc);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_small: %s", cudaGetErrorString(e));
     return check_launch("gemm_parallel_small");
   }
