@@ -1145,8 +1145,29 @@ int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStr
 // the packed-A cp.async kernel serves the large-problem regime of the
 // parallel schedule (the same regime as the 8x16 kernel); ELV_SGEMM_CP=0
 // falls back to the raw-A kernels for tuning comparisons.
+// tuning hook: ELV_K6_PATH=1 small 64x64 kernel, 2 cp.async 128x256 kernel
+// (packed A), 3 the unpacked 128x128 kernel; unset = by problem size
+static int k6_path_forced() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("ELV_K6_PATH");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+// The 128x256 cp.async kernel runs whole waves of one tile per SM; where its
+// last wave would be <95 % full, the 64x64-tile kernel (4 resident per SM,
+// 16x finer tiles) wins.  Measured (profiles/r1/small/k6_paths.jsonl, TF):
+// 2048^3 48.7 vs 39.7 (old 128x128 mid kernel), 4096^3 57.2 vs 51.2,
+// 5120^3 57.1 vs 53.6; cp ahead at 3072^3 (57.1 vs 55.6), 6144^3 (58.1 vs
+// 56.7), 8192^3 (59.2 vs 57.8), 4096x8192x2048 (58.6 vs 57.2).
 static bool parallel_small(int M, int N) {
-  return (long long)((M + 127) / 128) * ((N + 127) / 128) < num_sms();
+  const int f = k6_path_forced();
+  if (f != 0) return f == 1;
+  const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
+  const long long sms = num_sms();
+  const long long waves = (tiles + sms - 1) / sms;
+  return tiles < 0.95 * (double)(waves * sms);
 }
 
 bool parallel_uses_packed_a(int M, int N) {
@@ -1156,8 +1177,11 @@ bool parallel_uses_packed_a(int M, int N) {
     enabled = e ? (atoi(e) != 0) : 1;
   }
   if (!enabled) return false;
-  const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
-  return tiles >= 2LL * num_sms() || parallel_small(M, N);
+  const int f = k6_path_forced();
+  if (f != 0) return f == 1 || f == 2;
+  (void)M;
+  (void)N;
+  return true;            // both the small and the cp.async kernel read packed A
 }
 
 size_t pack_a_bytes(int M, int K) { return (size_t)((M + 127) / 128) * 128 * (size_t)K * sizeof(float); }

@@ -1,11 +1,5 @@
 #!/bin/bash
-OUT=gpurun_out/${1:-s2bl}
+OUT=gpurun_out/${1:-s2bo}
 mkdir -p $OUT
-for f in 0 1; do
-  ELV_K6_SMALL_PDL=$f timeout 300 python scripts/small_timing.py 1024 1024 1024 | sed "s/^{/{\"k6_small_pdl\": $f, /" >> $OUT/small.jsonl 2>> $OUT/small.err
-done
-for pdl in 1 0; do
-  for n in 2048 4096 8192; do
-    ELV_PDL=$pdl timeout 300 python scripts/small_timing.py $n $n $n | sed "s/^{/{\"pdl\": $pdl, /" >> $OUT/small.jsonl 2>> $OUT/small.err
-  done
-done
+timeout 2400 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/summary.txt
+timeout 1200 python bench.py --workload ladder > $OUT/ladder.jsonl 2> $OUT/ladder.err; echo "ladder rc=$?" >> $OUT/summary.txt

@@ -19,6 +19,8 @@ def main():
     A = torch.empty((M, K), device=dev); synth.fill_device(A, 0, 0)
     B = torch.empty((K, N), device=dev); synth.fill_device(B, 0, 1)
     cases = [("parallel", False, "tf32"), ("parallel", True, "tf32"), ("parallel", True, "fp16")]
+    if os.environ.get("ONLY_SIMT"):
+        cases = cases[:1]
     for sched, tf, enc in cases:
         term = schedules.apply_padded(sched, M, N, K).term
         p = interp.plan(term, [(M, K), (K, N)], tf, enc)
