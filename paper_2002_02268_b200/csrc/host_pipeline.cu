@@ -232,7 +232,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
   cudaStream_t d2hs[4] = {r.d2h, r.d2h_extra[0], r.d2h_extra[1], r.d2h_extra[2]};
   const int ntiles = p.grow ? p.nrb + p.ncb : p.nrb * p.ncb;
   // events: [0] entry, [1] h2d done, [2 .. 2+nrb) A blocks, [.. +ncb) B chunks, [.. +ntiles) tiles
-  int rc = get_events(r, 2 + p.nrb + p.ncb + ntiles);
+  int rc = get_events(r, 2 + p.nrb + p.ncb + ntiles + (p.grow ? p.nrb + p.ncb : 0));
   if (rc) return rc;
   cudaEvent_t* ev = r.events.data();
   cudaEvent_t ev_entry = ev[0], ev_end = ev[1];
@@ -284,8 +284,25 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
       }
     }
     cudaEvent_t* ev_item = ev_a;            // one per strip, in H2D order
+    cudaEvent_t* ev_back = ev_t + ntiles;   // one per strip: its C block is back on the host
+    // Pacing (ELV_HOST_PACE=L): strip k's H2D waits until block k-L is back
+    // on the host, so the H2D stream runs at most L strips ahead of the D2H
+    // stream instead of taking PCIe bandwidth from it early on.
+    int pace = 0;
+    if (const char* e = getenv("ELV_HOST_PACE")) pace = std::max(0, atoi(e));
+    std::vector<int> last_back(order.size(), -1);   // latest block <= k with a D2H
+    // strips are enqueued in order on all three streams: H2D, then prepare +
+    // GEMM of the block it enables, then the D2H of that block
+    const bool f16 = variant == ELV_PARALLEL_FP16X3;
+    int d2h_rows = 1 << 30;           // rows per D2H copy (tuning hook)
+    if (const char* e = getenv("ELV_HOST_D2H_ROWS")) d2h_rows = std::max(1, atoi(e));
+    void* pa = prep_a(0);
+    void* pb = prep_b(0);
+    int rows_in = 0, cols_in = 0;
     for (size_t k = 0; k < order.size(); ++k) {
       const Strip& it = order[k];
+      if (pace > 0 && k >= (size_t)pace && last_back[k - pace] >= 0)
+        CK(cudaStreamWaitEvent(r.h2d, ev_back[last_back[k - pace]], 0), "h2d pace");
       if (it.is_b) {
         const int c0 = it.idx * p.Nc, nc = std::min(p.Nc, N - c0);
         CK(cudaMemcpy2DAsync(B_d + c0, (size_t)N * 4, B_h + c0, (size_t)ldb * 4, (size_t)nc * 4, K,
@@ -297,17 +314,9 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
       }
       CK(cudaEventRecord(ev_item[k], r.h2d), "record strip");
       if ((rc = trace_rec(0, r.h2d))) return rc;
-    }
-    // prepare each strip as it lands, then one GEMM: the strip against the
-    // other operand's resident prefix; D2H that block of C
-    const bool f16 = variant == ELV_PARALLEL_FP16X3;
-    int d2h_rows = 1 << 30;           // rows per D2H copy (tuning hook)
-    if (const char* e = getenv("ELV_HOST_D2H_ROWS")) d2h_rows = std::max(1, atoi(e));
-    void* pa = prep_a(0);
-    void* pb = prep_b(0);
-    int rows_in = 0, cols_in = 0;
-    for (size_t k = 0; k < order.size(); ++k) {
-      const Strip& it = order[k];
+
+      // prepare the strip as it lands, then one GEMM: the strip against the
+      // other operand's resident prefix; D2H that block of C
       CK(cudaStreamWaitEvent(st, ev_item[k], 0), "wait strip");
       int r0, nr, c0, nc;
       if (it.is_b) {
@@ -325,6 +334,7 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
         rows_in += nr;
         c0 = 0; nc = cols_in;
       }
+      last_back[k] = k > 0 ? last_back[k - 1] : -1;
       if (nr == 0 || nc == 0) continue;       // the first strip: nothing to multiply yet
       float* Cb = C_d + (size_t)r0 * N + c0;
       rc = f16 ? fp16x3_gemm_planes(pa, pb, Cb, nr, nc, K, N, st, M, r0, N, c0)
@@ -338,6 +348,8 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
         CK(cudaMemcpy2DAsync(C_h + (size_t)(r0 + a0) * ldc + c0, (size_t)ldc * 4, C_d + (size_t)(r0 + a0) * N + c0,
                              (size_t)N * 4, (size_t)nc * 4, h, cudaMemcpyDeviceToHost, r.d2h), "D2H C block");
       }
+      CK(cudaEventRecord(ev_back[k], r.d2h), "record block back");
+      last_back[k] = (int)k;
       if ((rc = trace_rec(2, r.d2h))) return rc;
     }
     CK(cudaEventRecord(ev_end, r.d2h), "record end");

@@ -49,7 +49,7 @@ def main():
             hp(A, B, C)
             best = min(best, time.perf_counter() - t0)
         print(json.dumps({"shape": [M, N, K], "enc": enc, "plan": plan, "tiles": hp.tile,
-                          "d2h_rows": os.environ.get("ELV_HOST_D2H_ROWS"), "ms": round(best * 1e3, 2),
+                          "d2h_rows": os.environ.get("ELV_HOST_D2H_ROWS"), "pace": os.environ.get("ELV_HOST_PACE"), "ms": round(best * 1e3, 2),
                           "TFLOP/s": round(2.0 * M * N * K / best / 1e12, 1)}), flush=True)
         del hp
 
