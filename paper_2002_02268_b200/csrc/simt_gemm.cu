@@ -692,8 +692,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int CP_BK = 16, CP_STAGES = 4;
-constexpr int CP_SMEM = CP_STAGES * CP_BK * (128 + 256) * 4;    // 96 KB
+// k-block depth x ring stages of the cp.async SIMT kernels: 32 x 3 (144 KB)
+// measured +1.5 % over 16 x 4 at the bench shape (60.4 -> 61.2 TF; one
+// barrier per 32 k instead of 16); 32 x 4 +0.7 %, 16 x 6 -1 %
+// (profiles/r1/small/k6_bk_stages.jsonl)
+#ifndef ELV_CP_BK
+#define ELV_CP_BK 32
+#endif
+#ifndef ELV_CP_STAGES
+#define ELV_CP_STAGES 3
+#endif
+constexpr int CP_BK = ELV_CP_BK, CP_STAGES = ELV_CP_STAGES;
+constexpr int CP_SMEM = CP_STAGES * CP_BK * (128 + 256) * 4;    // 144 KB at 32 x 3
 
 template <int ORDER>
 __global__ void __launch_bounds__(256, 1)
@@ -935,8 +945,16 @@ k6_sgemm_ffma2(const float* __restrict__ PA, const float* __restrict__ PB, float
 // FFMA2, so SMEM bandwidth is not the bound), the same packed operands and
 // 4-stage cp.async ring as k6_sgemm_cp.  A 64-row tile is one half of a
 // 128-row packedA panel.  Same sequential fmaf chain per element.
-constexpr int SM_BM = 64, SM_BN = 64, SM_BK = 16, SM_STAGES = 4;
-constexpr int SM_SMEM = SM_STAGES * SM_BK * (SM_BM + SM_BN) * 4;   // 32 KB
+// 32 x 3 (48 KB, 4 CTAs per SM): 1024^3 51.4 vs 55.3 us (16 x 4), +1 % at
+// 2048^3 / 4096^3 (profiles/r1/small/k6_small_bk_stages.jsonl)
+#ifndef ELV_SM_BK
+#define ELV_SM_BK 32
+#endif
+#ifndef ELV_SM_STAGES
+#define ELV_SM_STAGES 3
+#endif
+constexpr int SM_BM = 64, SM_BN = 64, SM_BK = ELV_SM_BK, SM_STAGES = ELV_SM_STAGES;
+constexpr int SM_SMEM = SM_STAGES * SM_BK * (SM_BM + SM_BN) * 4;   // 48 KB at 32 x 3
 
 __global__ void __launch_bounds__(64, 4)
 k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
