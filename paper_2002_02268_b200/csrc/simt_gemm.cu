@@ -677,7 +677,7 @@ k6_sgemm_8x16(const float* __restrict__ A, const float* __restrict__ P, float* _
 // K6 on packed operands (the default `parallel` path of elv_gemm): A is
 // packed by the prepass like B (packedA[M/128][K][128], the "packB" treatment
 // applied to the other operand), so every k-block of both tiles is a
-// contiguous run of 16-byte chunks.  The main loop is then a 4-stage
+// contiguous run of 16-byte chunks.  The main loop is then a multi-stage
 // cp.async (LDGSTS) pipeline with no register staging and no transposing
 // stores, and the registers that frees hold a second A/B fragment set so the
 // next k-step's LDS overlap the current 128 FFMAs.
@@ -943,7 +943,7 @@ k6_sgemm_ffma2(const float* __restrict__ PA, const float* __restrict__ PB, float
 // Small problems (fewer 128x256 tiles than SMs, e.g. 1024^3 -> 32): 64x64
 // tiles so every SM gets work, 64 threads x 8x8 outputs (4 LDS.128 per 32
 // FFMA2, so SMEM bandwidth is not the bound), the same packed operands and
-// 4-stage cp.async ring as k6_sgemm_cp.  A 64-row tile is one half of a
+// cp.async ring structure as k6_sgemm_cp.  A 64-row tile is one half of a
 // 128-row packedA panel.  Same sequential fmaf chain per element.
 // 32 x 3 (48 KB, 4 CTAs per SM): 1024^3 51.4 vs 55.3 us (16 x 4), +1 % at
 // 2048^3 / 4096^3 (profiles/r1/small/k6_small_bk_stages.jsonl)
