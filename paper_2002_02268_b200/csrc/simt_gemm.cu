@@ -226,6 +226,9 @@ __device__ __forceinline__ float4 load_b4_packed(const float* __restrict__ P, in
 // (xi outside ki: a thread's rows of A stay in registers while k sweeps,
 // yi vectorised in float4).
 // PACKED selects packedB panels (arrayPacking's toMem) over row-major B.
+#ifndef ELV_K34_FFMA2
+#define ELV_K34_FFMA2 1
+#endif
 template <bool PACKED>
 __global__ void __launch_bounds__(256)
 k34_outer4x4(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
@@ -238,11 +241,17 @@ k34_outer4x4(const float* __restrict__ A, const float* __restrict__ B, float* __
   const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
   const bool vecA = aligned16(A) && (lda & 3) == 0;
   const bool vecB = PACKED || (aligned16(B) && (ldb & 3) == 0);
+#if ELV_K34_FFMA2
+  unsigned long long acc2[4][2];                   // column pairs, FFMA2 (bitwise = fmaf)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc2[i][0] = acc2[i][1] = 0ull;
+#else
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#endif
 
   // A: 64 rows x 8 k = 128 float4 (threads 0..127); B: 8 x 64 = 128 float4 (threads 128..255)
   for (int k0 = 0; k0 < K; k0 += BK) {
@@ -264,15 +273,33 @@ k34_outer4x4(const float* __restrict__ A, const float* __restrict__ B, float* __
       const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
       const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
       const float av[4] = {a.x, a.y, a.z, a.w};
+#if ELV_K34_FFMA2
+      const unsigned long long b01 = pack2(b.x, b.y), b23 = pack2(b.z, b.w);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const unsigned long long ai = pack2(av[i], av[i]);
+        ffma2(acc2[i][0], ai, b01);
+        ffma2(acc2[i][1], ai, b23);
+      }
+#else
       const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+#endif
     }
     __syncthreads();
   }
   const bool vecC = aligned16(C) && (ldc & 3) == 0;
+#if ELV_K34_FFMA2
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 lo = unpack2(acc2[i][0]), hi = unpack2(acc2[i][1]);
+    acc[i][0] = lo.x; acc[i][1] = lo.y; acc[i][2] = hi.x; acc[i][3] = hi.y;
+  }
+#endif
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gi = row0 + ty * 4 + i, gj = col0 + tx * 4;
@@ -310,8 +337,14 @@ __device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
 
 // TBM = 128 (256 threads) or 64 (128 threads, small problems): the same
 // 8x8 register accumulators per thread, half the rows per CTA.
+#ifndef ELV_K56_FFMA2
+#define ELV_K56_FFMA2 1
+#endif
+#ifndef ELV_K56_MINB
+#define ELV_K56_MINB 2
+#endif
 template <bool PARALLEL, int TBM = G_BM>
-__global__ void __launch_bounds__(TBM * 2, 2)
+__global__ void __launch_bounds__(TBM * 2, ELV_K56_MINB)
 k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* __restrict__ C,
                int M, int N, int K, int lda, int ldc) {
   constexpr int NBUF = PARALLEL ? 2 : 1;
@@ -341,11 +374,19 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
   for (int t = first; t < num_tiles; t += stride) {
     TileCoord tc = PARALLEL ? tile_of(t, tiles_m, tiles_n) : TileCoord{(int)blockIdx.y, (int)blockIdx.x};
     const int row0 = tc.m * G_BM, col0 = tc.n * G_BN;
+#if ELV_K56_FFMA2
+    unsigned long long acc2[8][4];                 // column pairs, FFMA2 (bitwise = fmaf)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
+#else
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#endif
 
     struct VB { float4 v[BLD]; };
     auto ldA = [&](int k0) { return load_a4<G_BM, G_BK>(A, M, K, lda, vecA, row0 + a_r, k0 + a_k); };
@@ -380,11 +421,22 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
         const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol]);
         const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol + 16]);
         const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#if ELV_K56_FFMA2
+        const unsigned long long bp[4] = {pack2(b0.x, b0.y), pack2(b0.z, b0.w), pack2(b1.x, b1.y),
+                                          pack2(b1.z, b1.w)};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const unsigned long long ai = pack2(av[i], av[i]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ffma2(acc2[i][j], ai, bp[j]);
+        }
+#else
         const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+#endif
       }
     };
 
@@ -419,7 +471,12 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
       for (int h = 0; h < 2; ++h) {
         const int gj = col0 + tcol + h * 16;
         float* p = C + (size_t)gi * ldc + gj;
+#if ELV_K56_FFMA2
+        const float2 lo = unpack2(acc2[i][2 * h]), hi = unpack2(acc2[i][2 * h + 1]);
+        const float v[4] = {lo.x, lo.y, hi.x, hi.y};
+#else
         const float* v = &acc[i][h * 4];
+#endif
         if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
         else
 #pragma unroll

@@ -1,10 +1,9 @@
 #!/bin/bash
-OUT=gpurun_out/${1:-s2bs}
+OUT=gpurun_out/${1:-s2bu}
 mkdir -p $OUT
-for rep in 1 2; do
-for lib in libelevate_b200.so libelevate_b200_sm32x3.so libelevate_b200_sm32x2.so libelevate_b200_sm8x6.so; do
-  for n in 1024 2048 4096; do
-  ELV_LIB=$PWD/paper_2002_02268_b200/$lib ONLY_SIMT=1 timeout 300 python scripts/small_timing.py $n $n $n | sed "s/^{/{\"lib\": \"$lib\", /" >> $OUT/small.jsonl 2>> $OUT/small.err
+for lib in libelevate_b200.so libelevate_b200_k34.so; do
+  for n in 1024 8192; do
+  ELV_LIB=$PWD/paper_2002_02268_b200/$lib SCHEDS=loopPerm,arrayPacking,cacheBlocks timeout 300 python scripts/small_timing.py $n $n $n | sed "s/^{/{\"lib\": \"$lib\", /" >> $OUT/small.jsonl 2>> $OUT/small.err
   done
 done
-done
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_codegen.py -q -x -p no:cacheprovider > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/summary.txt

@@ -21,6 +21,8 @@ def main():
     cases = [("parallel", False, "tf32"), ("parallel", True, "tf32"), ("parallel", True, "fp16")]
     if os.environ.get("ONLY_SIMT"):
         cases = cases[:1]
+    if os.environ.get("SCHEDS"):
+        cases = [(x, False, "tf32") for x in os.environ["SCHEDS"].split(",")]
     for sched, tf, enc in cases:
         term = schedules.apply_padded(sched, M, N, K).term
         p = interp.plan(term, [(M, K), (K, N)], tf, enc)
@@ -63,7 +65,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         gr = e0.elapsed_time(e1) / 200
-        print(json.dumps({"shape": [M, N, K], "variant": p.variant, "enc": enc, "us_single": round(ms * 1e3, 2),
+        print(json.dumps({"shape": [M, N, K], "sched": sched, "variant": p.variant, "enc": enc, "us_single": round(ms * 1e3, 2),
                           "us_back_to_back": round(b2b * 1e3, 2), "us_graph": round(gr * 1e3, 2),
                           "TFLOP/s_single": round(2.0 * M * N * K / ms / 1e9, 1),
                           "TFLOP/s_graph": round(2.0 * M * N * K / gr / 1e9, 1)}), flush=True)
