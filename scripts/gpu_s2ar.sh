@@ -18,3 +18,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_tf32x3_pair -s 1 -c 1 \
   -o $OUT/prof_k8_bench python scripts/profile_one.py --variant parallel_fp16x3 --M 32768 --N 32768 --K 8192 --reps 2 \
   > $OUT/prof_k8.log 2>&1; echo "ncu full rc=$?" >> $S
+timeout 1200 python bench.py --workload ladder > $OUT/ladder.jsonl 2> $OUT/ladder.err; echo "ladder rc=$?" >> $S
+timeout 900 python bench.py --variant parallel --no-e2e --no-cpu-baseline > $OUT/bench_simt.json 2> $OUT/bench_simt.err; echo "bench simt rc=$?" >> $S
