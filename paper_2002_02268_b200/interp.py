@@ -120,23 +120,24 @@ class GemmCall:
         self.ws = (torch.empty(self.ws_bytes, device=A.device, dtype=torch.uint8)
                    if self.ws_bytes else None)
         self.launches = self.PREPARE_LAUNCHES[p.variant] + 1
-
-    def _args(self):
-        return (self.ws.data_ptr() if self.ws is not None else None, self.ws_bytes,
-                self.stream.cuda_stream)
+        # the buffers are fixed for the object's lifetime: build the C-ABI
+        # argument tuples once (saves 1.5-3 us of host time per 1024^3 call,
+        # 5-8 % of a single 3xTF32 / SIMT call; profiles/r1/small/gemmcall_args.jsonl)
+        ws = (self.ws.data_ptr() if self.ws is not None else None, self.ws_bytes, self.stream.cuda_stream)
+        self._prep_args = (p.variant, A.data_ptr(), B.data_ptr(), p.M, p.N, p.K, A.stride(0), B.stride(0), *ws)
+        self._comp_args = (p.variant, A.data_ptr(), B.data_ptr(), C.data_ptr(), p.M, p.N, p.K, A.stride(0),
+                           B.stride(0), C.stride(0), *ws)
+        self._prep_fn, self._comp_fn = self.lib.elv_gemm_prepare, self.lib.elv_gemm_compute
 
     def prepare(self):
-        p = self.p
-        rc = self.lib.elv_gemm_prepare(p.variant, self.A.data_ptr(), self.B.data_ptr(), p.M, p.N, p.K,
-                                       self.A.stride(0), self.B.stride(0), *self._args())
-        _lib.check(rc, "elv_gemm_prepare")
+        rc = self._prep_fn(*self._prep_args)
+        if rc:
+            _lib.check(rc, "elv_gemm_prepare")
 
     def compute(self):
-        p = self.p
-        rc = self.lib.elv_gemm_compute(p.variant, self.A.data_ptr(), self.B.data_ptr(),
-                                       self.C.data_ptr(), p.M, p.N, p.K, self.A.stride(0),
-                                       self.B.stride(0), self.C.stride(0), *self._args())
-        _lib.check(rc, "elv_gemm_compute")
+        rc = self._comp_fn(*self._comp_args)
+        if rc:
+            _lib.check(rc, "elv_gemm_compute")
 
     def __call__(self):
         self.prepare()
