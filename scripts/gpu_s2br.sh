@@ -1,11 +1,7 @@
 #!/bin/bash
-OUT=gpurun_out/${1:-s2bx}
+OUT=gpurun_out/${1:-s2by}
 mkdir -p $OUT
-for rep in 1 2; do
-for nt in 64 128; do
-  for n in 1024 2048 4096; do
-  ELV_K6_SMALL_THREADS=$nt ONLY_SIMT=1 timeout 300 python scripts/small_timing.py $n $n $n | sed "s/^{/{\"nt\": $nt, /" >> $OUT/small.jsonl 2>> $OUT/small.err
-  done
+for lib in libelevate_b200.so libelevate_b200_kt64.so; do
+  ELV_LIB=$PWD/paper_2002_02268_b200/$lib timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k16 --csv --log-file $OUT/k16_$lib.csv python scripts/profile_one.py --variant parallel_fp16x3 --M 32768 --N 32768 --K 8192 --reps 3 > $OUT/prof_$lib.log 2>&1
 done
-done
-ELV_K6_SMALL_THREADS=128 timeout 1200 python -m pytest tests/test_gpu_parity.py -q -x -k "parallel or small or odd" -p no:cacheprovider > $OUT/pytest128.log 2>&1; echo "pytest128 rc=$?" >> $OUT/summary.txt
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_rowshard.py -q -x -k "fp16 or host" -p no:cacheprovider > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/summary.txt
