@@ -3,11 +3,14 @@
 //
 // This is the reference's calling convention -- interp.run(e, [A, B]) takes
 // host values and returns a host value (reference pkg/src/stratir/interp.py:
-// 157-162) -- made fast: the output is cut into R x Nc tiles; the H2D stream
-// brings in B column chunks and A row blocks in the order that enables C
-// tiles soonest, the caller's stream prepares (packB / tf32 split) and
-// multiplies each tile as soon as both its operands have landed, and the D2H
-// stream returns each C tile as soon as it is written.  PCIe is full duplex
+// 157-162) -- made fast.  Two plans (make_plan): the grid cuts the output
+// into R x Nc tiles, the H2D stream brings in B column chunks and A row
+// blocks in the order that enables C tiles soonest, the caller's stream
+// prepares (packB / tf32 / fp16 split) and multiplies each tile as soon as
+// both its operands have landed, and the D2H stream returns each C tile as
+// soon as it is written; the growing schedule (tensor-core variants, large
+// C) brings A and B in strips and multiplies each landed strip against the
+// other operand's resident prefix, so C starts flowing back after a few MB.  PCIe is full duplex
 // (measured ~55 GB/s each way, ~100 GB/s both), so for large problems the
 // step is bound by the D2H of C (the largest transfer) plus pipeline fill.  Tiles of C are independent (the mapPar axis), and each
 // tile's per-element arithmetic is the single-launch kernel's, so the result
