@@ -169,12 +169,14 @@ class HostPipeline:
     """Host-resident A, B -> host C with the transfers overlapped: a thin
     binding of the C-ABI host pipeline `elv_gemm_host` (csrc/host_pipeline.cu).
 
-    The output is cut into R x Nc tiles; B column chunks and A row blocks
-    cross PCIe on the library's H2D stream in first-use order, each tile is
-    prepared (packB / tf32 split) and multiplied on the compute stream as soon
-    as its operands land, and goes back on the D2H stream as soon as it is
-    written (PCIe is full duplex).  Tiles of C are independent (the mapPar
-    axis) and each tile's per-element arithmetic is the single-launch
+    The output is cut into R x Nc tiles (or, for the tensor-core variants on
+    large outputs, A and B arrive in strips and each landed strip is
+    multiplied against the other operand's resident prefix); operands cross
+    PCIe on the library's H2D stream in first-use order, each block is
+    prepared (packB / tf32 / fp16 split) and multiplied on the compute stream
+    as soon as its operands land, and goes back on the D2H stream as soon as
+    it is written (PCIe is full duplex).  Blocks of C are independent (the
+    mapPar axis) and each block's per-element arithmetic is the single-launch
     kernel's, so the result is bit-identical to `gemm`.  The device workspace
     (A, B, C and the prepared operands) is torch-owned and cached here."""
 
