@@ -1214,15 +1214,51 @@ k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, flo
   split_a_row(A, K, lda, Kp, blockIdx.x, s, inv, hi, lo);
 }
 
-// elv_gemm's variant-8 prepare in one launch: blocks [0, M) scale and split
-// the rows of A, the rest take column-maximum slabs of B (independent work)
+// Short rows (K <= K16_WARP_ROW_K): one WARP per row -- the maximum is a
+// shuffle reduction with no block barrier, and a block covers 8 rows, so a
+// 1024^3 prepare launches 128 A blocks instead of 1024 one-row blocks (the
+// one-row blocks were latency-bound there).  Same scales and bits.
+constexpr int K16_WARP_ROW_K = 2048;
+__device__ __forceinline__ void split_a_row_warp(const float* __restrict__ A, int M, int K, int lda, int Kp, int r,
+                                                 float* __restrict__ s, float* __restrict__ inv,
+                                                 __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const float* row = A + (size_t)r * lda;
+  float m = 0.f;
+  for (int k = lane; k < K; k += 32) m = fmaxf(m, fabsf(__ldg(row + k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float sc, iv;
+  pow2_scale(m, &sc, &iv);
+  if (lane == 0) { s[r] = sc; inv[r] = iv; }
+  __half2* h2 = reinterpret_cast<__half2*>(hi + (size_t)r * Kp);
+  __half2* l2 = reinterpret_cast<__half2*>(lo + (size_t)r * Kp);
+  for (int k2 = lane; k2 < Kp / 2; k2 += 32) {
+    const int k = 2 * k2;
+    __half a0, a1, b0, b1;
+    split16(k < K ? __ldg(row + k) * sc : 0.f, &a0, &b0);
+    split16(k + 1 < K ? __ldg(row + k + 1) * sc : 0.f, &a1, &b1);
+    h2[k2] = __halves2half2(a0, a1);
+    l2[k2] = __halves2half2(b0, b1);
+  }
+}
+
+// elv_gemm's variant-8 prepare in one launch: blocks [0, ga) scale and split
+// the rows of A (one row per block, or 8 rows per block with warp_rows), the
+// rest take column-maximum slabs of B (independent work)
 __global__ void __launch_bounds__(256)
 k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
             float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo, const float* __restrict__ B,
-            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits) {
+            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits, int warp_rows) {
   const int b = blockIdx.x;
-  if (b < M) split_a_row(A, K, lda, Kp, b, s, inv, hi, lo);
-  else col_max_slab(B, K, N, ldb, (b - M) % gxb, (b - M) / gxb, maxbits);
+  const int ga = warp_rows ? (M + 7) / 8 : M;
+  if (b < ga) {
+    if (warp_rows) split_a_row_warp(A, M, K, lda, Kp, b * 8 + (threadIdx.x >> 5), s, inv, hi, lo);
+    else split_a_row(A, K, lda, Kp, b, s, inv, hi, lo);
+  } else {
+    col_max_slab(B, K, N, ldb, (b - ga) % gxb, (b - ga) / gxb, maxbits);
+  }
 }
 
 // B planes: [N][Kp] (B transposed to K-major) through 64(k) x 32(n) SMEM
@@ -1355,9 +1391,12 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   unsigned int* tmax = reinterpret_cast<unsigned int*>(PB.s);
   if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
   const int gxb = (N + 255) / 256, gyb = (K + COLMAX_SLAB - 1) / COLMAX_SLAB;
-  const long long blocks = (long long)M + (long long)gxb * gyb;
+  const int warp_rows = K <= K16_WARP_ROW_K && env_int("ELV_FP16X3_WARP_ROWS", 1) != 0;
+  const long long ga = warp_rows ? (M + 7) / 8 : M;
+  const long long blocks = ga + (long long)gxb * gyb;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
-  k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax);
+  k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax,
+                                                warp_rows);
   k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, tmax, PB.hi, PB.lo,
                                                                              PB.inv);
   return check_launch("fp16x3_prepare");

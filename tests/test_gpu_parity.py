@@ -390,3 +390,23 @@ def test_nan_and_inf_propagate_like_ieee(cuda, variant):
     Ah, Bh = A.cpu().numpy()[mask_r], B.cpu().numpy()[:, mask_c]
     ok, worst = oracle.check(C[mask_r][:, mask_c], oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
     assert ok, worst
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 1031, 777), (333, 700, 2048), (260, 520, 2049)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_fp16x3_warp_row_prepare_bitwise(cuda, shape, monkeypatch):
+    """Short rows (K <= 2048) split one row per warp instead of one per block:
+    bit-identical planes and C, including a zero row, a scaled row and K just
+    past the threshold (block-per-row path on both sides)."""
+    M, N, K = shape
+    A, B = _device_inputs(M, N, K, 16, cuda)
+    A[3] = 0.0
+    A[5] *= 2.0 ** -50
+    term = schedules.apply_padded("parallel", M, N, K).term
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("ELV_FP16X3_WARP_ROWS", flag)
+        outs.append(interp.run_tensor(term, A, B, tf32x3=True, tc_encoding="fp16"))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert torch.all(outs[0][3] == 0)
