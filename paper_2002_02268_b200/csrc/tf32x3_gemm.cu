@@ -31,7 +31,9 @@
 
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <stdlib.h>
 
 namespace elv {
@@ -886,27 +888,44 @@ static int pair_mode(int M, int N) {
   const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
   return pair_tiles >= num_sms() ? 32 : 0;
 }
-// per-device wave counter (library-internal scratch, 4 bytes), zeroed on the
-// launch stream before every launch; ELV_WAVE_SYNC=0 disables the sync.
+// Wave counter (library-internal scratch, 4 bytes) zeroed on the launch
+// stream before every launch; ELV_WAVE_SYNC=0 disables the sync.  One counter
+// per (device, stream): launches on one stream run in order, so the zeroing
+// never races a running kernel; a counter shared across streams could be
+// zeroed under a concurrently running GEMM whose producers then wait for
+// increments that never come.  The first launch on a stream allocates (not
+// allowed under graph capture: that launch simply runs without the sync).
 static unsigned int* wave_counter(int dev, cudaStream_t st) {
   static int enabled = -1;
   if (enabled < 0) enabled = env_int("ELV_WAVE_SYNC", 1) != 0;
   if (!enabled) return nullptr;
   static std::mutex mu;
-  static unsigned int* ctrs[64] = {nullptr};
-  if (dev < 0 || dev >= 64) return nullptr;
+  static std::map<std::pair<int, cudaStream_t>, unsigned int*> ctrs;
+  unsigned int* c = nullptr;
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (ctrs[dev] == nullptr && cudaMalloc(&ctrs[dev], 256) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
+    auto it = ctrs.find({dev, st});
+    if (it != ctrs.end()) {
+      c = it->second;
+    } else {
+      if (ctrs.size() >= 4096) return nullptr;
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      if (cudaMalloc(&c, 256) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      ctrs[{dev, st}] = c;
     }
   }
-  if (cudaMemsetAsync(ctrs[dev], 0, sizeof(unsigned int), st) != cudaSuccess) {
+  if (cudaMemsetAsync(c, 0, sizeof(unsigned int), st) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  return ctrs[dev];
+  return c;
 }
 
 static int tile_group(int dflt) {
