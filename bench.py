@@ -122,24 +122,68 @@ def roofline_peak(variant: str, peaks: dict, n_sms: int, cublas: dict | None = N
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks / throttle reasons sampled DURING the timed region.
+
+    NVML polled in-process every 10 ms (the bench's timed region is ~0.4 s, too
+    short for `nvidia-smi -lms`, whose start-up alone takes ~0.2 s); falls back
+    to `nvidia-smi -lms 200` when NVML is unavailable. `index` is the CUDA
+    device; NVML is addressed by its PCI bus id so CUDA_VISIBLE_DEVICES cannot
+    misroute it."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    PERIOD_S = 0.01
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.t = None
+        self.stop = threading.Event()
+        self.lines = []          # nvidia-smi fallback
+        self.samples = []        # (sm_mhz, max_mhz, reason names)
+        self.source = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll_nvml(self, nv, h):
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), [n for n, b in zip(self.NAMES, bits) if r & b]))
+            except Exception:
+                break
+            self.stop.wait(self.PERIOD_S)
 
     def __enter__(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.source = "nvml (10 ms)"
+            self.t.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
+            self.source = "nvidia-smi (200 ms)"
             self.t.start()
         except OSError:
             self.proc = None
@@ -150,33 +194,34 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.t:
             self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        samples = list(self.samples)
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                sm, mx = float(parts[0]), float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
+            samples.append((sm, mx, [n for n, v in zip(self.NAMES, parts[3:7])
+                                     if v.lower().startswith("active")]))
+        if not samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(s[0] for s in samples),
+                "sm_max_mhz": max(s[1] for s in samples),
+                "reasons": sorted({n for s in samples for n in s[2]}),
+                "samples": len(samples), "source": self.source}
 
 
 def traffic_from_profiles(kernel_key: str):

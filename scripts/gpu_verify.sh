@@ -1,0 +1,10 @@
+#!/bin/bash
+# Re-entry check: smoke, GPU tests, default bench line on the current build.
+OUT=gpurun_out/${1:-verify}
+mkdir -p $OUT
+S=$OUT/summary.txt
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+timeout 300 python __graft_entry__.py smoke > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $S
+timeout 1800 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $S
+tail -4 $OUT/pytest_gpu.log >> $S
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $S
