@@ -1177,10 +1177,10 @@ __device__ __forceinline__ void pow2_scale(float m, float* s, float* inv) {
 // per thread, combined with an integer atomicMax on the (non-negative) bits
 constexpr int COLMAX_SLAB = 64;
 __device__ __forceinline__ void col_max_slab(const float* __restrict__ B, int K, int N, int ldb, int bx, int by,
-                                             unsigned int* __restrict__ maxbits) {
+                                             unsigned int* __restrict__ maxbits, int slab = COLMAX_SLAB) {
   const int j = bx * 256 + threadIdx.x;
   if (j >= N) return;
-  const int k0 = by * COLMAX_SLAB, k1 = min(K, k0 + COLMAX_SLAB);
+  const int k0 = by * slab, k1 = min(K, k0 + slab);
   float m = 0.f;
   for (int k = k0; k < k1; ++k) m = fmaxf(m, fabsf(__ldg(B + (size_t)k * ldb + j)));
   atomicMax(maxbits + j, __float_as_uint(m));
@@ -1263,20 +1263,65 @@ __device__ __forceinline__ void split_a_row_warp(const float* __restrict__ A, in
   }
 }
 
+// The same warp-per-row split with the row held in registers: each lane
+// loads its float4 chunks once (all loads in flight together), reduces the
+// maximum and splits from registers -- no second pass over the row and no
+// dependent load chain.  Needs K % 4 == 0, lda % 4 == 0 and a 16 B aligned A;
+// identical scales and bits (max is order-free, the split is per element).
+constexpr int K16_VEC_CHUNKS = K16_WARP_ROW_K / 128;
+__device__ __forceinline__ void split_a_row_warp_vec(const float* __restrict__ A, int M, int K, int lda, int Kp,
+                                                     int r, float* __restrict__ s, float* __restrict__ inv,
+                                                     __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const float4* row = reinterpret_cast<const float4*>(A + (size_t)r * lda);
+  float4 v[K16_VEC_CHUNKS];
+  float m = 0.f;
+#pragma unroll
+  for (int c = 0; c < K16_VEC_CHUNKS; ++c) {
+    const int k = c * 128 + lane * 4;
+    v[c] = k < K ? __ldg(row + c * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float sc, iv;
+  pow2_scale(m, &sc, &iv);
+  if (lane == 0) { s[r] = sc; inv[r] = iv; }
+#pragma unroll
+  for (int c = 0; c < K16_VEC_CHUNKS; ++c) {
+    const int k = c * 128 + lane * 4;
+    if (k < Kp) {
+      __half h[4], l[4];
+      split16(v[c].x * sc, &h[0], &l[0]);
+      split16(v[c].y * sc, &h[1], &l[1]);
+      split16(v[c].z * sc, &h[2], &l[2]);
+      split16(v[c].w * sc, &h[3], &l[3]);
+      const __half2 h01 = __halves2half2(h[0], h[1]), h23 = __halves2half2(h[2], h[3]);
+      const __half2 l01 = __halves2half2(l[0], l[1]), l23 = __halves2half2(l[2], l[3]);
+      *reinterpret_cast<uint2*>(hi + (size_t)r * Kp + k) =
+          make_uint2(*reinterpret_cast<const unsigned int*>(&h01), *reinterpret_cast<const unsigned int*>(&h23));
+      *reinterpret_cast<uint2*>(lo + (size_t)r * Kp + k) =
+          make_uint2(*reinterpret_cast<const unsigned int*>(&l01), *reinterpret_cast<const unsigned int*>(&l23));
+    }
+  }
+}
+
 // elv_gemm's variant-8 prepare in one launch: blocks [0, ga) scale and split
 // the rows of A (one row per block, or 8 rows per block with warp_rows), the
 // rest take column-maximum slabs of B (independent work)
 __global__ void __launch_bounds__(256)
 k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
             float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo, const float* __restrict__ B,
-            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits, int warp_rows) {
+            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits, int warp_rows, int slab) {
   const int b = blockIdx.x;
   const int ga = warp_rows ? (M + 7) / 8 : M;
   if (b < ga) {
-    if (warp_rows) split_a_row_warp(A, M, K, lda, Kp, b * 8 + (threadIdx.x >> 5), s, inv, hi, lo);
+    if (warp_rows == 2) split_a_row_warp_vec(A, M, K, lda, Kp, b * 8 + (threadIdx.x >> 5), s, inv, hi, lo);
+    else if (warp_rows) split_a_row_warp(A, M, K, lda, Kp, b * 8 + (threadIdx.x >> 5), s, inv, hi, lo);
     else split_a_row(A, K, lda, Kp, b, s, inv, hi, lo);
   } else {
-    col_max_slab(B, K, N, ldb, (b - ga) % gxb, (b - ga) / gxb, maxbits);
+    col_max_slab(B, K, N, ldb, (b - ga) % gxb, (b - ga) / gxb, maxbits, slab);
   }
 }
 
@@ -1409,13 +1454,25 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   const int Kp = (int)kpad16(K);
   unsigned int* tmax = reinterpret_cast<unsigned int*>(PB.s);
   if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
-  const int gxb = (N + 255) / 256, gyb = (K + COLMAX_SLAB - 1) / COLMAX_SLAB;
-  const int warp_rows = K <= K16_WARP_ROW_K && env_int("ELV_FP16X3_WARP_ROWS", 1) != 0;
+  // Short rows: one warp per A row (2: row in registers, when float4 loads
+  // are legal; 1: two scalar passes); ELV_FP16X3_WARP_ROWS caps the mode
+  // (0 = one block per row).  Column-maximum slabs shrink from 64 rows
+  // until the B part has >= 4 blocks per SM (1024^3: 64 -> 512 blocks of
+  // 8 rows) -- with few, long slabs the dependent load chain set the time.
+  const int gxb = (N + 255) / 256;
+  const bool vec_ok = K % 4 == 0 && lda % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  const int warp_rows = K <= K16_WARP_ROW_K ? min(env_int("ELV_FP16X3_WARP_ROWS", 2), vec_ok ? 2 : 1) : 0;
+  int slab = env_int("ELV_FP16X3_COLMAX_SLAB", 0);
+  if (slab <= 0) {
+    slab = COLMAX_SLAB;
+    while (slab > 8 && (long long)gxb * ((K + slab - 1) / slab) < 4LL * 148) slab /= 2;
+  }
+  const int gyb = (K + slab - 1) / slab;
   const long long ga = warp_rows ? (M + 7) / 8 : M;
   const long long blocks = ga + (long long)gxb * gyb;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
   k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax,
-                                                warp_rows);
+                                                warp_rows, slab);
   k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, tmax, PB.hi, PB.lo,
                                                                              PB.inv);
   return check_launch("fp16x3_prepare");

@@ -392,21 +392,25 @@ def test_nan_and_inf_propagate_like_ieee(cuda, variant):
     assert ok, worst
 
 
-@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 1031, 777), (333, 700, 2048), (260, 520, 2049)],
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 1031, 777), (333, 700, 2048), (260, 520, 2049),
+                                   (130, 70, 516)],
                          ids=lambda s: "x".join(map(str, s)))
 def test_fp16x3_warp_row_prepare_bitwise(cuda, shape, monkeypatch):
-    """Short rows (K <= 2048) split one row per warp instead of one per block:
-    bit-identical planes and C, including a zero row, a scaled row and K just
-    past the threshold (block-per-row path on both sides)."""
+    """Short rows (K <= 2048) split one row per warp instead of one per block
+    (mode 2: the row held in registers, float4 loads; mode 1: two scalar
+    passes), and B's column maxima in slabs of 8..64 rows: bit-identical C
+    in every mode, including a zero row, a scaled row, K not a multiple of 4
+    (mode 2 falls back to 1) and K just past the threshold."""
     M, N, K = shape
     A, B = _device_inputs(M, N, K, 16, cuda)
     A[3] = 0.0
     A[5] *= 2.0 ** -50
     term = schedules.apply_padded("parallel", M, N, K).term
     outs = []
-    for flag in ("1", "0"):
+    for flag, slab in (("2", "0"), ("1", "0"), ("0", "64"), ("2", "8"), ("1", "16")):
         monkeypatch.setenv("ELV_FP16X3_WARP_ROWS", flag)
+        monkeypatch.setenv("ELV_FP16X3_COLMAX_SLAB", slab)
         outs.append(interp.run_tensor(term, A, B, tf32x3=True, tc_encoding="fp16"))
     torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1])
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
     assert torch.all(outs[0][3] == 0)
