@@ -1314,6 +1314,7 @@ __global__ void __launch_bounds__(256)
 k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
             float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo, const float* __restrict__ B,
             int N, int ldb, int gxb, unsigned int* __restrict__ maxbits, int warp_rows, int slab) {
+  griddep_launch_dependents();                    // the split-transpose may stage its B tiles meanwhile
   const int b = blockIdx.x;
   const int ga = warp_rows ? (M + 7) / 8 : M;
   if (b < ga) {
@@ -1335,18 +1336,20 @@ k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp
                       float* __restrict__ inv_t) {
   __shared__ float tile[64][33];
   __shared__ float scale[32];
+  griddep_launch_dependents();                    // the GEMM waits (griddepcontrol.wait) for our completion
   const int k0 = blockIdx.y * 64, n0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  if (ty == 0) {
-    float sc = 1.f, iv = 1.f;
-    if (n0 + tx < N) pow2_scale(__uint_as_float(maxbits[n0 + tx]), &sc, &iv);
-    scale[tx] = sc;
-    if (blockIdx.y == 0 && n0 + tx < N) inv_t[n0 + tx] = iv;
-  }
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < 8; ++r) {                   // B is an input: staged before the maxima are ready
     const int k = k0 + ty + 8 * r, n = n0 + tx;
     tile[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
+  }
+  griddep_wait();                                 // column maxima from k16_prep_ab (PDL launch)
+  if (ty == 0) {
+    float sc = 1.f, iv = 1.f;
+    if (n0 + tx < N) pow2_scale(__uint_as_float(__ldcg(maxbits + n0 + tx)), &sc, &iv);
+    scale[tx] = sc;
+    if (blockIdx.y == 0 && n0 + tx < N) inv_t[n0 + tx] = iv;
   }
   __syncthreads();
 #pragma unroll
@@ -1473,8 +1476,10 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
   k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax,
                                                 warp_rows, slab);
-  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, tmax, PB.hi, PB.lo,
-                                                                             PB.inv);
+  if (cudaPeekAtLastError() != cudaSuccess) return check_launch("fp16x3_prepare");
+  const cudaError_t e = launch_pdl(k16_split_transpose_b, dim3((N + 31) / 32, (Kp + 63) / 64), dim3(256), 0, st, B, K,
+                                   N, ldb, Kp, (const unsigned int*)tmax, PB.hi, PB.lo, PB.inv);
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3_prepare: %s", cudaGetErrorString(e));
   return check_launch("fp16x3_prepare");
 }
 
