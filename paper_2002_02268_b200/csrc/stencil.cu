@@ -116,14 +116,29 @@ k_bf_band(const float* __restrict__ img, float* __restrict__ out, int H, int W, 
       h1 = h2;
     }
   } else {
+    // 3x3 window slid down the band in registers: 3 SMEM reads per output
+    // instead of 9; the taps are folded in the same (a, b) order, so the
+    // result is bitwise the unbanded naive kernel's
     const float w[9] = {W0, W1, W0, W1, W2, W1, W0, W1, W0};
+    float x[3][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) x[a][b] = tile[a][t + b];
     for (int r = 0; r < rows; ++r) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) x[2][b] = tile[r + 2][t + b];
       float acc = 0.f;
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) acc = fmaf(w[3 * a + b], tile[r + a][t + b], acc);
+        for (int b = 0; b < 3; ++b) acc = fmaf(w[3 * a + b], x[a][b], acc);
       out[(size_t)(r0 + r) * ldo + j] = acc;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        x[0][b] = x[1][b];
+        x[1][b] = x[2][b];
+      }
     }
   }
 }
