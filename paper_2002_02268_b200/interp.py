@@ -262,6 +262,9 @@ def _run_generic(e, args, device=None):
     kernel per term (codegen.py, the GPU analogue of SPEC's codegen-c)."""
     from . import codegen
     kinds = [type(a) for a in args]
+    empty = _empty_gemm(e, args, out)
+    if empty is not None:
+        return empty
     ts = [_as_host_f32(a) for a in args]
     if device is None:
         cuda_in = [t for t in ts if t.is_cuda]
@@ -297,6 +300,51 @@ def run(e, args: list, *, device=None, tf32x3: bool | None = None, out=None, tc_
         return _run_generic(e, args, device)
 
 
+def _operand_shape(x):
+    """(rows, cols) of a matrix operand; cols is None for an empty list (no
+    row to read it from); None when x is not a 2-D operand."""
+    if isinstance(x, list):
+        if not x:
+            return 0, None
+        if not isinstance(x[0], list):
+            return None
+        return len(x), len(x[0])
+    if isinstance(x, (np.ndarray, torch.Tensor)) and x.ndim == 2:
+        return int(x.shape[0]), int(x.shape[1])
+    return None
+
+
+def _empty_gemm(e, args, out):
+    """Zero-extent GEMMs, answered from the shapes alone -- there is no
+    arithmetic to run -- with the reference interpreter's outcome:
+      * no rows in A: `map` over [] is [] (interp.py:80-83), whatever B is;
+      * rows, but B has no rows (K = 0): `transpose` of an empty array
+        raises EvalError (interp.py:115-120);
+      * rows, K > 0, no columns in B: the baseline schedule maps over the
+        empty transpose -> M empty rows; the tiled schedules transpose an
+        empty column tile and raise the same EvalError.
+    Returns None when no extent is zero (the kernel path runs)."""
+    sa, sb = _operand_shape(args[0]), _operand_shape(args[1])
+    if sa is None or sb is None:
+        return None
+    (M, K), (K2, N) = sa, sb
+    if M and K2 and N:
+        return None
+    name = dispatch.decode(e).schedule        # EvalError unless e is one of the seven GEMM schedules
+    if M and not K2:
+        raise EvalError("transpose of empty array")
+    if M and name != "baseline":
+        raise EvalError("transpose of empty array")
+    n = N or 0
+    if isinstance(args[0], list):
+        return [[] for _ in range(M)]
+    if out is not None:
+        return out
+    if isinstance(args[0], np.ndarray):
+        return np.zeros((M, n), dtype=np.float32)
+    return torch.empty((M, n), dtype=torch.float32, device=args[0].device)
+
+
 def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out=None,
                   tc_encoding: str | None = None):
     if len(args) == 1:
@@ -304,6 +352,9 @@ def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out
     if len(args) != 2:
         raise EvalError(f"no B200 kernel for term: {len(args)}-argument program")
     kinds = [type(a) for a in args]
+    empty = _empty_gemm(e, args, out)
+    if empty is not None:
+        return empty
     ts = [_as_host_f32(a) for a in args]
     for t in ts:
         if t.dim() != 2:
