@@ -262,6 +262,7 @@ def _run_generic(e, args, device=None):
     kernel per term (codegen.py, the GPU analogue of SPEC's codegen-c)."""
     from . import codegen
     kinds = [type(a) for a in args]
+    args = [args[0], _truncate_ragged(args[1])]
     empty = _empty_gemm(e, args, out)
     if empty is not None:
         return empty
@@ -314,6 +315,18 @@ def _operand_shape(x):
     return None
 
 
+def _truncate_ragged(b):
+    """Every schedule reads B through `transpose`, which is `zip(*m)` in the
+    reference (interp.py:115-120): rows of unequal length are cut to the
+    shortest.  Mirror that for nested-list B (ragged A raises EvalError on
+    both sides: zip of unequal lengths)."""
+    if isinstance(b, list) and b and all(isinstance(r, list) for r in b):
+        n = min(len(r) for r in b)
+        if any(len(r) != n for r in b):
+            return [r[:n] for r in b]
+    return b
+
+
 def _empty_gemm(e, args, out):
     """Zero-extent GEMMs, answered from the shapes alone -- there is no
     arithmetic to run -- with the reference interpreter's outcome:
@@ -352,6 +365,7 @@ def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out
     if len(args) != 2:
         raise EvalError(f"no B200 kernel for term: {len(args)}-argument program")
     kinds = [type(a) for a in args]
+    args = [args[0], _truncate_ragged(args[1])]
     empty = _empty_gemm(e, args, out)
     if empty is not None:
         return empty

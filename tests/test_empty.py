@@ -59,3 +59,20 @@ def test_zero_extent_rejects_foreign_terms():
     ir = S().ir
     with pytest.raises(S().interp.EvalError):
         interp._empty_gemm(ir.Lam("a", None, ir.Lam("b", None, ir.Var("a"))), [[], []], None)
+
+
+def test_ragged_b_is_cut_to_the_shortest_row():
+    B = [[1.0, 2.0, 3.0], [4.0, 5.0], [6.0, 7.0, 8.0]]
+    assert interp._truncate_ragged(B) == [[1.0, 2.0], [4.0, 5.0], [6.0, 7.0]]
+    assert interp._truncate_ragged([[1.0], [2.0]]) == [[1.0], [2.0]]
+
+
+def test_any_divisible_shape_decodes():
+    """The reference evaluates a scheduled term at any shape its split sizes
+    divide (sizes are not read from the annotations at run time)."""
+    from paper_2002_02268_b200 import dispatch
+    term = schedules.apply("parallel", 64, 64, 64).term
+    p = dispatch.decode(term, [(32, 96), (96, 128)])
+    assert (p.M, p.N, p.K) == (32, 128, 96)
+    with pytest.raises(S().interp.EvalError):
+        dispatch.decode(term, [(40, 96), (96, 128)])      # pads to (64, 128, 96), not the term's shape

@@ -414,3 +414,20 @@ def test_fp16x3_warp_row_prepare_bitwise(cuda, shape, monkeypatch):
     torch.cuda.synchronize()
     assert all(torch.equal(outs[0], o) for o in outs[1:])
     assert torch.all(outs[0][3] == 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", schedules.SCHEDULE_NAMES)
+def test_ragged_b_and_shape_other_than_the_annotation(cuda, name):
+    """Like the reference interpreter: a term scheduled at mm(64,64,64) runs
+    on 32x96 . 96xN inputs (its split sizes divide them), and a ragged B is
+    cut to its shortest row (transpose = zip(*m), interp.py:115-120)."""
+    term = schedules.apply(name, 64, 64, 64).term
+    A, B = synth.matrix(32, 96, 5, 0), synth.matrix(96, 160, 5, 1)
+    Bl = B.tolist()
+    Bl[7] = Bl[7][:128]
+    C = np.array(interp.run(term, [A.tolist(), Bl]))
+    assert C.shape == (32, 128)
+    Bt = np.ascontiguousarray(B[:, :128])
+    ok, worst = oracle.check(C, oracle.mm_f64(A, Bt), oracle.absprod_np(A, Bt), 96)
+    assert ok, worst
