@@ -262,10 +262,6 @@ def _run_generic(e, args, device=None):
     kernel per term (codegen.py, the GPU analogue of SPEC's codegen-c)."""
     from . import codegen
     kinds = [type(a) for a in args]
-    args = [args[0], _truncate_ragged(args[1])]
-    empty = _empty_gemm(e, args, out)
-    if empty is not None:
-        return empty
     ts = [_as_host_f32(a) for a in args]
     if device is None:
         cuda_in = [t for t in ts if t.is_cuda]
