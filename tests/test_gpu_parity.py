@@ -431,3 +431,17 @@ def test_ragged_b_and_shape_other_than_the_annotation(cuda, name):
     Bt = np.ascontiguousarray(B[:, :128])
     ok, worst = oracle.check(C, oracle.mm_f64(A, Bt), oracle.absprod_np(A, Bt), 96)
     assert ok, worst
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("enc", ["tf32", "fp16"])
+def test_tensor_core_variant_on_a_shape_other_than_the_annotation(cuda, enc):
+    """The relaxed decode on the tcgen05 path: a parallel term scheduled at
+    mm(128,128,512) evaluated on 64x512 . 512x96 device operands."""
+    term = schedules.apply("parallel", 128, 128, 512).term
+    A, B = _device_inputs(64, 96, 512, 31, cuda)
+    C = interp.run_tensor(term, A, B, tf32x3=True, tc_encoding=enc).cpu().numpy()
+    assert C.shape == (64, 96)
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), 512)
+    assert ok, worst
