@@ -153,8 +153,26 @@ size_t elv_fp16x3_b_planes_bytes(int N, int K);
 int elv_fp16x3_applicable(int M, int N, int K);
 int elv_fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, void* stream);
 int elv_fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, void* stream);
+/* split_b from packedB panels (elv_pack_b layout) of N columns: what every
+ * rank of the row-shard pipeline runs on a broadcast chunk */
+int elv_fp16x3_split_b_packed(const float* packedB, int K, int N, void* b_planes, void* stream);
 int elv_fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
                            int M, int N, int K, int ldc, void* stream);
+
+/* Range guard of the tensor-core encodings (variants 7 and 8).  The splits
+ * mark every row of A / column of B holding an element outside the
+ * encoding's exact window (non-finite; tf32: 0 < |x| < 2^-100; fp16: a
+ * scaled value below fp16's normal range, i.e. more than 2^29 below its
+ * row / column maximum).  elv_gemm / elv_gemm_compute and elv_gemm_host
+ * recompute those rows and columns of C with the SIMT fp32 FMA chain
+ * automatically; planes-API callers run elv_tc_fixup after gemm_planes with
+ * the same operands in fp32 (A: M x K, lda; B: K x N row-major with ldb, or,
+ * with b_packed = 1, packedB panels (elv_pack_b layout) of these N columns).
+ * encoding: 7 (tf32 planes) or 8 (fp16 planes).  With nothing marked it is
+ * one short launch. */
+int elv_tc_fixup(int encoding, const void* a_planes, const void* b_planes, const float* A, int lda,
+                 const float* B, int ldb, int b_packed, float* C, int ldc, int M, int N, int K,
+                 void* stream);
 
 /* Synthetic inputs: X[i] = U(-1,1) with 24-bit resolution from
  * splitmix64((seed << 48) ^ (tensor_id << 40) ^ (offset + i)); bit-identical

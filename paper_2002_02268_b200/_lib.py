@@ -26,7 +26,7 @@ EXPORTS = (
     "elv_tf32x3_gemm_planes", "elv_binomial", "elv_binomial_variant_name",
     "elv_gemm_host", "elv_gemm_host_workspace_bytes", "elv_gemm_host_tiles", "elv_gemm_host_trace", "elv_copy2d",
     "elv_fp16x3_a_planes_bytes", "elv_fp16x3_b_planes_bytes", "elv_fp16x3_applicable", "elv_fp16x3_split_a",
-    "elv_fp16x3_split_b", "elv_fp16x3_gemm_planes",
+    "elv_fp16x3_split_b", "elv_fp16x3_gemm_planes", "elv_fp16x3_split_b_packed", "elv_tc_fixup",
 )
 
 _lib = None
@@ -80,6 +80,9 @@ def load():
         "elv_fp16x3_split_a": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
         "elv_fp16x3_split_b": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
         "elv_fp16x3_gemm_planes": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
+        "elv_fp16x3_split_b_packed": (c_int, [c_vp, c_int, c_int, c_vp, c_vp]),
+        "elv_tc_fixup": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_int, c_vp, c_int, c_int, c_int,
+                                 c_int, c_vp]),
         "elv_binomial": (c_int, [c_int, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
         "elv_binomial_variant_name": (ctypes.c_char_p, [c_int]),
         "elv_last_error": (ctypes.c_char_p, []),

@@ -112,7 +112,8 @@ def launch(variant: int, img, out, stream=None):
     lib = _lib.load()
     H, W = img.shape
     stream = stream or torch.cuda.current_stream(img.device)
-    rc = lib.elv_binomial(variant, img.data_ptr(), out.data_ptr(), H, W, img.stride(0), out.stride(0),
-                          stream.cuda_stream)
+    with torch.cuda.device(img.device):
+        rc = lib.elv_binomial(variant, img.data_ptr(), out.data_ptr(), H, W, img.stride(0), out.stride(0),
+                              stream.cuda_stream)
     _lib.check(rc, f"elv_binomial[{SCHEDULE_NAMES[variant]}]")
     return out

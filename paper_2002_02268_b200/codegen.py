@@ -748,8 +748,13 @@ def _check(res):
 
 
 @functools.lru_cache(maxsize=64)
-def _kernel_for_key(key: str, term_holder) -> Kernel:
-    return Kernel(compile_term(term_holder.term))
+def _kernel_for_key(key: str, device_index: int, term_holder) -> Kernel:
+    # a module belongs to the context it was loaded in: one Kernel per
+    # (term, device), loaded while that device is current
+    import torch
+    with torch.cuda.device(device_index):
+        torch.cuda.current_stream()              # make sure the device's primary context is current
+        return Kernel(compile_term(term_holder.term))
 
 
 class _Holder:
@@ -765,15 +770,19 @@ class _Holder:
         return isinstance(other, _Holder) and other.key == self.key
 
 
-def kernel_for(term) -> Kernel:
+def kernel_for(term, device_index: int | None = None) -> Kernel:
+    import torch
     key = S().ir.pretty(term)
-    return _kernel_for_key(key, _Holder(key, term))
+    if device_index is None:
+        device_index = torch.cuda.current_device()
+    return _kernel_for_key(key, device_index, _Holder(key, term))
 
 
 def run(term, tensors, stream=None):
     """Evaluate `term` on device tensors with a generated kernel."""
     import torch
-    k = kernel_for(term)
+    dev = tensors[0].device if tensors and tensors[0].is_cuda else torch.device("cuda", torch.cuda.current_device())
+    k = kernel_for(term, dev.index)
     if len(tensors) != len(k.c.in_shapes):
         raise S().interp.EvalError(f"the program takes {len(k.c.in_shapes)} arguments, got {len(tensors)}")
     ins = []
@@ -783,5 +792,6 @@ def run(term, tensors, stream=None):
         ins.append(t.contiguous().float())
     out = torch.empty(k.c.out_shape, device=ins[0].device, dtype=torch.float32)
     stream = stream or torch.cuda.current_stream(ins[0].device)
-    k(ins, out, stream.cuda_stream)
+    with torch.cuda.device(ins[0].device):
+        k(ins, out, stream.cuda_stream)
     return out

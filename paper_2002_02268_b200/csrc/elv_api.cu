@@ -268,9 +268,9 @@ int elv_gemm_compute(int variant, const float* A, const float* B, float* C, int 
       return launch_simt(variant, A, nullptr, static_cast<const float*>(workspace), C, M, N, K, lda, 0,
                          ldc, st);
     case ELV_PARALLEL_TF32X3:
-      return tf32x3_compute(C, M, N, K, ldc, workspace, workspace_bytes, st);
+      return tf32x3_compute(A, B, lda, ldb, C, M, N, K, ldc, workspace, workspace_bytes, st);
     case ELV_PARALLEL_FP16X3:
-      return fp16x3_compute(C, M, N, K, ldc, workspace, workspace_bytes, st);
+      return fp16x3_compute(A, B, lda, ldb, C, M, N, K, ldc, workspace, workspace_bytes, st);
   }
   return set_error(ELV_EVARIANT, "unknown variant %d", variant);
 }
@@ -332,11 +332,28 @@ int elv_fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, vo
   return fp16x3_split_b(B, K, N, ldb, b_planes, (cudaStream_t)stream);
 }
 
+int elv_fp16x3_split_b_packed(const float* packedB, int K, int N, void* b_planes, void* stream) {
+  if (bad_ptr(packedB) || bad_ptr(b_planes) || N < 1 || K < 1)
+    return set_error(ELV_EINVAL, "fp16x3_split_b_packed: bad arguments");
+  return fp16x3_split_b(packedB, K, N, 0, b_planes, (cudaStream_t)stream, 0, 0, true);
+}
+
 int elv_fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                            void* stream) {
   if (bad_ptr(a_planes) || bad_ptr(b_planes) || bad_ptr(C) || M < 1 || N < 1 || K < 1 || ldc < N)
     return set_error(ELV_EINVAL, "fp16x3_gemm_planes: bad arguments");
   return fp16x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
+}
+
+int elv_tc_fixup(int encoding, const void* a_planes, const void* b_planes, const float* A, int lda, const float* B,
+                 int ldb, int b_packed, float* C, int ldc, int M, int N, int K, void* stream) {
+  if (encoding != ELV_PARALLEL_TF32X3 && encoding != ELV_PARALLEL_FP16X3)
+    return set_error(ELV_EINVAL, "tc_fixup: encoding must be 7 (tf32) or 8 (fp16)");
+  if (bad_ptr(a_planes) || bad_ptr(b_planes) || bad_ptr(A) || bad_ptr(B) || bad_ptr(C) || M < 1 || N < 1 ||
+      K < 1 || lda < K || ldc < N || (!b_packed && ldb < N))
+    return set_error(ELV_EINVAL, "tc_fixup: bad arguments");
+  return tc_fixup_planes(encoding == ELV_PARALLEL_FP16X3, a_planes, b_planes, A, lda, B, ldb, b_packed != 0, C, ldc,
+                         M, N, K, (cudaStream_t)stream);
 }
 
 const char* elv_binomial_variant_name(int v) {

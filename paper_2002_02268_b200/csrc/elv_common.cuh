@@ -81,7 +81,9 @@ bool parallel_uses_packed_a(int M, int N);
 size_t tf32x3_workspace_bytes(int M, int N, int K);
 int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb,
                    void* ws, size_t ws_bytes, cudaStream_t st);
-int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+// compute = the GEMM on the prepared planes + the range-guard fix-up (reads A, B)
+int tf32x3_compute(const float* A, const float* B, int lda, int ldb, float* C, int M, int N, int K, int ldc, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
 size_t tf32x3_a_planes_bytes(int M, int K);
 size_t tf32x3_b_planes_bytes(int N, int K);
 // optional trailing arguments: the plane buffers hold `total` rows / columns
@@ -98,15 +100,24 @@ bool fp16x3_applicable(int M, int N, int K);
 size_t fp16x3_workspace_bytes(int M, int N, int K);
 int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda, int ldb, void* ws,
                    size_t ws_bytes, cudaStream_t st);
-int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+int fp16x3_compute(const float* A, const float* B, int lda, int ldb, float* C, int M, int N, int K, int ldc, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
 size_t fp16x3_a_planes_bytes(int M, int K);
 size_t fp16x3_b_planes_bytes(int N, int K);
 int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st, int total = 0,
                    int r0 = 0);
 int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st, int total = 0,
-                   int c0 = 0);
+                   int c0 = 0, bool packed = false);
 int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                        cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0);
+unsigned int* fp16x3_planes_flags(const void* buf, int total, int K);
+// Range-guard fix-up after a planes GEMM (tf32x3_gemm.cu, k_tc_fixup): the
+// rows / columns the splits marked are recomputed from the fp32 operands A
+// (rows [r0, r0+M) of the planes' operand, lda) and B (columns [c0, c0+N);
+// row-major with ldb, or packedB panels of those columns)
+int tc_fixup_planes(bool f16, const void* a_planes, const void* b_planes, const float* A, int lda, const float* B,
+                    int ldb, bool b_packed, float* C, int ldc, int M, int N, int K, cudaStream_t st, int a_total = 0,
+                    int r0 = 0, int b_total = 0, int c0 = 0);
 
 // binomial filter (stencil.cu)
 int launch_binomial(int variant, const float* img, float* out, int H, int W, int ldi, int ldo,

@@ -342,6 +342,9 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
       float* Cb = C_d + (size_t)r0 * N + c0;
       rc = f16 ? fp16x3_gemm_planes(pa, pb, Cb, nr, nc, K, N, st, M, r0, N, c0)
                : tf32x3_gemm_planes(pa, pb, Cb, nr, nc, K, N, st, M, r0, N, c0);
+      if (!rc)    // range guard: recompute marked rows / columns of this block
+        rc = tc_fixup_planes(f16, pa, pb, A_d + (size_t)r0 * K, K, B_d + c0, N, false, Cb, N, nr, nc, K, st, M, r0,
+                             N, c0);
       if (rc) return rc;
       CK(cudaEventRecord(ev_t[k], st), "record block");
       if ((rc = trace_rec(1, st))) return rc;
@@ -431,10 +434,11 @@ int elv_gemm_host(int variant, const float* A_h, const float* B_h, float* C_h, i
       have_a[i] = 1;
     }
     float* Cij = C_d + (size_t)r0 * N + c0;
-    if (variant == ELV_PARALLEL_TF32X3) {
-      rc = tf32x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st);
-    } else if (variant == ELV_PARALLEL_FP16X3) {
-      rc = fp16x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st);
+    if (variant == ELV_PARALLEL_TF32X3 || variant == ELV_PARALLEL_FP16X3) {
+      const bool f16 = variant == ELV_PARALLEL_FP16X3;
+      rc = f16 ? fp16x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st)
+               : tf32x3_gemm_planes(prep_a(i), prep_b(j), Cij, nr, nc, K, N, st);
+      if (!rc) rc = tc_fixup_planes(f16, prep_a(i), prep_b(j), Ai, K, B_d + c0, N, false, Cij, N, nr, nc, K, st);
     } else if (variant == ELV_PARALLEL && p.packed_a && parallel_uses_packed_a(nr, nc)) {
       rc = launch_parallel_packed(reinterpret_cast<const float*>(prep_a(i)),
                                   reinterpret_cast<const float*>(prep_b(j)), Cij, nr, nc, K, N, st);

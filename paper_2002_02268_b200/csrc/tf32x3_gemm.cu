@@ -1,28 +1,27 @@
 // K7: the parallel schedule's dense contraction on the 5th-generation tensor
-// cores, in fp32-accurate 3xTF32 form.
+// cores, in fp32-accurate 3xTF32 form (and K8, the same kernels on scaled
+// fp16 planes, below).
 //
 //   x = hi + lo,  hi = rna_tf32(x), lo = rna_tf32(x - hi)
-//   C = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi       (A_lo.B_lo ~ 2^-24, dropped)
+//   C = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi       (A_lo.B_lo ~ 2^-22, added for K < 512)
 //
-// accumulated in fp32 in TMEM.  The result meets the same sqrt(K)-scaled fp32
-// bound as the SIMT kernels; a single TF32 product does not.
-//
-// Pipeline (one persistent CTA per SM, 6 warps):
+// Pipeline (one persistent CTA -- or CTA pair -- per SM, 10 warps):
 //   warp 0      TMA producer: A_hi/A_lo (BM x BK) and Bt_hi/Bt_lo (BN x BK)
-//               tiles into a STAGES-deep SMEM ring (64B swizzle), mbarrier
-//               complete_tx signalling.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (kind::tf32, M=128, N=256, K=8 per instruction, 3 per k-step
-//               or 4 for short K), tcgen05.commit frees SMEM slots and
-//               publishes the accumulators.
-//   warps 2..5  epilogue: tcgen05.ld 32x32b of D_big and D_small ->
-//               C = RN(D_big + D_small) in registers -> global C.
-// Accuracy: the tensor core truncates (round-toward-zero) on every
-// accumulate; measured on B200 (scripts/tf32x3_numerics.py) a single shared
-// accumulator gives err/bound 0.13 mean / 0.7-0.96 worst at K >= 64 and up
-// to 6 at K=1, against SIMT FFMA's 0.04 at K=8192.  Separate accumulators for
-// hi.hi and the correction terms, an RN combine in the epilogue and lo.lo
-// for short K keep it inside the tau = 1 bound at every K.
+//               tiles into a STAGES-deep SMEM ring, mbarrier complete_tx.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.
+//   warps 2..9  epilogue: two warps per TMEM lane group (one per column half).
+// Accumulation in chunks: the tensor core rounds every accumulate toward
+// zero, and on one long chain that bias grows like K (measured on B200,
+// scripts/tc_numerics_r2.py: 10.9x the tau=1 bound at K=8192 on non-negative
+// inputs, profiles/r2/tc_numerics_before_chunked.jsonl).  So every k-block
+// is one chunk accumulated into a FRESH TMEM buffer (two buffers, ping-pong):
+// the correction products first (they build up at their own, 2^-11 smaller
+// scale), then hi.hi -- only KSUB truncations per chunk land on the chunk's
+// magnitude -- and the epilogue warps add the chunks into fp32 registers
+// with round-to-nearest (a blocked summation, like the SIMT kernels' RN fold
+// but over K/BK partial sums).  Draining 128 KB of TMEM per chunk and CTA
+// costs ~300 of the chunk's ~1500 MMA cycles at the measured ~420 B/clk
+// (profiles/r2/tmem_ld_bw.jsonl), overlapped with the next chunk's MMAs.
 // The split prepass (split_a / split_transpose_b below) is the packB of this
 // variant: it writes the hi/lo planes K-major, zero-padded to BK, so TMA
 // boxes and UMMA K-major descriptors apply to both operands.
@@ -40,8 +39,9 @@ namespace elv {
 namespace {
 
 constexpr int BM = 128, BK = 16;                  // BK fp32 = 64 B rows (SWIZZLE_64B)
-constexpr int NUM_THREADS = 192;
-constexpr int TMEM_COLS = 512;                    // pair kernel: D_big + D_small, 256 columns each
+constexpr int NUM_THREADS = 320;                  // 1-CTA kernel: producer, MMA, 8 epilogue warps
+constexpr int EPI_WARPS = 8;
+constexpr int TMEM_COLS = 512;                    // pair kernel: two 256-column chunk buffers
 
 // The 1-CTA kernel is templated on its N tile (256, 128 or 64): narrow tiles
 // give small problems (e.g. 1024^3: 32 tiles of 128x256 for 148 SMs) more
@@ -53,7 +53,7 @@ template <int TBN, int TBK = BK, bool F16 = false> struct OneCfg {
   static constexpr int B_TILE = TBN * ROW_BYTES;
   static constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;
   static constexpr int NST = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
-  static constexpr int TMEM = 2 * TBN;             // D_big | D_small
+  static constexpr int TMEM = 2 * TBN;             // two chunk buffers (ping-pong)
   static constexpr int SMEM = NST * STAGE + 256 + 1024;
   static constexpr int KSUB = TBK / (F16 ? 16 : 8);     // MMAs per product per stage
   static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
@@ -211,6 +211,55 @@ struct TileSched {
   }
 };
 
+// Scaled MMA: D = A.B + D * 2^-11 (scale-input-d; kind::f16 / kind::tf32,
+// sm_100a).  Used once per chunk to bring the fp16 encoding's correction
+// partial (lo planes carry 2^11) to the scale of hi.hi.
+template <bool F16>
+__device__ __forceinline__ void tc_mma_one_sc11(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc) {
+  if (F16)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p, 11;\n}\n" ::"r"(d_tmem), "l"(a_desc),
+                 "l"(b_desc), "r"(idesc), "r"(1u)
+                 : "memory");
+  else
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p, 11;\n}\n" ::"r"(d_tmem), "l"(a_desc),
+                 "l"(b_desc), "r"(idesc), "r"(1u)
+                 : "memory");
+}
+
+// Exact power-of-two unscaling of the fp16 encoding: v * 2^(e_row + e_col)
+// as two factors of the same sign of exponent, so an intermediate overflows
+// or underflows only when the result does (e_row, e_col in [-115, 113]).
+__device__ __forceinline__ int pow2_exp(float p) { return (int)((__float_as_uint(p) >> 23) & 0xffu) - 127; }
+__device__ __forceinline__ float unscale2(float v, int e) {
+  const int e1 = e >> 1, e2 = e - e1;
+  return v * __int_as_float((e1 + 127) << 23) * __int_as_float((e2 + 127) << 23);
+}
+
+// Unscale one 32-column chunk of a row (fp16 encoding): lane j holds the
+// column scale 1/t of column j (one coalesced load per warp), broadcast by
+// shuffles -- no per-element loads, few live registers.
+__device__ __forceinline__ void unscale_chunk(float* v, int er, float inv_t_lane) {
+  const int ec_lane = pow2_exp(inv_t_lane);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = unscale2(v[j], er + __shfl_sync(0xffffffffu, ec_lane, j));
+}
+
+// Epilogue drain of one chunk: this warp's NC x 32 accumulator columns added
+// (RN) into the register-resident running sums.
+template <int NC>
+__device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[NC * 32]) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + (uint32_t)(c * 32), r);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[c * 32 + q] += __uint_as_float(r[q]);
+  }
+}
+
 template <int TBN, int TBK, bool F16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
@@ -223,15 +272,15 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   constexpr int STAGE_BYTES = Cfg::STAGE;
   constexpr int B_TILE_BYTES = Cfg::B_TILE;
   constexpr int A_TILE_BYTES = Cfg::A_TILE;
-  constexpr int BK = TBK;
   constexpr int BN = TBN;
+  constexpr int NC = TBN / 64;                       // 32-column groups per epilogue warp
   constexpr uint32_t kIdesc = Cfg::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
+  uint64_t* tfull = empty + STAGES;                  // [2]: chunk in TMEM buffer b complete
+  uint64_t* tempty = tfull + 2;                      // [2]: buffer b drained by the epilogue
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -242,8 +291,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     tma_prefetch_desc(&map_ahi); tma_prefetch_desc(&map_alo);
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 4);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -271,7 +319,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], STAGE_BYTES);
-          const int k0 = kb * BK;
+          const int k0 = kb * TBK;
           tma_load_2d(&map_ahi, &full[s], st, k0, m0);
           tma_load_2d(&map_alo, &full[s], st + A_TILE_BYTES, k0, m0);
           tma_load_2d(&map_bhi, &full[s], st + 2 * A_TILE_BYTES, k0, n0);
@@ -283,19 +331,13 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      // D_big (TMEM cols [0,256)) accumulates hi.hi; D_small (cols [256,512))
-      // accumulates hi.lo + lo.hi (+ lo.lo for short K).  The tensor core
-      // rounds every accumulate toward zero, so keeping the 2^-11-smaller
-      // correction terms out of the big accumulator cuts the number of
-      // truncations that land on |C|-sized values by 3x.
+      // ---------------- MMA issuer: one chunk per k-block ----------------
       int s = 0; uint32_t ph = 0;
-      int it = 0;
-      const uint32_t d_big = tmem_base, d_small = tmem_base + (uint32_t)BN;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-        mbar_wait(&tempty[0], (uint32_t)(it & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < num_kb; ++kb) {
+      uint32_t q = 0;                                  // chunk counter (TMEM buffer q & 1)
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int kb = 0; kb < num_kb; ++kb, ++q) {
+          const uint32_t b = q & 1;
+          mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
@@ -303,68 +345,70 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           const uint64_t alo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + A_TILE_BYTES);
           const uint64_t bhi = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES);
           const uint64_t blo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+          const uint32_t d = tmem_base + b * (uint32_t)BN;
+          // corrections first, into the fresh accumulator, then hi.hi (see mma_chunk)
 #pragma unroll
-          for (int k = 0; k < Cfg::KSUB; ++k) {
-            const uint64_t koff = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along the row
-            const uint32_t acc = (kb | k) != 0;                 // 0: overwrite (first k-step)
-            tc_mma_one<F16>(d_small, ahi + koff, blo + koff, kIdesc, acc);
-            tc_mma_one<F16>(d_small, alo + koff, bhi + koff, kIdesc, 1u);
-            if (!F16 && with_lolo) tc_mma_one<F16>(d_small, alo + koff, blo + koff, kIdesc, 1u);
-            tc_mma_one<F16>(d_big, ahi + koff, bhi + koff, kIdesc, acc);
+          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, ahi + 2 * k, blo + 2 * k, kIdesc, k != 0);
+#pragma unroll
+          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, alo + 2 * k, bhi + 2 * k, kIdesc, 1u);
+          if (!F16 && with_lolo) {
+#pragma unroll
+            for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, alo + 2 * k, blo + 2 * k, kIdesc, 1u);
           }
+          if (F16) tc_mma_one_sc11<F16>(d, ahi, bhi, kIdesc);
+          else tc_mma_one<F16>(d, ahi, bhi, kIdesc, 1u);
+#pragma unroll
+          for (int k = 1; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, ahi + 2 * k, bhi + 2 * k, kIdesc, 1u);
           tc_commit(&empty[s]);                 // frees the slot when these MMAs finish
+          tc_commit(&tfull[b]);                 // chunk complete in buffer b
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        tc_commit(&tfull[0]);                   // accumulators complete
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5): C = RN(D_big + D_small) ----------------
+    // ---------------- epilogue (warps 2..9): C = RN-sum of the chunks ----------------
     const int g = warp & 3;                      // TMEM lane group this warp may access
+    const int h = (warp - 2) >> 2;               // column half
     const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    uint32_t q = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int m0, n0;
       sched.coords(t, m0, n0);
-      mbar_wait(&tfull[0], (uint32_t)(it & 1));
-      tc_fence_after();
       const int row = m0 + g * 32 + lane;
-      float* crow = C + (size_t)row * ldc;
-      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16);
+      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (BN / 2));
+      float acc[NC * 32];
+#pragma unroll
+      for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t rb[32], rs[32];
-        tmem_ld_32x32b_x32(lane_base + (uint32_t)(c * 32), rb);
-        tmem_ld_32x32b_x32(lane_base + (uint32_t)(BN + c * 32), rs);
-        float v[32];
-        const int col = n0 + c * 32;
-        if (F16) {                                 // see the pair kernel: exact power-of-two unscaling
-          const float rs_i = row < M ? __ldg(inv_s + row) : 0.f;
+      for (int kb = 0; kb < num_kb; ++kb, ++q) {
+        const uint32_t b = q & 1;
+        mbar_wait(&tfull[b], (q >> 1) & 1);
+        tc_fence_after();
+        drain_add<NC>(lane_base + b * (uint32_t)BN, acc);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+      }
+      float* crow = C + (size_t)row * ldc;
+      const int er = (F16 && row < M) ? pow2_exp(__ldg(inv_s + row)) : 0;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float tj = col + q < N ? __ldg(inv_t + col + q) : 0.f;
-            v[q] = (__uint_as_float(rb[q]) + __uint_as_float(rs[q]) * 0x1p-11f) * rs_i * tj;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
-        }
+      for (int c = 0; c < NC; ++c) {
+        const int col = n0 + h * (BN / 2) + c * 32;
+        float* v = acc + c * 32;
+        if (F16) unscale_chunk(v, er, col < N - lane ? __ldg(inv_t + col + lane) : 1.f);
         if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(crow + col + 4 * q) =
-                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(crow + col + 4 * j) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (col + q < N) crow[col + q] = v[q];
+            for (int j = 0; j < 32; ++j)
+              if (col + j < N) crow[col + j] = v[j];
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[0]);
     }
   }
 
@@ -390,7 +434,10 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 // [0] MMA: waiting tempty  [1] MMA: waiting full  [2] MMA: total
 // [3] producer: waiting empty  [4] producer: wave sync  [5] epilogue: waiting tfull
 // [6] epilogue: drain  [7] tiles
-__device__ unsigned long long g_k7_prof[512][8];
+// [5] epilogue: waiting tfull  [6] epilogue: store per tile  [8] epilogue: TMEM drain (ld + add)
+// [9] epilogue: chunks  [10] epilogue: arrive
+constexpr int K7_PROF_SLOTS = 12;
+__device__ unsigned long long g_k7_prof[512][K7_PROF_SLOTS];
 #define PROF_T(x) const long long x = clock64()
 #define PROF_ADD(i, v) prof[i] += (unsigned long long)(v)
 #else
@@ -435,8 +482,12 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Arrive on a (possibly remote) CTA's mbarrier.  Default .release.cta
+// semantics: an explicit .release.cluster costs a GPU-scope MEMBAR per call,
+// which the chunked epilogue would pay on every k-block; ordering of the
+// TMEM reads it publishes comes from tcgen05.wait::ld + fence::before_thread_sync.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst,
                                                  int c0, int c1) {
@@ -476,6 +527,21 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+template <bool F16>
+__device__ __forceinline__ void tc_mma_pair_sc11(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                 uint32_t idesc) {
+  if (F16)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p, 11;\n}\n" ::"r"(d_tmem), "l"(a_desc),
+                 "l"(b_desc), "r"(idesc), "r"(1u)
+                 : "memory");
+  else
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p, 11;\n}\n" ::"r"(d_tmem), "l"(a_desc),
+                 "l"(b_desc), "r"(idesc), "r"(1u)
+                 : "memory");
+}
+
 template <int BKT, bool F16, bool TMA_C>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
@@ -490,18 +556,19 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   constexpr int P_B_TILE = Cfg::B_TILE;
   constexpr int P_STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr uint32_t kIdescPair = Cfg::IDESC;
+  constexpr int NC = P_BN / 2 / 32;                  // 32-column groups per epilogue warp (its half)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + P_STAGES * P_STAGE_BYTES;      // 1 KB-aligned (stages are)
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + Cfg::EPI_BYTES);
   uint64_t* empty = full + P_STAGES;
-  uint64_t* tfull = empty + P_STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = empty + P_STAGES;                // [2]
+  uint64_t* tempty = tfull + 2;                      // [2] (leader's copy counts both CTAs' warps)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef ELV_K7_PROF
-  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof[K7_PROF_SLOTS] = {};
 #endif
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -514,8 +581,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
     if (TMA_C) tma_prefetch_desc(&map_c);
     for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 2 * P_EPI_WARPS);         // epilogue warps of both CTAs (leader's copy)
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * P_EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -564,19 +630,11 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           uint8_t* st = smem + s * P_STAGE_BYTES;
           const uint32_t bar = full0 + (uint32_t)(s * 8);
           const int k0 = kb * BKT;
-#ifdef ELV_K7_EXPERIMENT_NOLO
-          // tuning experiment only (wrong results): load the hi planes only, to
-          // measure how power-capped throughput responds to L2->SMEM traffic
-          if (leader) mbar_expect_tx(&full[s], P_STAGE_BYTES);
-          tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
-          tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
-#else
           if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
           tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
           tma_load_2d_pair(&map_alo, bar, st + P_A_TILE, k0, ma);
           tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
           tma_load_2d_pair(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb);
-#endif
           if (++s == P_STAGES) { s = 0; ph ^= 1; }
         }
         if (wave_ctr != nullptr) atomicAdd(wave_ctr, 1u);
@@ -584,20 +642,29 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      // ---------------- MMA issuer (leader CTA only) ----------------
+      // ---------------- MMA issuer (leader CTA only): one chunk per k-block ----------------
+      // Each k-block accumulates into a FRESH TMEM buffer (ping-pong, 2 x 256
+      // columns) that the epilogue drains into fp32 registers with
+      // round-to-nearest adds.  The tensor core rounds every accumulate
+      // toward zero; over one long chain that bias grows with K (measured:
+      // 10.9x the tau=1 bound at K=8192 on non-negative inputs,
+      // profiles/r2/tc_numerics_before_chunked.jsonl).  Within a chunk the
+      // correction products go first, so they accumulate at their own (small)
+      // scale, and the hi.hi products last: only KSUB truncations per chunk
+      // fall on the chunk's magnitude.  fp16: the lo planes carry 2^11, and
+      // the first hi.hi MMA rescales the correction partial by 2^-11
+      // (scale-input-d), so one accumulator holds the whole chunk.
       int s = 0; uint32_t ph = 0;
-      int it = 0;
-      const uint32_t d_big = tmem_base, d_small = tmem_base + (uint32_t)P_BN;
+      uint32_t q = 0;
       PROF_T(m_start);
-      for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
-        PROF_T(q0);
-        mbar_wait(&tempty[0], (uint32_t)(it & 1) ^ 1);
-        PROF_T(q1);
-        PROF_ADD(0, q1 - q0);
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         PROF_ADD(7, 1);
-        tc_fence_after();
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < num_kb; ++kb, ++q) {
+          const uint32_t b = q & 1;
+          PROF_T(q0);
+          mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
           PROF_T(f0);
+          PROF_ADD(0, f0 - q0);
           mbar_wait(&full[s], ph);
           PROF_T(f1);
           PROF_ADD(1, f1 - f0);
@@ -608,71 +675,70 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           const uint64_t alo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + P_A_TILE);
           const uint64_t bhi = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE);
           const uint64_t blo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE + P_B_TILE);
+          const uint32_t d = tmem_base + b * (uint32_t)P_BN;
 #pragma unroll
-          for (int k = 0; k < Cfg::KSUB; ++k) {
-            const uint64_t koff = (uint64_t)((k * 32) >> 4);      // 32 B of K per MMA
-            const uint32_t acc = (kb | k) != 0;
-            tc_mma_pair<F16>(d_small, ahi + koff, blo + koff, kIdescPair, acc);
-            tc_mma_pair<F16>(d_small, alo + koff, bhi + koff, kIdescPair, 1u);
-            if (!F16 && with_lolo) tc_mma_pair<F16>(d_small, alo + koff, blo + koff, kIdescPair, 1u);
-            tc_mma_pair<F16>(d_big, ahi + koff, bhi + koff, kIdescPair, acc);
+          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, ahi + 2 * k, blo + 2 * k, kIdescPair, k != 0);
+#pragma unroll
+          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, alo + 2 * k, bhi + 2 * k, kIdescPair, 1u);
+          if (!F16 && with_lolo) {
+#pragma unroll
+            for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, alo + 2 * k, blo + 2 * k, kIdescPair, 1u);
           }
+          if (F16) tc_mma_pair_sc11<F16>(d, ahi, bhi, kIdescPair);
+          else tc_mma_pair<F16>(d, ahi, bhi, kIdescPair, 1u);
+#pragma unroll
+          for (int k = 1; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, ahi + 2 * k, bhi + 2 * k, kIdescPair, 1u);
           tc_commit_pair(&empty[s]);            // frees slot s in both CTAs
+          tc_commit_pair(&tfull[b]);            // chunk ready in both CTAs
           if (++s == P_STAGES) { s = 0; ph ^= 1; }
         }
-        tc_commit_pair(&tfull[0]);              // accumulators ready in both CTAs
       }
       PROF_T(m_end);
       PROF_ADD(2, m_end - m_start);
     }
   } else {
     // ---------------- epilogue (warps 2..9, both CTAs) ----------------
+    // warp -> TMEM lane group g (rows), column half h; each thread owns one
+    // row's 128 columns as register running sums across the chunks
     const int g = warp & 3;
+    const int h = (warp - 2) >> 2;
     const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
     const uint32_t tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
-    int it = 0;
-    for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+    uint32_t q = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters) {
       int m0, n0;
       coords(t, m0, n0);
-      PROF_T(d0);
-      mbar_wait(&tfull[0], (uint32_t)(it & 1));
-      PROF_T(d1);
-      PROF_ADD(5, d1 - d0);
-      tc_fence_after();
-      // warp -> TMEM lane group g (rows), column half h; each thread owns one
-      // row and writes 128 B runs of it
-      const int h = (warp - 2) >> 2;
       const int row = m0 + (int)rank * P_BM + g * 32 + lane;
-      float* crow = C + (size_t)row * ldc;
-      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16);
-      constexpr int NCH = P_BN / 2 / 32;             // 32-column chunks per half
+      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (P_BN / 2));
+      float acc[NC * 32];
+#pragma unroll
+      for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
-        const int cc = h * NCH + c;
-        uint32_t rb[32], rs[32];
-        tmem_ld_32x32b_x32(lane_base + (uint32_t)(cc * 32), rb);
-        tmem_ld_32x32b_x32(lane_base + (uint32_t)(P_BN + cc * 32), rs);
-        if (c == NCH - 1) {
-          // this warp's accumulator columns are in registers: release TMEM
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty0);
-        }
-        float v[32];
-        const int col = n0 + cc * 32;
-        if (F16) {
-          // planes were scaled by s_i * t_j (powers of two) and lo by 2^11:
-          // C = (big + small * 2^-11) / (s_i t_j), every scaling exact
-          const float rs_i = row < M ? __ldg(inv_s + row) : 0.f;
+      for (int kb = 0; kb < num_kb; ++kb, ++q) {
+        const uint32_t b = q & 1;
+        PROF_T(c0);
+        mbar_wait(&tfull[b], (q >> 1) & 1);
+        tc_fence_after();
+        PROF_T(c1);
+        drain_add<NC>(lane_base + b * (uint32_t)P_BN, acc);
+        tc_fence_before();
+        __syncwarp();
+        PROF_T(c2);
+        if (lane == 0) mbar_arrive_cluster(tempty0 + b * 8);
+        PROF_T(c3);
+        PROF_ADD(5, c1 - c0);
+        PROF_ADD(8, c2 - c1);
+        PROF_ADD(10, c3 - c2);
+        PROF_ADD(9, 1);
+      }
+      PROF_T(d1);
+      float* crow = C + (size_t)row * ldc;
+      const int er = (F16 && row < M) ? pow2_exp(__ldg(inv_s + row)) : 0;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float tj = col + q < N ? __ldg(inv_t + col + q) : 0.f;
-            v[q] = (__uint_as_float(rb[q]) + __uint_as_float(rs[q]) * 0x1p-11f) * rs_i * tj;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(rb[q]) + __uint_as_float(rs[q]);
-        }
+      for (int c = 0; c < NC; ++c) {
+        const int col = n0 + h * (P_BN / 2) + c * 32;
+        float* v = acc + c * 32;
+        if (F16) unscale_chunk(v, er, col < N - lane ? __ldg(inv_t + col + lane) : 1.f);
         if (TMA_C) {
           // 32 x 32 chunk -> this warp's SMEM tile in the 128B-swizzled layout
           // the tensor map expects -> one bulk tensor store (clipped at M, N)
@@ -680,9 +746,9 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(tile + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(tile + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
@@ -696,13 +762,13 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
         } else if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(crow + col + 4 * q) =
-                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(crow + col + 4 * j) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (col + q < N) crow[col + q] = v[q];
+            for (int j = 0; j < 32; ++j)
+              if (col + j < N) crow[col + j] = v[j];
           }
         }
       }
@@ -712,7 +778,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   }
 #ifdef ELV_K7_PROF
   if (lane == 0 && warp <= 2 && blockIdx.x < 512)
-    for (int i = 0; i < 8; ++i) if (prof[i]) atomicAdd(&g_k7_prof[blockIdx.x][i], prof[i]);
+    for (int i = 0; i < K7_PROF_SLOTS; ++i) if (prof[i]) atomicAdd(&g_k7_prof[blockIdx.x][i], prof[i]);
 #endif
 
   if (TMA_C && warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -733,12 +799,30 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// Range guard.  The 3-product split is exact to 2^-22 only for finite
+// elements inside the encoding's window: tf32 keeps fp32's exponent range,
+// so only |x| < 2^-100 (lo would leave the normal range) and non-finite x
+// fall outside; the scaled fp16 encoding keeps an element only if its scaled
+// value is >= 2^-14 (fp16's normal range; below it hi and lo lose relative
+// precision), i.e. within 2^29 of its row / column maximum.  The split
+// kernels mark every row of A / column of B holding such an element
+// (flag = 1; zeroed first, see the callers), and k_tc_fixup recomputes the
+// marked rows and columns of C with the SIMT fp32 FMA chain.
+__device__ __forceinline__ bool tf32_out_of_window(float x) {
+  const float a = fabsf(x);
+  return !(a <= 3.402823466e38f) || (a != 0.f && a < 0x1p-100f);
+}
+__device__ __forceinline__ bool f16_out_of_window(float x, float y) {
+  const float b = fabsf(y);
+  return !(fabsf(x) <= 3.402823466e38f) || (b != 0.f && b < 0x1p-14f);
+}
+
 // One row segment of 4 k's per thread: float4 in, two float4 out (rows of A
 // are K-major already, so the planes are a padded elementwise map).  2D grid:
 // x over Kp/4, y-stride over rows -- no 64-bit division per element.
 __device__ __forceinline__ void split_a_block(const float* __restrict__ A, float* __restrict__ hi,
                                               float* __restrict__ lo, int M, int K, int lda, int Kp, bool vec,
-                                              int bx, int by, int gy) {
+                                              int bx, int by, int gy, unsigned int* __restrict__ flag) {
   const int k = (bx * 256 + threadIdx.x) * 4;
   if (k >= Kp) return;
   for (int r = by; r < M; r += gy) {
@@ -752,6 +836,8 @@ __device__ __forceinline__ void split_a_block(const float* __restrict__ A, float
       x.z = k + 2 < K ? __ldg(src + 2) : 0.f;
       x.w = k + 3 < K ? __ldg(src + 3) : 0.f;
     }
+    if (tf32_out_of_window(x.x) || tf32_out_of_window(x.y) || tf32_out_of_window(x.z) || tf32_out_of_window(x.w))
+      flag[r] = 1u;
     const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
     const float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
                                  tf32_rna(x.w - h.w));
@@ -762,8 +848,8 @@ __device__ __forceinline__ void split_a_block(const float* __restrict__ A, float
 }
 __global__ void __launch_bounds__(256)
 k_split_a(const float* __restrict__ A, float* __restrict__ hi, float* __restrict__ lo, int M, int K,
-          int lda, int Kp, bool vec) {
-  split_a_block(A, hi, lo, M, K, lda, Kp, vec, blockIdx.x, blockIdx.y, gridDim.y);
+          int lda, int Kp, bool vec, unsigned int* __restrict__ flag) {
+  split_a_block(A, hi, lo, M, K, lda, Kp, vec, blockIdx.x, blockIdx.y, gridDim.y, flag);
 }
 
 // 32x32 tiles through SMEM: reads of B rows and writes of Bt rows coalesce.
@@ -772,7 +858,7 @@ k_split_a(const float* __restrict__ A, float* __restrict__ hi, float* __restrict
 template <bool PACKED>
 __device__ __forceinline__ void split_transpose_b_block(const float* __restrict__ B, float* __restrict__ hi,
                                                         float* __restrict__ lo, int K, int N, int ldb, int Kp,
-                                                        int bx, int by) {
+                                                        int bx, int by, unsigned int* __restrict__ flag) {
   __shared__ float t[32][33];
   const int k0 = by * 32, n0 = bx * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
@@ -790,6 +876,7 @@ __device__ __forceinline__ void split_transpose_b_block(const float* __restrict_
     const int n = n0 + ty + 8 * r, k = k0 + tx;
     if (n < N && k < Kp) {
       const float x = t[tx][ty + 8 * r];
+      if (tf32_out_of_window(x)) flag[n] = 1u;
       const float h = tf32_rna(x);
       hi[(size_t)n * Kp + k] = h;
       lo[(size_t)n * Kp + k] = tf32_rna(x - h);
@@ -799,8 +886,8 @@ __device__ __forceinline__ void split_transpose_b_block(const float* __restrict_
 template <bool PACKED>
 __global__ void __launch_bounds__(256)
 k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* __restrict__ lo,
-                    int K, int N, int ldb, int Kp) {
-  split_transpose_b_block<PACKED>(B, hi, lo, K, N, ldb, Kp, blockIdx.x, blockIdx.y);
+                    int K, int N, int ldb, int Kp, unsigned int* __restrict__ flag) {
+  split_transpose_b_block<PACKED>(B, hi, lo, K, N, ldb, Kp, blockIdx.x, blockIdx.y, flag);
 }
 
 // elv_gemm's prepare for variant 7 in one launch: blocks [0, ga) split A,
@@ -808,11 +895,113 @@ k_split_transpose_b(const float* __restrict__ B, float* __restrict__ hi, float* 
 __global__ void __launch_bounds__(256)
 k_split_ab(const float* __restrict__ A, float* __restrict__ ahi, float* __restrict__ alo, int M, int lda,
            bool vecA, int gxa, int gya, const float* __restrict__ B, float* __restrict__ bhi,
-           float* __restrict__ blo, int N, int ldb, int gxb, int K, int Kp) {
+           float* __restrict__ blo, int N, int ldb, int gxb, int K, int Kp, unsigned int* __restrict__ flag_a,
+           unsigned int* __restrict__ flag_b) {
   griddep_launch_dependents();
   const int b = blockIdx.x, ga = gxa * gya;
-  if (b < ga) split_a_block(A, ahi, alo, M, K, lda, Kp, vecA, b % gxa, b / gxa, gya);
-  else split_transpose_b_block<false>(B, bhi, blo, K, N, ldb, Kp, (b - ga) % gxb, (b - ga) / gxb);
+  if (b < ga) split_a_block(A, ahi, alo, M, K, lda, Kp, vecA, b % gxa, b / gxa, gya, flag_a);
+  else split_transpose_b_block<false>(B, bhi, blo, K, N, ldb, Kp, (b - ga) % gxb, (b - ga) / gxb, flag_b);
+}
+
+// ----------------------------------------------------------------------------
+// Range-guard fix-up: the rows of A / columns of B that a split marked
+// (tf32_out_of_window / f16_out_of_window) are recomputed after the tensor-
+// core GEMM with the SIMT kernels' arithmetic -- C_ij = fmaf chain over k
+// ascending from 0, the parallel schedule's sequential fold
+// (reference interp.py:84-89, 145-148) in fp32.  One block per 64-row segment
+// of A (blocks [0, gm)) or 64-column segment of B (the rest): a segment
+// without marks returns after reading its 64 flags, so with nothing marked
+// the call is one short launch.  Marked segments work in groups of 16 rows
+// (x 256 columns per pass, 16 FMAs per B load) or 16 columns (x 256 rows,
+// A staged through SMEM so its rows are read coalesced).
+constexpr int FIX_SEG = 64, FIX_GRP = 16, FIX_T = 256, FIX_KT = 32;
+
+__device__ __forceinline__ float fix_ld_b(const float* __restrict__ B, int ldb, int packed, int K, int k, int n) {
+  return packed ? __ldg(B + ((size_t)(n >> 5) * K + k) * 32 + (n & 31)) : __ldg(B + (size_t)k * ldb + n);
+}
+
+__global__ void __launch_bounds__(FIX_T)
+k_tc_fixup(const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, int b_packed,
+           float* __restrict__ C, int ldc, int M, int N, int K, const unsigned int* __restrict__ flag_a,
+           const unsigned int* __restrict__ flag_b) {
+  __shared__ int list[FIX_SEG];
+  __shared__ int cnt;
+  __shared__ float As[FIX_T][FIX_KT + 1];
+  __shared__ float Bs[FIX_KT][FIX_GRP + 1];
+  griddep_wait();                                   // the GEMM's C (and the splits' flags) are complete
+  const int gm = (M + FIX_SEG - 1) / FIX_SEG;
+  const bool rowmode = (int)blockIdx.x < gm;
+  const int seg0 = (rowmode ? (int)blockIdx.x : (int)blockIdx.x - gm) * FIX_SEG;
+  const int lim = rowmode ? M : N;
+  const unsigned int* flag = rowmode ? flag_a : flag_b;
+  const int tid = threadIdx.x;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  if (tid < FIX_SEG && seg0 + tid < lim && __ldcg(flag + seg0 + tid) != 0u) list[atomicAdd(&cnt, 1)] = seg0 + tid;
+  __syncthreads();
+  const int n = cnt;
+  if (n == 0) return;
+  for (int g0 = 0; g0 < n; g0 += FIX_GRP) {
+    const int gn = min(FIX_GRP, n - g0);
+    if (rowmode) {
+      // rows list[g0 .. g0+gn) x all N columns, 256 columns per pass
+      for (int c0 = 0; c0 < N; c0 += FIX_T) {
+        const int col = c0 + tid;
+        float acc[FIX_GRP];
+#pragma unroll
+        for (int r = 0; r < FIX_GRP; ++r) acc[r] = 0.f;
+        for (int k0 = 0; k0 < K; k0 += FIX_KT) {
+          const int kn = min(FIX_KT, K - k0);
+#pragma unroll
+          for (int i = 0; i < FIX_GRP * FIX_KT / FIX_T; ++i) {
+            const int idx = tid + i * FIX_T, r = idx / FIX_KT, kk = idx % FIX_KT;
+            As[r][kk] = (r < gn && kk < kn) ? __ldg(A + (size_t)list[g0 + r] * lda + k0 + kk) : 0.f;
+          }
+          __syncthreads();
+          if (col < N) {
+            for (int kk = 0; kk < kn; ++kk) {
+              const float b = fix_ld_b(B, ldb, b_packed, K, k0 + kk, col);
+#pragma unroll
+              for (int r = 0; r < FIX_GRP; ++r) acc[r] = fmaf(As[r][kk], b, acc[r]);
+            }
+          }
+          __syncthreads();
+        }
+        if (col < N)
+          for (int r = 0; r < gn; ++r) C[(size_t)list[g0 + r] * ldc + col] = acc[r];
+      }
+    } else {
+      // all M rows x columns list[g0 .. g0+gn), 256 rows per pass
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int r0 = 0; r0 < M; r0 += FIX_T) {
+        const int row = r0 + tid;
+        float acc[FIX_GRP];
+#pragma unroll
+        for (int c = 0; c < FIX_GRP; ++c) acc[c] = 0.f;
+        for (int k0 = 0; k0 < K; k0 += FIX_KT) {
+          const int kn = min(FIX_KT, K - k0);
+          for (int rr = 0; rr < 32; ++rr) {           // warp w stages rows w*32 .. w*32+31, lane = k
+            const int ar = r0 + warp * 32 + rr;
+            As[warp * 32 + rr][lane] = (ar < M && lane < kn) ? __ldg(A + (size_t)ar * lda + k0 + lane) : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < FIX_GRP * FIX_KT / FIX_T; ++i) {
+            const int idx = tid + i * FIX_T, kk = idx / FIX_GRP, c = idx % FIX_GRP;
+            Bs[kk][c] = (c < gn && kk < kn) ? fix_ld_b(B, ldb, b_packed, K, k0 + kk, list[g0 + c]) : 0.f;
+          }
+          __syncthreads();
+          for (int kk = 0; kk < kn; ++kk) {
+            const float a = As[tid][kk];
+#pragma unroll
+            for (int c = 0; c < FIX_GRP; ++c) acc[c] = fmaf(a, Bs[kk][c], acc[c]);
+          }
+          __syncthreads();
+        }
+        if (row < M)
+          for (int c = 0; c < gn; ++c) C[(size_t)row * ldc + list[g0 + c]] = acc[c];
+      }
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -982,18 +1171,43 @@ static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, con
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3_pair");
 }
+// tf32 plane buffers: [hi rows x Kp | lo rows x Kp] fp32 | range-guard flags (rows u32)
+static inline size_t up128(size_t x) { return (x + 127) / 128 * 128; }
 static inline size_t planes_bytes(int rows, int K) {
-  return (size_t)(2 * (long long)rows * kpad(K)) * sizeof(float) + 128;
+  return (size_t)(2 * (long long)rows * kpad(K)) * sizeof(float) + 128 + up128((size_t)rows * 4);
 }
 static inline float* align128(const void* p) {
   return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+static inline unsigned int* planes_flags(const void* buf, int total, int K) {
+  return reinterpret_cast<unsigned int*>(align128(buf) + 2 * (size_t)total * kpad(K));
 }
 
 size_t tf32x3_a_planes_bytes(int M, int K) { return planes_bytes(M, K); }
 size_t tf32x3_b_planes_bytes(int N, int K) { return planes_bytes(N, K); }
 
+// elv_gemm workspace for variant 7 = [A planes | B planes | flags A (M) | flags B (N)]:
+// the tail keeps both operands' range-guard flags contiguous (one memset)
 size_t tf32x3_workspace_bytes(int M, int N, int K) {
-  return tf32x3_a_planes_bytes(M, K) + tf32x3_b_planes_bytes(N, K);
+  return tf32x3_a_planes_bytes(M, K) + tf32x3_b_planes_bytes(N, K) + 128 + up128((size_t)(M + N) * 4);
+}
+static unsigned int* ws_tail_flags(void* ws, int M, int N, int K) {
+  return reinterpret_cast<unsigned int*>(
+      align128(static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K) + tf32x3_b_planes_bytes(N, K)));
+}
+
+// The fix-up after a tensor-core GEMM of a row window of A planes (flags
+// flag_a[0, M)) and a column window of B planes (flag_b[0, N)); A, B are the
+// fp32 operands of the same windows (B row-major, or packedB panels).
+int tc_fixup(const float* A, int lda, const float* B, int ldb, bool b_packed, float* C, int ldc, int M, int N, int K,
+             const unsigned int* flag_a, const unsigned int* flag_b, cudaStream_t st) {
+  const long long blocks = (long long)(M + FIX_SEG - 1) / FIX_SEG + (N + FIX_SEG - 1) / FIX_SEG;
+  if (blocks <= 0) return ELV_OK;
+  if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tc_fixup: problem too large");
+  const cudaError_t e = launch_pdl(k_tc_fixup, dim3((unsigned)blocks), dim3(FIX_T), 0, st, A, lda, B, ldb,
+                                   (int)b_packed, C, ldc, M, N, K, flag_a, flag_b);
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "tc_fixup: %s", cudaGetErrorString(e));
+  return check_launch("tc_fixup");
 }
 
 
@@ -1014,10 +1228,12 @@ int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaSt
   if (total <= 0) total = M;
   float* hi = align128(a_planes) + (size_t)r0 * Kp;
   float* lo = hi + (size_t)total * Kp;
+  unsigned int* flag = planes_flags(a_planes, total, K) + r0;
+  if (cudaMemsetAsync(flag, 0, (size_t)M * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3: memset");
   int gx, gy;
   split_a_grid(M, Kp, &gx, &gy);
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
-  k_split_a<<<dim3(gx, gy), 256, 0, st>>>(A, hi, lo, M, K, lda, Kp, vec);
+  k_split_a<<<dim3(gx, gy), 256, 0, st>>>(A, hi, lo, M, K, lda, Kp, vec, flag);
   return check_launch("tf32x3_split_a");
 }
 
@@ -1027,9 +1243,11 @@ int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_p
   if (total <= 0) total = N;
   float* hi = align128(b_planes) + (size_t)c0 * Kp;
   float* lo = hi + (size_t)total * Kp;
+  unsigned int* flag = planes_flags(b_planes, total, K) + c0;
+  if (cudaMemsetAsync(flag, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3: memset");
   dim3 grid((N + 31) / 32, (Kp + 31) / 32);
-  if (packed) k_split_transpose_b<true><<<grid, 256, 0, st>>>(B, hi, lo, K, N, 0, Kp);
-  else k_split_transpose_b<false><<<grid, 256, 0, st>>>(B, hi, lo, K, N, ldb, Kp);
+  if (packed) k_split_transpose_b<true><<<grid, 256, 0, st>>>(B, hi, lo, K, N, 0, Kp, flag);
+  else k_split_transpose_b<false><<<grid, 256, 0, st>>>(B, hi, lo, K, N, ldb, Kp, flag);
   return check_launch("tf32x3_split_b");
 }
 
@@ -1138,14 +1356,33 @@ int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   const long long blocks = (long long)gxa * gya + (long long)gxb * gyb;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tf32x3: problem too large for one split launch");
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
-  k_split_ab<<<(unsigned)blocks, 256, 0, st>>>(A, ahi, alo, M, lda, vec, gxa, gya, B, bhi, blo, N, ldb, gxb, K, Kp);
+  unsigned int* flags = ws_tail_flags(ws, M, N, K);
+  if (cudaMemsetAsync(flags, 0, (size_t)(M + N) * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3: memset");
+  k_split_ab<<<(unsigned)blocks, 256, 0, st>>>(A, ahi, alo, M, lda, vec, gxa, gya, B, bhi, blo, N, ldb, gxb, K, Kp,
+                                               flags, flags + M);
   return check_launch("tf32x3_split_ab");
 }
 
-int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+int tf32x3_compute(const float* A, const float* B, int lda, int ldb, float* C, int M, int N, int K, int ldc, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
   if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
-  return tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
+  const int rc = tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
+  if (rc) return rc;
+  const unsigned int* flags = ws_tail_flags(ws, M, N, K);
+  return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, flags, flags + M, st);
+}
+
+// The fix-up of a planes-API GEMM (row window [r0, r0+M) of A planes holding
+// a_total rows, column window [c0, c0+N) of B planes holding b_total)
+int tc_fixup_planes(bool f16, const void* a_planes, const void* b_planes, const float* A, int lda, const float* B,
+                    int ldb, bool b_packed, float* C, int ldc, int M, int N, int K, cudaStream_t st, int a_total,
+                    int r0, int b_total, int c0) {
+  if (a_total <= 0) a_total = M;
+  if (b_total <= 0) b_total = N;
+  const unsigned int* fa = (f16 ? fp16x3_planes_flags(a_planes, a_total, K) : planes_flags(a_planes, a_total, K)) + r0;
+  const unsigned int* fb = (f16 ? fp16x3_planes_flags(b_planes, b_total, K) : planes_flags(b_planes, b_total, K)) + c0;
+  return tc_fixup(A, lda, B, ldb, b_packed, C, ldc, M, N, K, fa, fb, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1158,9 +1395,12 @@ int tf32x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_b
 // lands in [2^14, 2^15), and lo by 2^11 so it does not underflow:
 //   a s_i = hi + lo / 2^11 (+ 2^-22 |a s_i|),  hi, lo in fp16
 //   C_ij = (hi.hi + 2^-11 (hi.lo + lo.hi)) / (s_i t_j)       (exact scalings)
-// Elements more than ~2^28 below their row / column maximum lose relative
-// precision to fp16 subnormals; against the per-element bound (which sums
-// |a||b| over the row) that is below 2^-50 of the bound's scale.
+// Elements more than 2^29 below their row / column maximum would lose
+// relative precision to fp16 subnormals; the range guard (f16_out_of_window)
+// marks their rows / columns for the SIMT fix-up.  The scale's exponent is
+// clamped only on the low side (rows with a maximum below 2^-101 keep a
+// finite 2^115 scale; their small elements are then guarded): s and 1/s stay
+// normal powers of two for every finite maximum, up to 2^128.
 constexpr int K16_ALIGN = 64;                     // 128 B rows of fp16 per stage
 static inline long long kpad16(int K) { return round_up(K, K16_ALIGN); }
 
@@ -1168,7 +1408,7 @@ __device__ __forceinline__ void pow2_scale(float m, float* s, float* inv) {
   if (!(m > 0.f) || !isfinite(m)) { *s = 1.f; *inv = 1.f; return; }
   int e;
   frexpf(m, &e);                                  // m = f 2^e, f in [0.5, 1)
-  e = max(-100, min(100, e));
+  e = max(-100, e);                               // e <= 128 for finite m
   *s = ldexpf(1.f, 15 - e);                        // m s in [2^14, 2^15)
   *inv = ldexpf(1.f, e - 15);
 }
@@ -1176,18 +1416,29 @@ __device__ __forceinline__ void pow2_scale(float m, float* s, float* inv) {
 // column maxima of B (K x N row-major): a 64-row slab per block, one column
 // per thread, combined with an integer atomicMax on the (non-negative) bits
 constexpr int COLMAX_SLAB = 64;
+// B element (k, n): row-major with ldb, or (PACKED) packedB panels
+// [N/32][K][32] (elv_pack_b layout: the multi-GPU broadcast unit)
+template <bool PACKED>
+__device__ __forceinline__ float ld_b_elem(const float* __restrict__ B, int K, int ldb, int k, int n) {
+  return PACKED ? __ldg(B + ((size_t)(n >> 5) * K + k) * 32 + (n & 31)) : __ldg(B + (size_t)k * ldb + n);
+}
+template <bool PACKED = false>
 __device__ __forceinline__ void col_max_slab(const float* __restrict__ B, int K, int N, int ldb, int bx, int by,
-                                             unsigned int* __restrict__ maxbits, int slab = COLMAX_SLAB) {
+                                             unsigned int* __restrict__ maxbits, unsigned int* __restrict__ flag,
+                                             int slab = COLMAX_SLAB) {
   const int j = bx * 256 + threadIdx.x;
   if (j >= N) return;
+  if (by == 0) flag[j] = 0u;                      // range-guard flags, set by the split-transpose that follows
   const int k0 = by * slab, k1 = min(K, k0 + slab);
   float m = 0.f;
-  for (int k = k0; k < k1; ++k) m = fmaxf(m, fabsf(__ldg(B + (size_t)k * ldb + j)));
+  for (int k = k0; k < k1; ++k) m = fmaxf(m, fabsf(ld_b_elem<PACKED>(B, K, ldb, k, j)));
   atomicMax(maxbits + j, __float_as_uint(m));
 }
+template <bool PACKED>
 __global__ void __launch_bounds__(256)
-k16_col_max(const float* __restrict__ B, int K, int N, int ldb, unsigned int* __restrict__ maxbits) {
-  col_max_slab(B, K, N, ldb, blockIdx.x, blockIdx.y, maxbits);
+k16_col_max(const float* __restrict__ B, int K, int N, int ldb, unsigned int* __restrict__ maxbits,
+            unsigned int* __restrict__ flag) {
+  col_max_slab<PACKED>(B, K, N, ldb, blockIdx.x, blockIdx.y, maxbits, flag);
 }
 
 __device__ __forceinline__ void split16(float x, __half* hi, __half* lo) {
@@ -1201,7 +1452,7 @@ __device__ __forceinline__ void split16(float x, __half* hi, __half* lo) {
 // block, then scaled and split (row scale fused with the split).
 __device__ __forceinline__ void split_a_row(const float* __restrict__ A, int K, int lda, int Kp, int r,
                                             float* __restrict__ s, float* __restrict__ inv, __half* __restrict__ hi,
-                                            __half* __restrict__ lo) {
+                                            __half* __restrict__ lo, unsigned int* __restrict__ flag) {
   __shared__ float red[8];
   const float* row = A + (size_t)r * lda;
   float m = 0.f;
@@ -1218,19 +1469,26 @@ __device__ __forceinline__ void split_a_row(const float* __restrict__ A, int K, 
   if (threadIdx.x == 0) { s[r] = sc; inv[r] = iv; }
   __half2* h2 = reinterpret_cast<__half2*>(hi + (size_t)r * Kp);
   __half2* l2 = reinterpret_cast<__half2*>(lo + (size_t)r * Kp);
+  bool bad = false;
   for (int k2 = threadIdx.x; k2 < Kp / 2; k2 += 256) {       // second read hits L1/L2
     const int k = 2 * k2;
+    const float x0 = k < K ? __ldg(row + k) : 0.f, x1 = k + 1 < K ? __ldg(row + k + 1) : 0.f;
+    const float y0 = x0 * sc, y1 = x1 * sc;
+    bad |= f16_out_of_window(x0, y0) || f16_out_of_window(x1, y1);
     __half a0, a1, b0, b1;
-    split16(k < K ? __ldg(row + k) * sc : 0.f, &a0, &b0);
-    split16(k + 1 < K ? __ldg(row + k + 1) * sc : 0.f, &a1, &b1);
+    split16(y0, &a0, &b0);
+    split16(y1, &a1, &b1);
     h2[k2] = __halves2half2(a0, a1);
     l2[k2] = __halves2half2(b0, b1);
   }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) flag[r] = bad ? 1u : 0u;
 }
 __global__ void __launch_bounds__(256)
 k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
-                 float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo) {
-  split_a_row(A, K, lda, Kp, blockIdx.x, s, inv, hi, lo);
+                 float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo,
+                 unsigned int* __restrict__ flag) {
+  split_a_row(A, K, lda, Kp, blockIdx.x, s, inv, hi, lo, flag);
 }
 
 // Short rows (K <= K16_WARP_ROW_K): one WARP per row -- the maximum is a
@@ -1240,7 +1498,8 @@ k16_split_a_rows(const float* __restrict__ A, int M, int K, int lda, int Kp, flo
 constexpr int K16_WARP_ROW_K = 2048;
 __device__ __forceinline__ void split_a_row_warp(const float* __restrict__ A, int M, int K, int lda, int Kp, int r,
                                                  float* __restrict__ s, float* __restrict__ inv,
-                                                 __half* __restrict__ hi, __half* __restrict__ lo) {
+                                                 __half* __restrict__ hi, __half* __restrict__ lo,
+                                                 unsigned int* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
   if (r >= M) return;
   const float* row = A + (size_t)r * lda;
@@ -1253,14 +1512,20 @@ __device__ __forceinline__ void split_a_row_warp(const float* __restrict__ A, in
   if (lane == 0) { s[r] = sc; inv[r] = iv; }
   __half2* h2 = reinterpret_cast<__half2*>(hi + (size_t)r * Kp);
   __half2* l2 = reinterpret_cast<__half2*>(lo + (size_t)r * Kp);
+  bool bad = false;
   for (int k2 = lane; k2 < Kp / 2; k2 += 32) {
     const int k = 2 * k2;
+    const float x0 = k < K ? __ldg(row + k) : 0.f, x1 = k + 1 < K ? __ldg(row + k + 1) : 0.f;
+    const float y0 = x0 * sc, y1 = x1 * sc;
+    bad |= f16_out_of_window(x0, y0) || f16_out_of_window(x1, y1);
     __half a0, a1, b0, b1;
-    split16(k < K ? __ldg(row + k) * sc : 0.f, &a0, &b0);
-    split16(k + 1 < K ? __ldg(row + k + 1) * sc : 0.f, &a1, &b1);
+    split16(y0, &a0, &b0);
+    split16(y1, &a1, &b1);
     h2[k2] = __halves2half2(a0, a1);
     l2[k2] = __halves2half2(b0, b1);
   }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) flag[r] = bad ? 1u : 0u;
 }
 
 // The same warp-per-row split with the row held in registers: each lane
@@ -1271,7 +1536,8 @@ __device__ __forceinline__ void split_a_row_warp(const float* __restrict__ A, in
 constexpr int K16_VEC_CHUNKS = K16_WARP_ROW_K / 128;
 __device__ __forceinline__ void split_a_row_warp_vec(const float* __restrict__ A, int M, int K, int lda, int Kp,
                                                      int r, float* __restrict__ s, float* __restrict__ inv,
-                                                     __half* __restrict__ hi, __half* __restrict__ lo) {
+                                                     __half* __restrict__ hi, __half* __restrict__ lo,
+                                                     unsigned int* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
   if (r >= M) return;
   const float4* row = reinterpret_cast<const float4*>(A + (size_t)r * lda);
@@ -1288,15 +1554,19 @@ __device__ __forceinline__ void split_a_row_warp_vec(const float* __restrict__ A
   float sc, iv;
   pow2_scale(m, &sc, &iv);
   if (lane == 0) { s[r] = sc; inv[r] = iv; }
+  bool bad = false;
 #pragma unroll
   for (int c = 0; c < K16_VEC_CHUNKS; ++c) {
     const int k = c * 128 + lane * 4;
     if (k < Kp) {
+      const float4 y = make_float4(v[c].x * sc, v[c].y * sc, v[c].z * sc, v[c].w * sc);
+      bad |= f16_out_of_window(v[c].x, y.x) || f16_out_of_window(v[c].y, y.y) ||
+             f16_out_of_window(v[c].z, y.z) || f16_out_of_window(v[c].w, y.w);
       __half h[4], l[4];
-      split16(v[c].x * sc, &h[0], &l[0]);
-      split16(v[c].y * sc, &h[1], &l[1]);
-      split16(v[c].z * sc, &h[2], &l[2]);
-      split16(v[c].w * sc, &h[3], &l[3]);
+      split16(y.x, &h[0], &l[0]);
+      split16(y.y, &h[1], &l[1]);
+      split16(y.z, &h[2], &l[2]);
+      split16(y.w, &h[3], &l[3]);
       const __half2 h01 = __halves2half2(h[0], h[1]), h23 = __halves2half2(h[2], h[3]);
       const __half2 l01 = __halves2half2(l[0], l[1]), l23 = __halves2half2(l[2], l[3]);
       *reinterpret_cast<uint2*>(hi + (size_t)r * Kp + k) =
@@ -1305,6 +1575,8 @@ __device__ __forceinline__ void split_a_row_warp_vec(const float* __restrict__ A
           make_uint2(*reinterpret_cast<const unsigned int*>(&l01), *reinterpret_cast<const unsigned int*>(&l23));
     }
   }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) flag[r] = bad ? 1u : 0u;
 }
 
 // elv_gemm's variant-8 prepare in one launch: blocks [0, ga) scale and split
@@ -1313,16 +1585,18 @@ __device__ __forceinline__ void split_a_row_warp_vec(const float* __restrict__ A
 __global__ void __launch_bounds__(256)
 k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
             float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo, const float* __restrict__ B,
-            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits, int warp_rows, int slab) {
+            int N, int ldb, int gxb, unsigned int* __restrict__ maxbits, int warp_rows, int slab,
+            unsigned int* __restrict__ flag_a, unsigned int* __restrict__ flag_b) {
   griddep_launch_dependents();                    // the split-transpose may stage its B tiles meanwhile
   const int b = blockIdx.x;
   const int ga = warp_rows ? (M + 7) / 8 : M;
   if (b < ga) {
-    if (warp_rows == 2) split_a_row_warp_vec(A, M, K, lda, Kp, b * 8 + (threadIdx.x >> 5), s, inv, hi, lo);
-    else if (warp_rows) split_a_row_warp(A, M, K, lda, Kp, b * 8 + (threadIdx.x >> 5), s, inv, hi, lo);
-    else split_a_row(A, K, lda, Kp, b, s, inv, hi, lo);
+    const int r = b * 8 + (threadIdx.x >> 5);
+    if (warp_rows == 2) split_a_row_warp_vec(A, M, K, lda, Kp, r, s, inv, hi, lo, flag_a);
+    else if (warp_rows) split_a_row_warp(A, M, K, lda, Kp, r, s, inv, hi, lo, flag_a);
+    else split_a_row(A, K, lda, Kp, b, s, inv, hi, lo, flag_a);
   } else {
-    col_max_slab(B, K, N, ldb, (b - ga) % gxb, (b - ga) / gxb, maxbits, slab);
+    col_max_slab(B, K, N, ldb, (b - ga) % gxb, (b - ga) / gxb, maxbits, flag_b, slab);
   }
 }
 
@@ -1330,10 +1604,11 @@ k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* _
 // tiles: coalesced 128 B reads along B's rows, 128 B half2 writes along the
 // planes' rows.  Each block turns its 32 columns' maxima (k16_col_max) into
 // scales once; the blocks of the first k-tile publish 1/t_j.
+template <bool PACKED>
 __global__ void __launch_bounds__(256)
 k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp,
                       const unsigned int* __restrict__ maxbits, __half* __restrict__ hi, __half* __restrict__ lo,
-                      float* __restrict__ inv_t) {
+                      float* __restrict__ inv_t, unsigned int* __restrict__ flag) {
   __shared__ float tile[64][33];
   __shared__ float scale[32];
   griddep_launch_dependents();                    // the GEMM waits (griddepcontrol.wait) for our completion
@@ -1342,7 +1617,7 @@ k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp
 #pragma unroll
   for (int r = 0; r < 8; ++r) {                   // B is an input: staged before the maxima are ready
     const int k = k0 + ty + 8 * r, n = n0 + tx;
-    tile[ty + 8 * r][tx] = (k < K && n < N) ? __ldg(B + (size_t)k * ldb + n) : 0.f;
+    tile[ty + 8 * r][tx] = (k < K && n < N) ? ld_b_elem<PACKED>(B, K, ldb, k, n) : 0.f;
   }
   griddep_wait();                                 // column maxima from k16_prep_ab (PDL launch)
   if (ty == 0) {
@@ -1357,9 +1632,12 @@ k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp
     const int nl = ty + 8 * r, n = n0 + nl, k = k0 + 2 * tx;
     if (n < N && k < Kp) {
       const float sc = scale[nl];
+      const float x0 = tile[2 * tx][nl], x1 = tile[2 * tx + 1][nl];
+      const float y0 = x0 * sc, y1 = x1 * sc;
+      if (f16_out_of_window(x0, y0) || f16_out_of_window(x1, y1)) flag[n] = 1u;   // zeroed by the maxima pass
       __half a0, a1, b0, b1;
-      split16(tile[2 * tx][nl] * sc, &a0, &b0);
-      split16(tile[2 * tx + 1][nl] * sc, &a1, &b1);
+      split16(y0, &a0, &b0);
+      split16(y1, &a1, &b1);
       *reinterpret_cast<__half2*>(hi + (size_t)n * Kp + k) = __halves2half2(a0, a1);
       *reinterpret_cast<__half2*>(lo + (size_t)n * Kp + k) = __halves2half2(b0, b1);
     }
@@ -1368,47 +1646,55 @@ k16_split_transpose_b(const float* __restrict__ B, int K, int N, int ldb, int Kp
 
 // Plane buffers of the fp16 encoding (the unit the C ABI, the row-shard
 // broadcast and the host pipeline move around):
-//   A planes = [hi M x Kp | lo M x Kp] fp16 | s (M f32) | 1/s (M f32)
-//   B planes = [hi N x Kp | lo N x Kp] fp16 | t (N f32; max bits first) | 1/t (N f32)
-static inline size_t up128(size_t x) { return (x + 127) / 128 * 128; }
+//   A planes = [hi M x Kp | lo M x Kp] fp16 | s (M f32) | 1/s (M f32) | guard flags (M u32)
+//   B planes = [hi N x Kp | lo N x Kp] fp16 | t (N f32; max bits first) | 1/t (N f32) | flags (N u32)
 size_t fp16x3_a_planes_bytes(int M, int K) {
-  return 128 + up128((size_t)M * kpad16(K) * 2) * 2 + up128((size_t)M * 4) * 2;
+  return 128 + up128((size_t)M * kpad16(K) * 2) * 2 + up128((size_t)M * 4) * 3;
 }
 size_t fp16x3_b_planes_bytes(int N, int K) { return fp16x3_a_planes_bytes(N, K); }
 struct Planes16 {
   __half *hi, *lo;
   float* s;            // A: s_i ; B: max bits (as u32)
   float* inv;          // 1/s_i or 1/t_j
+  unsigned int* flag;  // range guard
 };
 static Planes16 planes16(const void* buf, int rows, int K) {
   uint8_t* b = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(buf) + 127) & ~uintptr_t(127));
   const size_t plane = up128((size_t)rows * kpad16(K) * 2), vec = up128((size_t)rows * 4);
   return {reinterpret_cast<__half*>(b), reinterpret_cast<__half*>(b + plane),
-          reinterpret_cast<float*>(b + 2 * plane), reinterpret_cast<float*>(b + 2 * plane + vec)};
+          reinterpret_cast<float*>(b + 2 * plane), reinterpret_cast<float*>(b + 2 * plane + vec),
+          reinterpret_cast<unsigned int*>(b + 2 * plane + 2 * vec)};
 }
+unsigned int* fp16x3_planes_flags(const void* buf, int total, int K) { return planes16(buf, total, K).flag; }
 
 // rows [r0, r0 + n) of plane buffers that hold `total` rows (see tf32x3_split_a)
 static Planes16 planes16_at(const void* buf, int n, int K, int total, int r0) {
   Planes16 P = planes16(buf, total > 0 ? total : n, K);
   const size_t off = (size_t)r0 * kpad16(K);
-  return {P.hi + off, P.lo + off, P.s + r0, P.inv + r0};
+  return {P.hi + off, P.lo + off, P.s + r0, P.inv + r0, P.flag + r0};
 }
 
 int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaStream_t st, int total, int r0) {
   const Planes16 P = planes16_at(a_planes, M, K, total, r0);
   const int Kp = (int)kpad16(K);
-  k16_split_a_rows<<<M, 256, 0, st>>>(A, M, K, lda, Kp, P.s, P.inv, P.hi, P.lo);
+  k16_split_a_rows<<<M, 256, 0, st>>>(A, M, K, lda, Kp, P.s, P.inv, P.hi, P.lo, P.flag);
   return check_launch("fp16x3_split_a");
 }
 
-int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st, int total, int c0) {
+int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st, int total, int c0,
+                   bool packed) {
   const Planes16 P = planes16_at(b_planes, N, K, total, c0);
   const int Kp = (int)kpad16(K);
   unsigned int* tmax = reinterpret_cast<unsigned int*>(P.s);
   if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
-  k16_col_max<<<dim3((N + 255) / 256, (K + COLMAX_SLAB - 1) / COLMAX_SLAB), 256, 0, st>>>(B, K, N, ldb, tmax);
-  k16_split_transpose_b<<<dim3((N + 31) / 32, (Kp + 63) / 64), 256, 0, st>>>(B, K, N, ldb, Kp, tmax, P.hi, P.lo,
-                                                                             P.inv);
+  const dim3 gm((N + 255) / 256, (K + COLMAX_SLAB - 1) / COLMAX_SLAB), gs((N + 31) / 32, (Kp + 63) / 64);
+  if (packed) {
+    k16_col_max<true><<<gm, 256, 0, st>>>(B, K, N, 0, tmax, P.flag);
+    k16_split_transpose_b<true><<<gs, 256, 0, st>>>(B, K, N, 0, Kp, tmax, P.hi, P.lo, P.inv, P.flag);
+  } else {
+    k16_col_max<false><<<gm, 256, 0, st>>>(B, K, N, ldb, tmax, P.flag);
+    k16_split_transpose_b<false><<<gs, 256, 0, st>>>(B, K, N, ldb, Kp, tmax, P.hi, P.lo, P.inv, P.flag);
+  }
   return check_launch("fp16x3_split_b");
 }
 
@@ -1475,28 +1761,32 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   const long long blocks = ga + (long long)gxb * gyb;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
   k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax,
-                                                warp_rows, slab);
+                                                warp_rows, slab, PA.flag, PB.flag);
   if (cudaPeekAtLastError() != cudaSuccess) return check_launch("fp16x3_prepare");
-  const cudaError_t e = launch_pdl(k16_split_transpose_b, dim3((N + 31) / 32, (Kp + 63) / 64), dim3(256), 0, st, B, K,
-                                   N, ldb, Kp, (const unsigned int*)tmax, PB.hi, PB.lo, PB.inv);
+  const cudaError_t e = launch_pdl(k16_split_transpose_b<false>, dim3((N + 31) / 32, (Kp + 63) / 64), dim3(256), 0, st, B, K,
+                                   N, ldb, Kp, (const unsigned int*)tmax, PB.hi, PB.lo, PB.inv, PB.flag);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3_prepare: %s", cudaGetErrorString(e));
   return check_launch("fp16x3_prepare");
 }
 
-int fp16x3_compute(float* C, int M, int N, int K, int ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (!fp16x3_applicable(M, N, K)) return tf32x3_compute(C, M, N, K, ldc, ws, ws_bytes, st);
+int fp16x3_compute(const float* A, const float* B, int lda, int ldb, float* C, int M, int N, int K, int ldc, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (!fp16x3_applicable(M, N, K)) return tf32x3_compute(A, B, lda, ldb, C, M, N, K, ldc, ws, ws_bytes, st);
   if (ws == nullptr || ws_bytes < fp16x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
-  return fp16x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
+  void* bp = static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K);
+  const int rc = fp16x3_gemm_planes(ws, bp, C, M, N, K, ldc, st);
+  if (rc) return rc;
+  return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, planes16(ws, M, K).flag, planes16(bp, N, K).flag, st);
 }
 
 }  // namespace elv
 
 #ifdef ELV_K7_PROF
-extern "C" int elv_debug_k7_prof(unsigned long long* host, int reset) {
+extern "C" int elv_debug_k7_prof(unsigned long long* host, int reset) {   // host: [512][K7_PROF_SLOTS]
   cudaMemcpyFromSymbol(host, elv::g_k7_prof, sizeof(elv::g_k7_prof));
   if (reset) {
-    static unsigned long long zeros[512][8];
+    static unsigned long long zeros[512][elv::K7_PROF_SLOTS];
     cudaMemcpyToSymbol(elv::g_k7_prof, zeros, sizeof(zeros));
   }
   return (int)cudaGetLastError();

@@ -119,8 +119,10 @@ def term_shape(term):
             ty = S().typecheck.typecheck(term)
         except S().typecheck.TypeError_ as e:
             raise EvalError(f"no B200 kernel for term: {e}") from None
-        da, _ = dims(ty.arg)
-        db, _ = dims(ty.res.arg)
+        da, _ = dims(ty.arg) if hasattr(ty, "arg") else ([], None)
+        db, _ = dims(ty.res.arg) if hasattr(ty, "res") and hasattr(ty.res, "arg") else ([], None)
+        if len(da) != 2 or len(db) != 2:
+            raise EvalError("no B200 kernel for term: not a matrix-matrix program")
     if da[1] != db[0]:
         raise EvalError(f"no B200 kernel for term: inner sizes {da[1]} != {db[0]}")
     return da[0], db[1], da[1]

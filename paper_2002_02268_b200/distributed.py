@@ -112,10 +112,14 @@ class PipelinedRowShardGemm:
       all      : broadcast(P_c) on NCCL's stream (async, issued in order)
       all      : wait(P_c) -> C[:, chunk c] = A_shard . B[:, chunk c]
                  SIMT (variant 6): elv_gemm_prepacked on the packed chunk
-                 3xTF32 (variant 7): split_b_packed(P_c) on a side stream as
-                 soon as P_c lands (overlapping the GEMM of chunk c-1), then
-                 gemm_planes; A's hi/lo planes are made once per step while
-                 chunk 0 is in flight
+                 3xTF32 / 3xFP16 (variants 7 / 8): split_b_packed(P_c) on a
+                 side stream as soon as P_c lands (overlapping the GEMM of
+                 chunk c-1), then gemm_planes + the range-guard fix-up
+                 (elv_tc_fixup, which reads the fp32 chunk P_c); A's planes
+                 are made once per step while chunk 0 is in flight.  Every
+                 rank receives fp32 packedB -- the same 4 B per element as
+                 fp16 hi/lo planes, half the tf32 planes' -- so every rank
+                 can recompute guarded columns.
     The first chunk is half the size of the others (nothing hides its
     broadcast); with 4 chunks and N = 32768 the rest are 37 units of 256
     columns, i.e. 16*37 = 592 = 8 full waves of 74 pair tiles per GEMM at 8
@@ -142,28 +146,19 @@ class PipelinedRowShardGemm:
         if self.variant == 8 and not all(self.lib.elv_fp16x3_applicable(max(M, 1), n1 - n0, K)
                                          for n0, n1 in self.chunks):
             self.variant = 7                        # chunk GEMMs too small for the fp16 encoding
-        self.prep = torch.cuda.Stream(device) if self.variant == 7 else None
-        if self.variant == 8:
-            # rank src prepares each chunk's scaled fp16 planes and broadcasts
-            # them (4 B per element, as packed fp32 would be): no split on the
-            # receivers
-            self.a_planes = torch.empty(self.lib.elv_fp16x3_a_planes_bytes(max(M, 1), K), device=device,
-                                        dtype=torch.uint8)
-            self.b_planes = [torch.empty(self.lib.elv_fp16x3_b_planes_bytes(n1 - n0, K), device=device,
-                                         dtype=torch.uint8) for n0, n1 in self.chunks]
-            # per step: (src) column max + split per chunk; A split; one GEMM per chunk
-            self.launches = (2 * len(self.chunks) if self.rank == src else 0) + 1 + len(self.chunks)
-            return
+        tc = self.variant in (7, 8)
+        self.prep = torch.cuda.Stream(device) if tc else None
         self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
-        if self.variant == 7:
-            self.a_planes = torch.empty(self.lib.elv_tf32x3_a_planes_bytes(max(M, 1), K),
-                                        device=device, dtype=torch.uint8)
-            self.b_planes = [torch.empty(self.lib.elv_tf32x3_b_planes_bytes(n1 - n0, K),
-                                         device=device, dtype=torch.uint8) for n0, n1 in self.chunks]
-        # launches per step on this rank: pack (src only) + split_a + per chunk (split_b + gemm | gemm)
-        per_chunk = 2 if self.variant == 7 else 1
-        self.launches = (len(self.chunks) if self.rank == src else 0) + \
-            (1 if self.variant == 7 else 0) + per_chunk * len(self.chunks)
+        if tc:
+            pa = self.lib.elv_fp16x3_a_planes_bytes if self.variant == 8 else self.lib.elv_tf32x3_a_planes_bytes
+            pb = self.lib.elv_fp16x3_b_planes_bytes if self.variant == 8 else self.lib.elv_tf32x3_b_planes_bytes
+            self.a_planes = torch.empty(pa(max(M, 1), K), device=device, dtype=torch.uint8)
+            self.b_planes = [torch.empty(pb(n1 - n0, K), device=device, dtype=torch.uint8) for n0, n1 in self.chunks]
+        # kernels per step on this rank: pack (src only) + split_a + per chunk
+        # (split_b [fp16: column maxima + split] + gemm + fix-up | gemm)
+        per_chunk = (4 if self.variant == 8 else 3) if tc else 1
+        self.launches = (len(self.chunks) if self.rank == src else 0) + (1 if tc else 0) + \
+            per_chunk * len(self.chunks)
 
     def _panel(self, n0: int) -> torch.Tensor:
         return self.P[(n0 // 32) * self.K * 32:]
@@ -177,8 +172,6 @@ class PipelinedRowShardGemm:
         recorded after it (to start that chunk's D2H)."""
         lib, K, N, st = self.lib, self.K, self.N, self.stream.cuda_stream
         M = A_shard.shape[0]
-        if self.variant == 8:
-            return self._step_fp16(A_shard, B, C_shard, b_ready, a_ready, chunk_done)
         works = []
         with torch.cuda.stream(self.stream):
             for c, (n0, n1) in enumerate(self.chunks):
@@ -198,7 +191,11 @@ class PipelinedRowShardGemm:
                     if w is not None:
                         w.wait()
                 return C_shard
-            if self.variant == 7:
+            if self.variant in (7, 8):
+                f16 = self.variant == 8
+                split_b = lib.elv_fp16x3_split_b_packed if f16 else lib.elv_tf32x3_split_b_packed
+                split_a = lib.elv_fp16x3_split_a if f16 else lib.elv_tf32x3_split_a
+                gemm = lib.elv_fp16x3_gemm_planes if f16 else lib.elv_tf32x3_gemm_planes
                 # side stream: split each packed chunk as soon as it lands (after
                 # the previous step's GEMMs are done with the plane buffers)
                 self.prep.wait_stream(self.stream)
@@ -208,20 +205,22 @@ class PipelinedRowShardGemm:
                     for (n0, n1), w, bp in zip(self.chunks, works, self.b_planes):
                         if w is not None:
                             w.wait()                # the prep stream waits for chunk c
-                        self._check(lib.elv_tf32x3_split_b_packed(self._panel(n0).data_ptr(), K, n1 - n0,
-                                                                  bp.data_ptr(), pst), "split_b_packed")
+                        self._check(split_b(self._panel(n0).data_ptr(), K, n1 - n0, bp.data_ptr(), pst),
+                                    "split_b_packed")
                         ev = torch.cuda.Event()
                         ev.record(self.prep)
                         ready.append(ev)
                 if a_ready is not None:
                     self.stream.wait_event(a_ready)
-                self._check(lib.elv_tf32x3_split_a(A_shard.data_ptr(), M, K, A_shard.stride(0),
-                                                   self.a_planes.data_ptr(), st), "split_a")
+                ap = self.a_planes.data_ptr()
+                self._check(split_a(A_shard.data_ptr(), M, K, A_shard.stride(0), ap, st), "split_a")
                 for c, ((n0, n1), bp, ev) in enumerate(zip(self.chunks, self.b_planes, ready)):
                     self.stream.wait_event(ev)
-                    self._check(lib.elv_tf32x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(),
-                                                           C_shard.data_ptr() + 4 * n0, M, n1 - n0, K,
-                                                           C_shard.stride(0), st), "gemm_planes")
+                    Cc = C_shard.data_ptr() + 4 * n0
+                    self._check(gemm(ap, bp.data_ptr(), Cc, M, n1 - n0, K, C_shard.stride(0), st), "gemm_planes")
+                    self._check(lib.elv_tc_fixup(self.variant, ap, bp.data_ptr(), A_shard.data_ptr(),
+                                                 A_shard.stride(0), self._panel(n0).data_ptr(), 0, 1, Cc,
+                                                 C_shard.stride(0), M, n1 - n0, K, st), "tc_fixup")
                     self._done(chunk_done, c, n0, n1)
                 return C_shard
             if a_ready is not None:
@@ -232,37 +231,6 @@ class PipelinedRowShardGemm:
                 self._check(lib.elv_gemm_prepacked(self.variant, A_shard.data_ptr(), self._panel(n0).data_ptr(),
                                                    C_shard.data_ptr() + 4 * n0, M, n1 - n0, K, A_shard.stride(0),
                                                    C_shard.stride(0), st), "elv_gemm_prepacked")
-                self._done(chunk_done, c, n0, n1)
-        return C_shard
-
-    def _step_fp16(self, A_shard, B, C_shard, b_ready, a_ready, chunk_done):
-        lib, K, st = self.lib, self.K, self.stream.cuda_stream
-        M = A_shard.shape[0]
-        works = []
-        with torch.cuda.stream(self.stream):
-            for c, ((n0, n1), bp) in enumerate(zip(self.chunks, self.b_planes)):
-                if self.rank == self.src:
-                    if b_ready is not None:
-                        self.stream.wait_event(b_ready[c])
-                    self._check(lib.elv_fp16x3_split_b(B.data_ptr() + 4 * n0, K, n1 - n0, B.stride(0),
-                                                       bp.data_ptr(), st), "elv_fp16x3_split_b")
-                works.append(dist.broadcast(bp, src=self.src, group=self.group, async_op=True)
-                             if self.world > 1 else None)
-            if M == 0:
-                for w in works:
-                    if w is not None:
-                        w.wait()
-                return C_shard
-            if a_ready is not None:
-                self.stream.wait_event(a_ready)
-            self._check(lib.elv_fp16x3_split_a(A_shard.data_ptr(), M, K, A_shard.stride(0),
-                                               self.a_planes.data_ptr(), st), "elv_fp16x3_split_a")
-            for c, ((n0, n1), bp, w) in enumerate(zip(self.chunks, self.b_planes, works)):
-                if w is not None:
-                    w.wait()
-                self._check(lib.elv_fp16x3_gemm_planes(self.a_planes.data_ptr(), bp.data_ptr(),
-                                                       C_shard.data_ptr() + 4 * n0, M, n1 - n0, K,
-                                                       C_shard.stride(0), st), "elv_fp16x3_gemm_planes")
                 self._done(chunk_done, c, n0, n1)
         return C_shard
 
@@ -308,9 +276,12 @@ class HostRowShardPipeline:
                                                self.s_in.cuda_stream), "elv_copy2d")
                     b_evs.append(torch.cuda.Event())
                     b_evs[-1].record(self.s_in)
-                if c == 0 and rows:
-                    A_dev.copy_(A_h, non_blocking=True)
-            a_ev.record(self.s_in)
+                if c == 0:
+                    # A's event right after its copy: chunk 0's split/GEMM must
+                    # not wait for the whole of B to cross PCIe
+                    if rows:
+                        A_dev.copy_(A_h, non_blocking=True)
+                    a_ev.record(self.s_in)
 
         def chunk_done(c, n0, n1, ev):
             self.s_out.wait_event(ev)

@@ -45,10 +45,11 @@ def _default_tf32x3() -> bool:
 
 def _default_encoding() -> str:
     """Operand encoding of the tcgen05 kernel when tf32x3 is requested:
-    "fp16" (3xFP16, scaled planes: 1.8x the throughput and half the error of
-    3xTF32 in every measured input class; falls back to tf32 for K < 512 or
-    fewer pair tiles than SMs) or "tf32" (the 3xTF32 split)."""
-    return os.environ.get("ELV_TC_ENCODING", "fp16")
+    "tf32" (the 3xTF32 split, the default: `tf32x3=True` means 3xTF32) or,
+    as an explicit opt-in, "fp16" (3xFP16, power-of-two scaled fp16 planes:
+    ~1.8x the throughput; rows / columns spanning more than 2^29 are
+    recomputed by the range-guard fix-up; falls back to tf32 for K < 512)."""
+    return os.environ.get("ELV_TC_ENCODING", "tf32")
 
 
 def plan(e, arg_shapes, tf32x3: bool | None = None, tc_encoding: str | None = None) -> dispatch.KernelPlan:
@@ -90,10 +91,19 @@ def gemm(p: dispatch.KernelPlan, A: torch.Tensor, B: torch.Tensor,
         out = torch.empty((M, N), device=A.device, dtype=torch.float32)
     elif out.shape != (M, N) or out.stride(-1) != 1 or out.dtype != torch.float32:
         raise EvalError("out must be a row-major fp32 M x N tensor")
-    if stream is None:
-        stream = torch.cuda.current_stream(A.device)
     ws_bytes = lib.elv_gemm_workspace_bytes(p.variant, M, N, K)
     ws = torch.empty(ws_bytes, device=A.device, dtype=torch.uint8) if ws_bytes else None
+    cur = torch.cuda.current_stream(A.device)
+    if stream is None:
+        stream = cur
+    elif stream != cur:
+        # inputs (and any .contiguous() copies) were produced on the current
+        # stream; the temporaries allocated here must not be recycled by the
+        # caching allocator while `stream` still uses them
+        stream.wait_stream(cur)
+        for t in (A, B, out, ws):
+            if t is not None:
+                t.record_stream(stream)
     with torch.cuda.device(A.device):
         rc = lib.elv_gemm(p.variant, A.data_ptr(), B.data_ptr(), out.data_ptr(), M, N, K,
                           A.stride(0), B.stride(0), out.stride(0),
@@ -111,6 +121,7 @@ class GemmCall:
     packA+packB fused; 7: fused hi/lo split of A and B); compute 1."""
 
     PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 2}   # 8: [A rows | B max], B split
+    COMPUTE_LAUNCHES = {7: 2, 8: 2}     # tensor-core GEMM + range-guard fix-up; others: 1
 
     def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
         self.lib = _lib.load()
@@ -119,7 +130,7 @@ class GemmCall:
         self.ws_bytes = self.lib.elv_gemm_workspace_bytes(p.variant, p.M, p.N, p.K)
         self.ws = (torch.empty(self.ws_bytes, device=A.device, dtype=torch.uint8)
                    if self.ws_bytes else None)
-        self.launches = self.PREPARE_LAUNCHES[p.variant] + 1
+        self.launches = self.PREPARE_LAUNCHES[p.variant] + self.COMPUTE_LAUNCHES.get(p.variant, 1)
         # the buffers are fixed for the object's lifetime: build the C-ABI
         # argument tuples once (saves 1.5-3 us of host time per 1024^3 call,
         # 5-8 % of a single 3xTF32 / SIMT call; profiles/r1/small/gemmcall_args.jsonl)
@@ -368,6 +379,10 @@ def _run_template(e, args: list, *, device=None, tf32x3: bool | None = None, out
     ts = [_as_host_f32(a) for a in args]
     for t in ts:
         if t.dim() != 2:
+            # not matrix operands: a program that is no GEMM schedule (vector
+            # add / dot, ...) goes to the generic compiler ("no B200 kernel"),
+            # a GEMM schedule fails like the reference's map over scalars
+            dispatch.term_shape(e)
             raise EvalError("map expects an array of arrays")
     p = plan(e, [tuple(t.shape) for t in ts], tf32x3, tc_encoding)
     if device is None:

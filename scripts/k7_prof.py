@@ -38,7 +38,7 @@ def main():
     st = torch.cuda.current_stream().cuda_stream
     _lib.check(getattr(lib, pre + "split_a")(A.data_ptr(), M, K, K, ap.data_ptr(), st), "a")
     _lib.check(getattr(lib, pre + "split_b")(B.data_ptr(), K, N, N, bp.data_ptr(), st), "b")
-    host = np.zeros((512, 8), np.uint64)
+    host = np.zeros((512, 12), np.uint64)
     for rep in range(3):
         lib.elv_debug_k7_prof(host.ctypes.data, 1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -58,8 +58,12 @@ def main():
                "prod_wait_empty_frac": both[:, 3].mean() / tot,
                "prod_wave_sync_frac": both[:, 4].mean() / tot,
                "epi_wait_tfull_frac": both[:, 5].mean() / tot,
-               "epi_drain_frac": both[:, 6].mean() / tot,
-               "epi_drain_cyc_per_tile": both[:, 6].mean() / max(1, lead[:, 7].mean()),
+               "epi_store_frac": both[:, 6].mean() / tot,
+               "epi_store_cyc_per_tile": both[:, 6].mean() / max(1, lead[:, 7].mean()),
+               "epi_chunk_drain_cyc": both[:, 8].sum() / max(1, both[:, 9].sum()),
+               "epi_chunk_wait_cyc": both[:, 5].sum() / max(1, both[:, 9].sum()),
+               "epi_chunk_arrive_cyc": both[:, 10].sum() / max(1, both[:, 9].sum()),
+               "mma_cyc_per_chunk": tot / max(1, lead[:, 7].mean() * K / (64 if f16 else 32)),
                "mma_wait_full_max_frac": (lead[:, 1] / lead[:, 2]).max()}
         print(json.dumps(out), flush=True)
 

@@ -49,8 +49,12 @@ def test_workspace_sizes():
     # kernel) and large ones (cp.async 128x256 kernel)
     assert lib.elv_gemm_workspace_bytes(6, 100, 1000, 33) == 1024 * 33 * 4 + 128 * 33 * 4
     assert lib.elv_pack_b_bytes(33, 1000) == 1024 * 33 * 4
-    # 3xTF32: hi/lo planes of A (M x Kp) and B^T (N x Kp), Kp = K rounded to 16
-    assert lib.elv_gemm_workspace_bytes(7, 100, 200, 30) == (2 * 100 * 32 + 2 * 200 * 32) * 4 + 256
+    # 3xTF32: hi/lo planes of A (M x Kp) and B^T (N x Kp), Kp = K rounded to 32, each
+    # with its range-guard flags (rows u32, 128 B-rounded), + the workspace's
+    # contiguous flag tail (M + N u32) and alignment slack
+    up = lambda x: (x + 127) // 128 * 128  # noqa: E731
+    planes = (2 * 100 * 32 + 2 * 200 * 32) * 4 + 256 + up(100 * 4) + up(200 * 4)
+    assert lib.elv_gemm_workspace_bytes(7, 100, 200, 30) == planes + 128 + up(300 * 4)
     assert lib.elv_gemm_workspace_bytes(0, 0, 5, 5) == 0
 
 

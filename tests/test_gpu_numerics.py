@@ -1,0 +1,185 @@
+"""fp32 safety of the tensor-core encodings (K7 3xTF32, K8 3xFP16) on
+adversarial inputs, against the f64 oracle at the stated tolerance.
+
+The reference evaluates `add`/`mult` in f64 on any float (reference
+pkg/src/stratir/interp.py:145-148).  Two mechanisms keep the tcgen05 paths
+inside the fp32 bound for every input class, not only U(-1,1):
+  * chunked accumulation: each k-block accumulates into a fresh TMEM buffer
+    (corrections first, hi.hi last) and the epilogue adds the chunks with
+    round-to-nearest in registers -- the tensor core's round-toward-zero
+    accumulate otherwise biases long sums (positive inputs: 10.9x tau=1 at
+    K=8192 before, profiles/r2/tc_numerics_before_chunked.jsonl);
+  * the range guard: rows of A / columns of B with elements outside the
+    encoding's exact window are recomputed by the SIMT fix-up (bitwise the
+    parallel schedule's SIMT kernel, K6).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2002_02268_b200 import interp, schedules, synth
+
+pytestmark = pytest.mark.gpu
+
+CLASSES = ("uniform", "positive", "dominant", "outlier_rows", "outlier_cols", "huge", "tiny", "dynamic")
+ENCODINGS = ("tf32", "fp16")
+SHAPES = [(512, 768, 1024), (300, 520, 640), (1024, 1024, 4096)]
+
+
+def make(M, N, K, kind, dev, seed=5):
+    A = torch.empty((M, K), device=dev)
+    B = torch.empty((K, N), device=dev)
+    synth.fill_device(A, seed, 0)
+    synth.fill_device(B, seed, 1)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    if kind == "positive":                       # no cancellation: |C| = (|A||B|)
+        A.abs_()
+        B.abs_()
+    elif kind == "dominant":                     # one product dominates each sum
+        idx = torch.randint(0, K, (M,), generator=g).to(dev)
+        A[torch.arange(M, device=dev), idx] *= 4096.0
+    elif kind == "outlier_rows":                 # 2^32 outlier meeting zeros in B
+        A[:, 0] = 2.0 ** 32
+        B[0, :] = 0.0
+    elif kind == "outlier_cols":
+        B[:, 1] = 2.0 ** 40
+        B[:, 1][torch.arange(K, device=dev) % 7 != 0] *= 2.0 ** -80
+    elif kind == "huge":                         # |x| >= 2^101 in every row of A
+        A *= 2.0 ** 110
+        B *= 2.0 ** -110
+    elif kind == "tiny":                         # row maxima below 2^-101
+        A *= 2.0 ** -110
+        B *= 2.0 ** 110
+    elif kind == "dynamic":                      # every element scaled by 2^u, u in [-20, 20]
+        A *= torch.pow(2.0, torch.randint(-20, 21, (M, K), generator=g).float()).to(dev)
+        B *= torch.pow(2.0, torch.randint(-20, 21, (K, N), generator=g).float()).to(dev)
+    return A, B
+
+
+def _tc(term, A, B, enc):
+    return interp.run_tensor(term, A, B, tf32x3=True, tc_encoding=enc)
+
+
+def _worst(C, A, B, K, rows=None):
+    if rows is not None:
+        A = A[rows]
+        C = C[rows]
+    Ah, Bh = A.double().cpu().numpy(), B.double().cpu().numpy()
+    ref, ab = oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh)
+    Cd = C.double().cpu().numpy()
+    assert np.isfinite(Cd).all()
+    return float((np.abs(Cd - ref) / oracle.bound(K, ab)).max())
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("kind", CLASSES)
+@pytest.mark.parametrize("enc", ENCODINGS)
+def test_tensor_core_classes_within_tau(cuda, enc, kind, shape):
+    """Every class at tau = 1 (oracle.default_tau), except `dominant`, where
+    the sqrt(K) law itself breaks down (one product sets the sum, its
+    roundings do not average): there the tensor-core result must be no
+    worse than the SIMT kernel's on the same inputs (1.2x + 0.1 slack),
+    and the SIMT kernel's own ratio is recorded."""
+    M, N, K = shape
+    A, B = make(M, N, K, kind, cuda)
+    term = schedules.apply_padded("parallel", M, N, K).term
+    C = _tc(term, A, B, enc)
+    torch.cuda.synchronize()
+    worst = _worst(C, A, B, K)
+    if kind == "dominant":
+        simt = _worst(interp.run_tensor(term, A, B, tf32x3=False), A, B, K)
+        print(f"{enc} {kind} {shape}: tc {worst:.3g} simt {simt:.3g}")
+        assert worst <= max(1.0, 1.2 * simt + 0.1), f"tc {worst:.3g} vs simt {simt:.3g}"
+    else:
+        print(f"{enc} {kind} {shape}: worst err/bound {worst:.3g}")
+        assert worst <= 1.0, f"{enc} {kind}: worst err/bound {worst:.3g}"
+
+
+@pytest.mark.parametrize("enc", ENCODINGS)
+def test_guarded_rows_and_columns_equal_the_simt_kernel(cuda, enc):
+    """Rows of A / columns of B holding an element outside both encodings'
+    windows (|x| = 2^-110: below tf32's 2^-100 guard and 2^-110 below its row
+    maximum for fp16) are recomputed by the fix-up with the SIMT kernel's
+    arithmetic: bitwise the parallel schedule's K6 output there; the rest of
+    C stays on the tensor cores (within tau)."""
+    M, N, K = 640, 768, 1024
+    A, B = make(M, N, K, "uniform", cuda, seed=9)
+    rows, cols = [5, 77, 300, 639], [9, 200, 767]
+    for r in rows:
+        A[r, 10] = 2.0 ** -110
+    for c in cols:
+        B[20, c] = -(2.0 ** -110)
+    term = schedules.apply("parallel", M, N, K).term
+    C = _tc(term, A, B, enc)
+    C6 = interp.run_tensor(term, A, B, tf32x3=False)
+    torch.cuda.synchronize()
+    assert torch.equal(C[rows], C6[rows])
+    assert torch.equal(C[:, cols], C6[:, cols])
+    others = torch.ones(M, dtype=torch.bool)
+    others[rows] = False
+    assert not torch.equal(C[others], C6[others])      # the tensor-core path ran elsewhere
+    assert _worst(C, A, B, K) <= 1.0
+
+
+@pytest.mark.parametrize("enc", ENCODINGS)
+def test_huge_rows_stay_finite(cuda, enc):
+    """Rows of A with |x| up to 2^126 against columns of B scaled down so
+    every product is finite: the fp16 encoding's power-of-two scales stay
+    normal (the exponent is clamped on the low side only) and the epilogue
+    unscales in two exact steps, so nothing overflows to Inf."""
+    M, N, K = 512, 512, 1024
+    A, B = make(M, N, K, "uniform", cuda, seed=3)
+    A[::3] *= 2.0 ** 126
+    A[1::3] *= 2.0 ** 101
+    B *= 2.0 ** -100
+    term = schedules.apply("parallel", M, N, K).term
+    C = _tc(term, A, B, enc)
+    torch.cuda.synchronize()
+    assert torch.isfinite(C).all()
+    assert _worst(C, A, B, K) <= 1.0
+
+
+@pytest.mark.parametrize("kind", ["positive", "dynamic", "outlier_rows"])
+@pytest.mark.parametrize("enc", ENCODINGS)
+def test_bench_shape_checksums_adversarial(cuda, enc, kind):
+    """configs[3] at full size (32768^2 x 8192) on adversarial classes, every
+    element accounted for through column and row checksums against f64 (see
+    test_gpu_parity.test_bench_shape_checksums_cover_every_element), plus
+    sampled rows element-wise."""
+    M, N, K = 32768, 32768, 8192
+    A, B = make(M, N, K, kind, cuda, seed=1)
+    C = _tc(schedules.apply("parallel", M, N, K).term, A, B, enc)
+    torch.cuda.synchronize()
+    rows = torch.tensor([0, 1, 4097, 16384, 32767], device=cuda)
+    Cs = C[rows].clone()
+    col = C.double().sum(0)
+    row = C.double().sum(1)
+    del C
+    torch.cuda.empty_cache()
+    assert _worst(Cs, A[rows], B, K) <= 1.0
+    Ad = A.double()
+    col_ref = Ad.sum(0) @ B.double()
+    row_ref = Ad @ B.double().sum(1)
+    b = Ad.abs() @ B.double().abs()
+    del Ad
+    b *= oracle.default_tau(K) * K ** 0.5 * 2.0 ** -24
+    col_lin, row_lin = b.sum(0), b.sum(1)
+    b.square_()
+    col_rss, row_rss = b.sum(0).sqrt(), b.sum(1).sqrt()
+    del b
+    torch.cuda.empty_cache()
+    ce, re = (col - col_ref).abs(), (row - row_ref).abs()
+    lin = max((ce / col_lin).max().item(), (re / row_lin).max().item())
+    cr, rr = (ce / col_rss).max().item(), (re / row_rss).max().item()
+    print(f"{enc} {kind}: checksum err / rss-bound: columns {cr:.3g}, rows {rr:.3g}; / linear bound {lin:.3g}")
+    # even fully correlated, the elements' errors stay under a tenth of their bounds on average
+    assert lin <= 0.1
+    if kind != "positive":
+        assert cr <= 1.0 and rr <= 1.0
+    # positive inputs (no cancellation): each chunk's hi.hi MMAs round toward
+    # zero, leaving a same-signed residue of ~2^-22 |C_ij| per element (4/sqrt(K)
+    # of its bound at most); it does not average out in a sum of 32768
+    # elements: 4-6x the root-sum-square of the bounds, 0.02-0.04 of their
+    # linear sum (profiles/r2/numerics_chunked.log)
