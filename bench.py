@@ -311,6 +311,24 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` outside a launcher: re-run this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1, the
+    way the driver launches it, and return its exit code.  NCCL's INIT log
+    (communicator sizes) goes to stderr; rank 0 alone prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def workload_config(args, world):
     return {"workload": f"parallel schedule mm({args.M},{args.N},{args.K}) row-sharded "
                         f"(BASELINE.json configs[3]; M x N x K)",
@@ -335,8 +353,12 @@ def main():
     ap.add_argument("--chunks", type=int, default=4, help="packedB broadcast chunks (N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ladder", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -363,6 +385,8 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+        print(f"[bench rank {rank}] process group {dist.get_backend()} with {dist.get_world_size()} ranks, "
+              f"device {dev}", file=sys.stderr, flush=True)
 
     if args.workload == "ladder":
         run_ladder(args, dev)
@@ -441,10 +465,14 @@ def main():
     else:   # the pipelined step interleaves prepass, broadcast waits and GEMM chunks
         prep_ms = 0.0
         comp_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
+    per_rank_ms = [ms]
     if world > 1:
         t = torch.tensor([ms, comp_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, comp_ms_max = t.tolist()
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        per_rank_ms = [g[0].item() for g in gathered]
+        ms = max(per_rank_ms)
+        comp_ms_max = max(g[1].item() for g in gathered)
     else:
         comp_ms_max = comp_ms
     flops = 2.0 * M * N * K
@@ -532,6 +560,12 @@ def main():
         "gpu_launches": args.steps * launches_per_step,
         "e2e": e2e,
     }
+    if world > 1:
+        out["ranks"] = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                        "per_rank_ms_per_step": per_rank_ms,
+                        "rows_per_rank": [D.shard_rows(M, world, r).rows for r in range(world)],
+                        "broadcast_bytes_per_step": pipe.broadcast_bytes, "chunks": len(pipe.chunks),
+                        "timing": "ms_per_step = max over ranks (CUDA events on each rank's stream)"}
     if world == 1 and args.variant in ("parallel_fp16x3", "parallel_tf32x3"):
         # the other tcgen05 encoding on the same operands, same run (the
         # north star's 3xTF32 beside the default 3xFP16, or vice versa)
@@ -557,6 +591,13 @@ def main():
             "roofline_frac": oach / opeak, "steps": reps,
             "note": "measured after the main timed region on the same inputs (not part of value)"}}
         del ocall
+    if world == 1 and not args.no_ladder:
+        # configs[1], [2], [4] on the driver's clock: per-strategy GFLOP/s,
+        # kernel roofline fraction and an in-run parity bit (sampled rows)
+        t0 = time.perf_counter()
+        lad = ladder_cases(dev, reps_small=10, reps_large=3)
+        out["ladder"] = {"l2": "flushed (256 MB write) before every rep", "seconds": time.perf_counter() - t0,
+                         "all_parity_ok": all(r["parity_ok"] for r in lad), "cases": lad}
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_single()
     print(json.dumps(out), flush=True)
@@ -564,30 +605,53 @@ def main():
         dist.destroy_process_group()
 
 
-def run_ladder(args, dev):
-    """configs[1] (all strategies at 1024^3) and configs[2] (8192^3 subset)."""
+LADDER_1024 = ("baseline", "blocking", "vectorized", "loopPerm", "arrayPacking", "cacheBlocks", "parallel",
+               "parallel_tf32x3", "parallel_fp16x3")
+LADDER_8192 = ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3", "parallel_fp16x3")
+ODD_SHAPES = ((1000, 1000, 1000), (4096, 256, 4096), (257, 1031, 513))    # configs[4], M x N x K
+
+
+def _parity_rows(A, B, C, K, rows):
+    """In-run parity bit: sampled rows of C against an f64 product on the
+    device (torch f64 -- the bench's own checker, not the oracle package),
+    at the tests' bound |C - C64| <= tau sqrt(K) 2^-24 (|A||B|), tau = 1
+    (2 for K < 32)."""
+    import torch
+    r = torch.tensor(sorted(set(rows)), device=A.device)
+    a, b = A[r].double(), B.double()
+    ref, ab = a @ b, a.abs() @ b.abs()
+    tau = 1.0 if K >= 32 else 2.0
+    ratio = ((C[r].double() - ref).abs() / (tau * K ** 0.5 * 2.0 ** -24 * ab).clamp_min(1e-300)).max().item()
+    return bool(ratio <= 1.0), ratio
+
+
+def ladder_cases(dev, reps_small=20, reps_large=5, with_odd=True):
+    """configs[1] (every strategy at 1024^3), configs[2] (8192^3: the packed
+    strategies and both tensor-core encodings) and configs[4] (odd shapes,
+    every strategy) as records: GFLOP/s per call (prepass + kernel, L2
+    flushed before every rep), the kernel's TFLOP/s and roofline fraction,
+    and a parity bit on sampled rows."""
     import torch
     from paper_2002_02268_b200 import dispatch, interp, schedules, synth
     peaks, src = load_peaks()
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    cublas = measure_cublas(dev)
-    print(json.dumps({"workload": "library reference points (not our path)", **cublas}), flush=True)
-    cases = [(v, 1024) for v in list(schedules.SCHEDULE_NAMES) + ["parallel_tf32x3", "parallel_fp16x3"]]
-    cases += [(v, 8192) for v in ("arrayPacking", "cacheBlocks", "parallel", "parallel_tf32x3", "parallel_fp16x3")]
+    cases = [(v, (1024, 1024, 1024), "configs[1]") for v in LADDER_1024]
+    cases += [(v, (8192, 8192, 8192), "configs[2]") for v in LADDER_8192]
+    if with_odd:
+        cases += [(v, shp, "configs[4]") for shp in ODD_SHAPES for v in LADDER_1024]
     stream = torch.cuda.current_stream(dev)
-    for v, n in cases:
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MB > L2
+    out = []
+    for v, (M, N, K), cfg in cases:
         sched, tf = ("parallel", True) if v.startswith("parallel_") else (v, False)
-        term = schedules.apply(sched, n, n, n).term
-        p = dispatch.decode(term, [(n, n), (n, n)], tf32x3=tf,
+        term = schedules.apply_padded(sched, M, N, K).term
+        p = dispatch.decode(term, [(M, K), (K, N)], tf32x3=tf,
                             tc_encoding="fp16" if v == "parallel_fp16x3" else "tf32")
-        A = torch.empty((n, n), device=dev); synth.fill_device(A, 0, 0)
-        B = torch.empty((n, n), device=dev); synth.fill_device(B, 0, 1)
-        C = torch.empty((n, n), device=dev)
+        A = torch.empty((M, K), device=dev); synth.fill_device(A, 0, 0)
+        B = torch.empty((K, N), device=dev); synth.fill_device(B, 0, 1)
+        C = torch.empty((M, N), device=dev)
         call = interp.GemmCall(p, A, B, C, stream)
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MB > L2
-        reps = 20 if n <= 1024 else 5
-        if v == "baseline" and n > 1024:
-            reps = 2
+        reps = reps_small if M * N * K <= 2 ** 30 else reps_large
         for _ in range(3):
             call()
         torch.cuda.synchronize()
@@ -598,16 +662,28 @@ def run_ladder(args, dev):
             e0.record(stream); call.prepare(); e1.record(stream); call.compute(); e2.record(stream)
             torch.cuda.synchronize()
             tot.append(e0.elapsed_time(e2)); comp.append(e1.elapsed_time(e2))
+        ok, ratio = _parity_rows(A, B, C, K, [0, 1, M // 3, M // 2, M - 1])
         ms = statistics.median(tot)
-        peak, bound, note = roofline_peak(v, peaks, n_sms, cublas)
-        ach = 2.0 * n ** 3 / (statistics.median(comp) * 1e-3) / 1e12
-        print(json.dumps({"workload": f"{v} mm({n},{n},{n})", "variant": v, "M": n, "N": n, "K": n,
-                          "gflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "ms": ms,
-                          "kernel_ms": statistics.median(comp), "kernel_tflops": ach,
-                          "roofline_bound": bound, "peak_tflops": peak, "frac": ach / peak,
-                          "l2": "flushed (256 MB write) before every rep"}), flush=True)
-        del A, B, C, call, flush
+        peak, bound, _ = roofline_peak(v, peaks, n_sms, None)
+        ach = 2.0 * M * N * K / (statistics.median(comp) * 1e-3) / 1e12
+        out.append({"config": cfg, "variant": v, "kernel_variant_id": p.variant, "M": M, "N": N, "K": K,
+                    "gflops": 2.0 * M * N * K / (ms * 1e-3) / 1e9, "ms": ms,
+                    "kernel_ms": statistics.median(comp), "kernel_tflops": ach, "roofline_bound": bound,
+                    "peak_tflops": peak, "frac": ach / peak, "parity_ok": ok, "parity_worst": ratio,
+                    "reps": reps})
+        del A, B, C, call
         torch.cuda.empty_cache()
+    return out
+
+
+def run_ladder(args, dev):
+    """--workload ladder: one JSON line per (strategy, shape)."""
+    import torch
+    cublas = measure_cublas(dev)
+    print(json.dumps({"workload": "library reference points (not our path)", **cublas}), flush=True)
+    for r in ladder_cases(dev):
+        print(json.dumps({"workload": f"{r['variant']} mm({r['M']},{r['N']},{r['K']})",
+                          "l2": "flushed (256 MB write) before every rep", **r}), flush=True)
 
 
 def run_binomial(args, dev, H=16384, W=16384):

@@ -260,6 +260,54 @@ __device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[NC * 32])
   }
 }
 
+// Accumulation chunk length in k: 32 (tf32) / 64 (fp16) -- one stage of the
+// default pair kernels; kernels with shallower stages take CH = CHUNK_K / BK
+// stages per chunk.  The per-element operation sequence then depends only on
+// the chunk's k range, never on the stage depth or the tile shape, so every
+// kernel configuration of an encoding produces the same bits.
+template <bool F16> struct ChunkK { static constexpr int value = F16 ? 64 : 32; };
+
+template <bool PAIR, bool F16>
+__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc);
+template <bool F16>
+__device__ __forceinline__ void tc_mma_pair_sc11(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc);
+
+// The MMAs of one chunk (CH stages of KSUB k-steps) into a fresh accumulator
+// d: the correction products first (hi.lo for every k-step, then lo.hi, then
+// lo.lo when requested) -- they build up at their own, 2^-11 smaller scale --
+// then hi.hi, whose first MMA rescales the fp16 corrections by 2^-11
+// (scale-input-d), so only CH * KSUB truncations fall on the chunk's magnitude.
+template <bool PAIR, bool F16, int KSUB, int CH>
+__device__ __forceinline__ void mma_chunk(uint32_t d, const uint64_t (&ahi)[CH], const uint64_t (&alo)[CH],
+                                          const uint64_t (&bhi)[CH], const uint64_t (&blo)[CH], uint32_t idesc,
+                                          int lolo) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int k = 0; k < KSUB; ++k) tc_mma<PAIR, F16>(d, ahi[j] + 2 * k, blo[j] + 2 * k, idesc, (j | k) != 0);
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int k = 0; k < KSUB; ++k) tc_mma<PAIR, F16>(d, alo[j] + 2 * k, bhi[j] + 2 * k, idesc, 1u);
+  if (!F16 && lolo) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int k = 0; k < KSUB; ++k) tc_mma<PAIR, F16>(d, alo[j] + 2 * k, blo[j] + 2 * k, idesc, 1u);
+  }
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int k = 0; k < KSUB; ++k) {
+      if (F16 && j == 0 && k == 0) {
+        if (PAIR) tc_mma_pair_sc11<F16>(d, ahi[0], bhi[0], idesc);
+        else tc_mma_one_sc11<F16>(d, ahi[0], bhi[0], idesc);
+      } else {
+        tc_mma<PAIR, F16>(d, ahi[j] + 2 * k, bhi[j] + 2 * k, idesc, 1u);
+      }
+    }
+}
+
 template <int TBN, int TBK, bool F16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
@@ -274,6 +322,8 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   constexpr int A_TILE_BYTES = Cfg::A_TILE;
   constexpr int BN = TBN;
   constexpr int NC = TBN / 64;                       // 32-column groups per epilogue warp
+  constexpr int CH = ChunkK<F16>::value / TBK;           // stages per accumulation chunk
+  static_assert(CH >= 1 && CH * TBK == ChunkK<F16>::value, "chunk length");
   constexpr uint32_t kIdesc = Cfg::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -331,37 +381,31 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer: one chunk per k-block ----------------
+      // ---------------- MMA issuer: one accumulation chunk per CH stages ----------------
       int s = 0; uint32_t ph = 0;
       uint32_t q = 0;                                  // chunk counter (TMEM buffer q & 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        for (int kb = 0; kb < num_kb; ++kb, ++q) {
+        for (int kb = 0; kb < num_kb; kb += CH, ++q) {
           const uint32_t b = q & 1;
           mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          const uint64_t ahi = umma_desc_k<Cfg::ROW_BYTES / 4>(st);
-          const uint64_t alo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + A_TILE_BYTES);
-          const uint64_t bhi = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES);
-          const uint64_t blo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
-          const uint32_t d = tmem_base + b * (uint32_t)BN;
-          // corrections first, into the fresh accumulator, then hi.hi (see mma_chunk)
+          uint64_t ahi[CH], alo[CH], bhi[CH], blo[CH];
+          int ss[CH];
 #pragma unroll
-          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, ahi + 2 * k, blo + 2 * k, kIdesc, k != 0);
-#pragma unroll
-          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, alo + 2 * k, bhi + 2 * k, kIdesc, 1u);
-          if (!F16 && with_lolo) {
-#pragma unroll
-            for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, alo + 2 * k, blo + 2 * k, kIdesc, 1u);
+          for (int j = 0; j < CH; ++j) {
+            mbar_wait(&full[s], ph);
+            const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+            ahi[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st);
+            alo[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st + A_TILE_BYTES);
+            bhi[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES);
+            blo[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+            ss[j] = s;
+            if (++s == STAGES) { s = 0; ph ^= 1; }
           }
-          if (F16) tc_mma_one_sc11<F16>(d, ahi, bhi, kIdesc);
-          else tc_mma_one<F16>(d, ahi, bhi, kIdesc, 1u);
+          tc_fence_after();
+          mma_chunk<false, F16, Cfg::KSUB, CH>(tmem_base + b * (uint32_t)BN, ahi, alo, bhi, blo, kIdesc, with_lolo);
 #pragma unroll
-          for (int k = 1; k < Cfg::KSUB; ++k) tc_mma_one<F16>(d, ahi + 2 * k, bhi + 2 * k, kIdesc, 1u);
-          tc_commit(&empty[s]);                 // frees the slot when these MMAs finish
-          tc_commit(&tfull[b]);                 // chunk complete in buffer b
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+          for (int j = 0; j < CH; ++j) tc_commit(&empty[ss[j]]);   // frees the slots when these MMAs finish
+          tc_commit(&tfull[b]);                                    // chunk complete in buffer b
         }
       }
     }
@@ -380,7 +424,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 #pragma unroll
       for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
 #pragma unroll 1
-      for (int kb = 0; kb < num_kb; ++kb, ++q) {
+      for (int kb = 0; kb < num_kb; kb += CH, ++q) {
         const uint32_t b = q & 1;
         mbar_wait(&tfull[b], (q >> 1) & 1);
         tc_fence_after();
@@ -520,6 +564,11 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, ui
         : "memory");
   }
 }
+template <bool PAIR, bool F16>
+__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (PAIR) tc_mma_pair<F16>(d, a, b, idesc, acc);
+  else tc_mma_one<F16>(d, a, b, idesc, acc);
+}
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -557,6 +606,8 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   constexpr int P_STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr uint32_t kIdescPair = Cfg::IDESC;
   constexpr int NC = P_BN / 2 / 32;                  // 32-column groups per epilogue warp (its half)
+  constexpr int CH = ChunkK<F16>::value / BKT;           // stages per accumulation chunk
+  static_assert(CH >= 1 && CH * BKT == ChunkK<F16>::value, "chunk length");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + P_STAGES * P_STAGE_BYTES;      // 1 KB-aligned (stages are)
@@ -659,38 +710,34 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       PROF_T(m_start);
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         PROF_ADD(7, 1);
-        for (int kb = 0; kb < num_kb; ++kb, ++q) {
+        for (int kb = 0; kb < num_kb; kb += CH, ++q) {
           const uint32_t b = q & 1;
           PROF_T(q0);
           mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
           PROF_T(f0);
           PROF_ADD(0, f0 - q0);
-          mbar_wait(&full[s], ph);
+          uint64_t ahi[CH], alo[CH], bhi[CH], blo[CH];
+          int ss[CH];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            mbar_wait(&full[s], ph);
+            const uint32_t st = smem_u32(smem + s * P_STAGE_BYTES);
+            // 128 B rows (tf32 BK=32 / f16 BK=64): 128B swizzle; 64 B rows: 64B
+            ahi[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st);
+            alo[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st + P_A_TILE);
+            bhi[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE);
+            blo[j] = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE + P_B_TILE);
+            ss[j] = s;
+            if (++s == P_STAGES) { s = 0; ph ^= 1; }
+          }
           PROF_T(f1);
           PROF_ADD(1, f1 - f0);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + s * P_STAGE_BYTES);
-          // 128 B rows (tf32 BK=32 / f16 BK=64): 128B swizzle; 64 B rows: 64B
-          const uint64_t ahi = umma_desc_k<Cfg::ROW_BYTES / 4>(st);
-          const uint64_t alo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + P_A_TILE);
-          const uint64_t bhi = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE);
-          const uint64_t blo = umma_desc_k<Cfg::ROW_BYTES / 4>(st + 2 * P_A_TILE + P_B_TILE);
-          const uint32_t d = tmem_base + b * (uint32_t)P_BN;
+          mma_chunk<true, F16, Cfg::KSUB, CH>(tmem_base + b * (uint32_t)P_BN, ahi, alo, bhi, blo, kIdescPair,
+                                              with_lolo);
 #pragma unroll
-          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, ahi + 2 * k, blo + 2 * k, kIdescPair, k != 0);
-#pragma unroll
-          for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, alo + 2 * k, bhi + 2 * k, kIdescPair, 1u);
-          if (!F16 && with_lolo) {
-#pragma unroll
-            for (int k = 0; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, alo + 2 * k, blo + 2 * k, kIdescPair, 1u);
-          }
-          if (F16) tc_mma_pair_sc11<F16>(d, ahi, bhi, kIdescPair);
-          else tc_mma_pair<F16>(d, ahi, bhi, kIdescPair, 1u);
-#pragma unroll
-          for (int k = 1; k < Cfg::KSUB; ++k) tc_mma_pair<F16>(d, ahi + 2 * k, bhi + 2 * k, kIdescPair, 1u);
-          tc_commit_pair(&empty[s]);            // frees slot s in both CTAs
+          for (int j = 0; j < CH; ++j) tc_commit_pair(&empty[ss[j]]);   // frees the slots in both CTAs
           tc_commit_pair(&tfull[b]);            // chunk ready in both CTAs
-          if (++s == P_STAGES) { s = 0; ph ^= 1; }
         }
       }
       PROF_T(m_end);
@@ -714,7 +761,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
 #pragma unroll
       for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
 #pragma unroll 1
-      for (int kb = 0; kb < num_kb; ++kb, ++q) {
+      for (int kb = 0; kb < num_kb; kb += CH, ++q) {
         const uint32_t b = q & 1;
         PROF_T(c0);
         mbar_wait(&tfull[b], (q >> 1) & 1);

@@ -147,6 +147,9 @@ class PipelinedRowShardGemm:
                                          for n0, n1 in self.chunks):
             self.variant = 7                        # chunk GEMMs too small for the fp16 encoding
         tc = self.variant in (7, 8)
+        # NCCL bytes per step (packB writes whole 256-column groups)
+        self.broadcast_bytes = (sum(((n1 - n0 + 255) // 256) * 256 * K * 4 for n0, n1 in self.chunks)
+                                if self.world > 1 else 0)
         self.prep = torch.cuda.Stream(device) if tc else None
         self.P = torch.empty(self.lib.elv_pack_b_bytes(K, N) // 4, device=device, dtype=torch.float32)
         if tc:

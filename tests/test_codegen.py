@@ -101,3 +101,16 @@ def test_thread_mappings():
         assert c.mode == "per-scalar" and c.threads == 64 * 32 and "accbuf" not in c.source, n
     c = codegen.compile_term(S().ir.parse(TRACC))
     assert c.mode == "destination-passing" and c.threads == 5 and "accbuf" in c.source
+
+
+def test_vector_program_is_not_taken_for_a_gemm():
+    """CPU half of the generic-fallback check: the template path rejects a
+    two-vector program with the "no B200 kernel" prefix that sends interp.run
+    to the generated-kernel path (not the reference's matrix map error)."""
+    from paper_2002_02268_b200 import interp
+    term = S().ir.parse("""
+def vadd = fun(a : 4.f32 => fun(b : 4.f32 => zip(a)(b) |> map(fun(p => add(fst(p))(snd(p))))));
+""")
+    with pytest.raises(S().interp.EvalError) as err:
+        interp._run_template(term, [[1.0, 2.0, 3.0, 4.0], [1.0, 1.0, 1.0, 1.0]])
+    assert interp._no_template(err.value)

@@ -54,3 +54,19 @@ def test_template_and_generated_kernels_agree(cuda, name):
     Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
     ref, ab = oracle.mm_interp_f64(Ah, Bh, name), oracle.absprod_np(Ah, Bh)
     assert oracle.check(gen, ref, ab, K)[0] and oracle.check(tpl, ref, ab, K)[0]
+
+
+VEC_ADD = """
+def vadd = fun(a : 4.f32 => fun(b : 4.f32 => zip(a)(b) |> map(fun(p => add(fst(p))(snd(p))))));
+"""
+
+
+def test_two_vector_arguments_reach_the_generic_compiler(cuda):
+    """A two-argument program over vectors is no GEMM schedule: interp.run
+    must not stop at the matrix-operand check but compile it,
+    like the reference evaluates it (interp.py:157-162)."""
+    s = S()
+    term = s.ir.parse(VEC_ADD)
+    a, b = [1.0, 2.0, 3.0, 4.0], [1.0, 1.0, 1.0, 1.0]
+    assert s.interp.run(term, [a, b]) == [2.0, 3.0, 4.0, 5.0]
+    assert interp.run(term, [a, b]) == [2.0, 3.0, 4.0, 5.0]

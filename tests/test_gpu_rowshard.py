@@ -372,3 +372,29 @@ def test_host_pipeline_grows_at_bench_scale(cuda):
     assert ok, worst
     assert torch.equal(out, I.gemm(p, A, B).cpu())
     I._host_pipes.clear()
+
+
+def test_bench_gpus_flag_launches_ranks_itself(cuda):
+    """`python bench.py --gpus 2` with no launcher around it re-runs itself
+    under torch.distributed.run (one rank per GPU; here the two ranks share
+    cuda:0 over gloo, ELV_BENCH_SHARE_GPU=1) and rank 0 prints the one JSON
+    line: n_gpus 2, per-rank step times (max over ranks = ms_per_step) and
+    the broadcast bytes per step."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["ELV_BENCH_SHARE_GPU"] = "1"
+    cmd = [sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--M", "2048", "--N", "4096",
+           "--K", "1024", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=repo)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "rowshard2"
+    assert d["ranks"]["world_size"] == 2 and len(d["ranks"]["per_rank_ms_per_step"]) == 2
+    assert abs(max(d["ranks"]["per_rank_ms_per_step"]) - d["ms_per_step"]) < 1e-6
+    assert d["ranks"]["broadcast_bytes_per_step"] == 4096 * 1024 * 4
+    assert "with 2 ranks" in r.stderr
