@@ -108,13 +108,16 @@ def roofline_peak(variant: str, peaks: dict, n_sms: int, cublas: dict | None = N
             f"MEASURED_PEAKS bf16_tflops {tf16:.0f} (burst) = the f16 dense rate; 3xFP16 issues 3 MMAs per "
             f"useful MAC, so the useful-fp32 ceiling is that / 3{lib}")
     if variant == "parallel_tf32x3":
-        tf32 = peaks["bf16_tflops"] / 2.0
-        alt = peaks.get("bf16_tflops_sustained", 0) / 2.0 / 3.0
+        # MEASURED_PEAKS has no TF32 figure, and half its (cuBLAS bf16) burst
+        # number is below what this kernel sustains at 8192^3 (885 TF of
+        # TF32 MMAs, profiles/r2): the stated fallback of B200_PROFILING.md
+        # (TF32 dense 1.1 PFLOP/s) is the denominator
+        tf32 = peaks.get("tf32_tflops", 1100.0)
+        src = "MEASURED_PEAKS tf32_tflops" if "tf32_tflops" in peaks else \
+            "fallback (B200_PROFILING.md: TF32 dense 1.1 PFLOP/s; MEASURED_PEAKS has no TF32 figure)"
         return tf32 / 3.0, "tensor", (
-            f"MEASURED_PEAKS bf16_tflops {peaks['bf16_tflops']:.0f} (burst) / 2 = TF32 dense "
-            f"{tf32:.0f} TF; 3xTF32 issues 3 MMAs per useful MAC, so the useful-fp32 ceiling is "
-            f"that / 3 (the sustained bf16 figure would give {alt:.0f} TF, measured at a lower "
-            f"power-capped clock){lib}")
+            f"{src} = {tf32:.0f} TF; 3xTF32 issues 3 MMAs per useful MAC, so the useful-fp32 ceiling is "
+            f"that / 3{lib}")
     fp32 = n_sms * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
     return fp32, "fp32-simt", (
         f"fp32 FFMA peak = {n_sms} SMs x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS); no "

@@ -53,8 +53,12 @@ template <int TBN, int TBK = BK, bool F16 = false> struct OneCfg {
   static constexpr int B_TILE = TBN * ROW_BYTES;
   static constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;
   static constexpr int NST = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
-  static constexpr int TMEM = 2 * TBN;             // two chunk buffers (ping-pong)
-  static constexpr int SMEM = NST * STAGE + 256 + 1024;
+  // chunk buffers: all 512 TMEM columns (one CTA per SM), so narrow tiles
+  // keep the MMA up to NBUF - 1 chunks ahead of the epilogue's drain (a
+  // 64-column chunk is only ~400 MMA cycles, shorter than one drain's latency)
+  static constexpr int NBUF = 512 / TBN > 8 ? 8 : 512 / TBN;
+  static constexpr int TMEM = 512;
+  static constexpr int SMEM = NST * STAGE + 512 + 1024;
   static constexpr int KSUB = TBK / (F16 ? 16 : 8);     // MMAs per product per stage
   static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
                                     ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -329,9 +333,10 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;                  // [2]: chunk in TMEM buffer b complete
-  uint64_t* tempty = tfull + 2;                      // [2]: buffer b drained by the epilogue
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr int NBUF = Cfg::NBUF;
+  uint64_t* tfull = empty + STAGES;                  // [NBUF]: chunk in TMEM buffer b complete
+  uint64_t* tempty = tfull + NBUF;                   // [NBUF]: buffer b drained by the epilogue
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN, group, BN};
@@ -341,7 +346,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     tma_prefetch_desc(&map_ahi); tma_prefetch_desc(&map_alo);
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], EPI_WARPS); }
+    for (int b = 0; b < NBUF; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -355,6 +360,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   griddep_wait();                                   // operand planes from the preceding split kernel
+  griddep_launch_dependents();                      // the range-guard fix-up may be scheduled (it waits for us)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -383,11 +389,11 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
     if (lane == 0) {
       // ---------------- MMA issuer: one accumulation chunk per CH stages ----------------
       int s = 0; uint32_t ph = 0;
-      uint32_t q = 0;                                  // chunk counter (TMEM buffer q & 1)
+      uint32_t q = 0;                                  // chunk counter (TMEM buffer q % NBUF)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         for (int kb = 0; kb < num_kb; kb += CH, ++q) {
-          const uint32_t b = q & 1;
-          mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
+          const uint32_t b = q % NBUF;
+          mbar_wait(&tempty[b], ((q / NBUF) & 1) ^ 1);
           uint64_t ahi[CH], alo[CH], bhi[CH], blo[CH];
           int ss[CH];
 #pragma unroll
@@ -425,8 +431,8 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
       for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
 #pragma unroll 1
       for (int kb = 0; kb < num_kb; kb += CH, ++q) {
-        const uint32_t b = q & 1;
-        mbar_wait(&tfull[b], (q >> 1) & 1);
+        const uint32_t b = q % NBUF;
+        mbar_wait(&tfull[b], (q / NBUF) & 1);
         tc_fence_after();
         drain_add<NC>(lane_base + b * (uint32_t)BN, acc);
         tc_fence_before();
@@ -533,6 +539,31 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// With an L2 cache policy (createpolicy): the pair kernel keeps the A panels
+// of its current m-group resident (evict_last) while B streams (evict_first).
+__device__ __forceinline__ void tma_load_2d_pair_hint(const CUtensorMap* map, uint32_t leader_bar, void* dst, int c0,
+                                                      int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst,
                                                  int c0, int c1) {
   asm volatile(
@@ -598,7 +629,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
                const __grid_constant__ CUtensorMap map_c,
                float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
                unsigned int* __restrict__ wave_ctr, const float* __restrict__ inv_s,
-               const float* __restrict__ inv_t) {
+               const float* __restrict__ inv_t, int l2_hints) {
   using Cfg = PairCfg<BKT, F16>;
   constexpr int P_STAGES = Cfg::STAGES;
   constexpr int P_A_TILE = Cfg::A_TILE;
@@ -646,6 +677,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   griddep_wait();                                   // operand planes from the preceding split kernel
+  griddep_launch_dependents();                      // the range-guard fix-up may be scheduled (it waits for us)
 
   // tile t: rows [mt*256, +256) (this CTA: + rank*128), cols [nt*256, +256) (this CTA stages + rank*128)
   auto coords = [&](int t, int& m0, int& n0) {
@@ -663,6 +695,8 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
       const uint32_t full0 = mapa_rank(smem_u32(&full[0]), 0);
+      const uint64_t pol_a = l2_policy_evict_last();
+      const uint64_t pol_b = l2_hints >= 2 ? l2_policy_evict_first() : l2_policy_evict_normal();
       int s = 0; uint32_t ph = 0;
       int wave = 0;
       for (int t = cluster_id; t < num_tiles; t += num_clusters, ++wave) {
@@ -682,10 +716,17 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           const uint32_t bar = full0 + (uint32_t)(s * 8);
           const int k0 = kb * BKT;
           if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
-          tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
-          tma_load_2d_pair(&map_alo, bar, st + P_A_TILE, k0, ma);
-          tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
-          tma_load_2d_pair(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb);
+          if (l2_hints) {
+            tma_load_2d_pair_hint(&map_ahi, bar, st, k0, ma, pol_a);
+            tma_load_2d_pair_hint(&map_alo, bar, st + P_A_TILE, k0, ma, pol_a);
+            tma_load_2d_pair_hint(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb, pol_b);
+            tma_load_2d_pair_hint(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb, pol_b);
+          } else {
+            tma_load_2d_pair(&map_ahi, bar, st, k0, ma);
+            tma_load_2d_pair(&map_alo, bar, st + P_A_TILE, k0, ma);
+            tma_load_2d_pair(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb);
+            tma_load_2d_pair(&map_blo, bar, st + 2 * P_A_TILE + P_B_TILE, k0, nb);
+          }
           if (++s == P_STAGES) { s = 0; ph ^= 1; }
         }
         if (wave_ctr != nullptr) atomicAdd(wave_ctr, 1u);
@@ -1164,6 +1205,14 @@ static unsigned int* wave_counter(int dev, cudaStream_t st) {
   return c;
 }
 
+// L2 residency hints in the pair kernel (ELV_L2_HINTS, default on): the
+// m-group's A panels evict_last, B evict_first
+static int l2_hints() {
+  static int v = -2;
+  if (v == -2) v = env_int("ELV_L2_HINTS", 0);
+  return v;
+}
+
 static int tile_group(int dflt) {
   static int v = -2;
   if (v == -2) v = env_int("ELV_TILE_GROUP", -1);
@@ -1176,6 +1225,11 @@ static bool c_store_tma() {
   if (v == -2) v = env_int("ELV_TMA_STORE_C", 1);
   return v != 0;
 }
+
+// m-tiles per L2 raster group of the pair kernel: with L2 hints the group's A
+// panels (group x 256 rows x K of hi+lo planes) stay resident -- 64 MB at
+// K = 8192 for 8 fp16 / 4 tf32 m-tiles, half the 126 MB L2
+template <bool F16> static int pair_group() { return (!F16 && l2_hints()) ? 4 : 8; }
 
 template <int BKT, bool F16 = false>
 static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C, int M,
@@ -1214,7 +1268,7 @@ static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, con
   unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;   // one wave: nothing to sync
   cudaError_t e = launch_pdl(kern, dim3(2 * clusters), dim3(P_NUM_THREADS),
                              (size_t)Cfg::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, mc, C, M, N, ldc, Kp / BKT,
-                             F16 ? 0 : with_lolo(K), tile_group(8), ctr, inv_s, inv_t);
+                             F16 ? 0 : with_lolo(K), tile_group(pair_group<F16>()), ctr, inv_s, inv_t, l2_hints());
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3_pair");
 }
@@ -1248,6 +1302,9 @@ static unsigned int* ws_tail_flags(void* ws, int M, int N, int K) {
 // fp32 operands of the same windows (B row-major, or packedB panels).
 int tc_fixup(const float* A, int lda, const float* B, int ldb, bool b_packed, float* C, int ldc, int M, int N, int K,
              const unsigned int* flag_a, const unsigned int* flag_b, cudaStream_t st) {
+  static int enabled = -1;                          // ELV_TC_FIXUP=0: tuning measurements only (unguarded)
+  if (enabled < 0) enabled = env_int("ELV_TC_FIXUP", 1) != 0;
+  if (!enabled) return ELV_OK;
   const long long blocks = (long long)(M + FIX_SEG - 1) / FIX_SEG + (N + FIX_SEG - 1) / FIX_SEG;
   if (blocks <= 0) return ELV_OK;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tc_fixup: problem too large");
