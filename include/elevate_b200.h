@@ -210,6 +210,26 @@ int elv_gemm_rowshard(int variant, int ndev, const int* devs,
                       float* const* packedB_per_dev, float* const* C_shards,
                       const int* rows, int N, int K, void* const* streams);
 
+/* The pipelined row shard for variants 4..8 (the C-ABI mirror of the Python
+ * PipelinedRowShardGemm; reference anchor: the mapPar(xo) shard axis,
+ * PAPER.md:80).  B_root (K x N row-major on devs[0]) is packed and NCCL-
+ * broadcast in `chunks` column chunks into packedB_per_dev[d] (each
+ * elv_pack_b_bytes(K, N), on devs[d]); each device splits every chunk as it
+ * lands (tensor-core variants, on an internal side stream) and multiplies it
+ * on streams[d] while later chunks are still in flight; the tensor-core
+ * variants include the range-guard fix-up.  A_shards[d]: rows[d] x K
+ * (lda = K); C_shards[d]: rows[d] x N (ldc = N).  workspaces[d] (device
+ * devs[d], workspace_bytes each, from elv_gemm_rowshard_workspace_bytes with
+ * the largest rows[d]) hold the planes; NULL allowed for variants 4..6.
+ * Bitwise equal to elv_gemm on each shard. */
+size_t elv_gemm_rowshard_workspace_bytes(int variant, int rows, int N, int K, int chunks);
+int elv_gemm_rowshard_pipelined(int variant, int ndev, const int* devs,
+                                const float* const* A_shards, const float* B_root,
+                                float* const* packedB_per_dev, float* const* C_shards,
+                                const int* rows, int N, int K, int chunks,
+                                void* const* workspaces, size_t workspace_bytes,
+                                void* const* streams);
+
 /* Thread-local message describing the last error on this thread. */
 const char* elv_last_error(void);
 int elv_abi_version(void);

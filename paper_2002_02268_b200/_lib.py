@@ -27,6 +27,7 @@ EXPORTS = (
     "elv_gemm_host", "elv_gemm_host_workspace_bytes", "elv_gemm_host_tiles", "elv_gemm_host_trace", "elv_copy2d",
     "elv_fp16x3_a_planes_bytes", "elv_fp16x3_b_planes_bytes", "elv_fp16x3_applicable", "elv_fp16x3_split_a",
     "elv_fp16x3_split_b", "elv_fp16x3_gemm_planes", "elv_fp16x3_split_b_packed", "elv_tc_fixup",
+    "elv_gemm_rowshard_workspace_bytes", "elv_gemm_rowshard_pipelined",
 )
 
 _lib = None
@@ -61,6 +62,11 @@ def load():
         "elv_gemm_rowshard": (c_int, [c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_vp),
                                       ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                       ctypes.POINTER(c_int), c_int, c_int, ctypes.POINTER(c_vp)]),
+        "elv_gemm_rowshard_workspace_bytes": (c_size, [c_int, c_int, c_int, c_int, c_int]),
+        "elv_gemm_rowshard_pipelined": (c_int, [c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_vp), c_vp,
+                                                ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_int),
+                                                c_int, c_int, c_int, ctypes.POINTER(c_vp), c_size,
+                                                ctypes.POINTER(c_vp)]),
         "elv_tf32x3_a_planes_bytes": (c_size, [c_int, c_int]),
         "elv_tf32x3_b_planes_bytes": (c_size, [c_int, c_int]),
         "elv_tf32x3_split_a": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),

@@ -10,6 +10,9 @@
 
 #include <dlfcn.h>
 #include <string.h>
+#include <map>
+#include <cmath>
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -435,4 +438,206 @@ int elv_gemm_rowshard(int variant, int ndev, const int* devs, const float* const
   return ELV_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined single-process row shard (variants 4..8): the C-ABI mirror of
+// distributed.PipelinedRowShardGemm for callers without Python.  B (row-major,
+// on devs[0]) is packed and NCCL-broadcast in column chunks (the first half
+// the size of the others: nothing hides its broadcast); on every device a
+// side stream splits each packed chunk into the tensor-core planes as soon as
+// it lands (variants 7, 8) while the compute stream multiplies the previous
+// chunk; the SIMT variants multiply the packed chunk directly.  Column blocks
+// of C are independent and the kernels' per-element arithmetic does not
+// depend on the chunking, so C is bitwise elv_gemm's.
+static std::vector<std::pair<int, int>> column_chunks(int N, int chunks) {
+  const int align = 256;
+  const int units = (N + align - 1) / align;
+  chunks = std::max(1, std::min(chunks, units));
+  std::vector<double> w(chunks, 1.0);
+  if (chunks > 1) w[0] = 0.5;
+  double tot = 0;
+  for (double x : w) tot += x;
+  std::vector<int> bounds{0};
+  double acc = 0;
+  for (int c = 0; c + 1 < chunks; ++c) {
+    acc += w[c];
+    int b = (int)std::lround(units * acc / tot);
+    b = std::min(std::max(b, bounds.back() + 1), units - (chunks - (int)bounds.size()));
+    bounds.push_back(b);
+  }
+  bounds.push_back(units);
+  std::vector<std::pair<int, int>> out;
+  for (size_t c = 0; c + 1 < bounds.size(); ++c) {
+    const int n0 = bounds[c] * align, n1 = std::min(bounds[c + 1] * align, N);
+    if (n1 > n0) out.push_back({n0, n1});
+  }
+  return out;
+}
+
+static inline size_t up256(size_t x) { return (x + 255) / 256 * 256; }
+
+// tensor-core encoding the pipeline runs for `variant` (fp16 needs K >= 512 in every chunk GEMM)
+static int rowshard_tc(int variant, int rows, int K, const std::vector<std::pair<int, int>>& ch) {
+  if (variant == ELV_PARALLEL_FP16X3) {
+    for (auto& c : ch)
+      if (!fp16x3_applicable(std::max(rows, 1), c.second - c.first, K)) return ELV_PARALLEL_TF32X3;
+    return ELV_PARALLEL_FP16X3;
+  }
+  return variant == ELV_PARALLEL_TF32X3 ? ELV_PARALLEL_TF32X3 : 0;
+}
+
+size_t elv_gemm_rowshard_workspace_bytes(int variant, int rows, int N, int K, int chunks) {
+  if (rows < 1 || N < 1 || K < 1 || chunks < 1) return 0;
+  const auto ch = column_chunks(N, chunks);
+  const int tc = rowshard_tc(variant, rows, K, ch);
+  if (!tc) return 0;
+  const bool f16 = tc == ELV_PARALLEL_FP16X3;
+  size_t b = up256(f16 ? fp16x3_a_planes_bytes(rows, K) : tf32x3_a_planes_bytes(rows, K));
+  for (auto& c : ch) {
+    const int nc = c.second - c.first;
+    b += up256(f16 ? fp16x3_b_planes_bytes(nc, K) : tf32x3_b_planes_bytes(nc, K));
+  }
+  return b;
+}
+
+struct RsStreams { cudaStream_t comm = nullptr, prep = nullptr; };
+static std::map<int, RsStreams> g_rs_streams;     // per device, created once
+
+int elv_gemm_rowshard_pipelined(int variant, int ndev, const int* devs, const float* const* A_shards,
+                                const float* B_root, float* const* packedB_per_dev, float* const* C_shards,
+                                const int* rows, int N, int K, int chunks, void* const* workspaces,
+                                size_t workspace_bytes, void* const* streams) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (variant < ELV_ARRAYPACKING || variant > ELV_PARALLEL_FP16X3)
+    return set_error(ELV_EVARIANT, "gemm_rowshard_pipelined: variant %d not supported (4..8)", variant);
+  if (ndev < 1 || !devs || !A_shards || !B_root || !packedB_per_dev || !C_shards || !rows || !streams ||
+      N < 1 || K < 1 || chunks < 1)
+    return set_error(ELV_EINVAL, "gemm_rowshard_pipelined: bad arguments");
+  if ((int)g_comms.size() != ndev) return set_error(ELV_ENCCL, "gemm_rowshard_pipelined: call elv_nccl_init first");
+  for (int d = 0; d < ndev; ++d)
+    if (g_comm_devs[d] != devs[d])
+      return set_error(ELV_ENCCL, "gemm_rowshard_pipelined: device list differs from elv_nccl_init");
+  const auto ch = column_chunks(N, chunks);
+  const int nch = (int)ch.size();
+  int max_rows = 1;
+  for (int d = 0; d < ndev; ++d) max_rows = std::max(max_rows, rows[d]);
+  const int tc = rowshard_tc(variant, max_rows, K, ch);
+  const bool f16 = tc == ELV_PARALLEL_FP16X3;
+  if (tc) {
+    if (!workspaces) return set_error(ELV_EWORKSPACE, "gemm_rowshard_pipelined: workspaces required");
+    for (int d = 0; d < ndev; ++d)
+      if (rows[d] > 0 && (!workspaces[d] ||
+                          workspace_bytes < elv_gemm_rowshard_workspace_bytes(variant, max_rows, N, K, chunks)))
+        return set_error(ELV_EWORKSPACE, "gemm_rowshard_pipelined: workspace too small");
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  int rc = ELV_OK;
+  std::vector<cudaEvent_t> evs;                    // destroyed at the end (released once their work completes)
+  auto event = [&](cudaEvent_t* e) {
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return false;
+    evs.push_back(*e);
+    return true;
+  };
+  auto fail = [&](int code) { rc = code; };
+  std::vector<RsStreams> S(ndev);
+  std::vector<cudaEvent_t> entry(ndev);
+  for (int d = 0; d < ndev && !rc; ++d) {
+    cudaSetDevice(devs[d]);
+    RsStreams& r = g_rs_streams[devs[d]];
+    if (!r.comm) {
+      if (cudaStreamCreateWithFlags(&r.comm, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&r.prep, cudaStreamNonBlocking) != cudaSuccess)
+        fail(set_error(ELV_ECUDA, "gemm_rowshard_pipelined: stream creation"));
+    }
+    S[d] = r;
+    // the side streams start after the caller's earlier work on these buffers
+    if (!rc && (!event(&entry[d]) || cudaEventRecord(entry[d], (cudaStream_t)streams[d]) != cudaSuccess ||
+                cudaStreamWaitEvent(r.comm, entry[d], 0) != cudaSuccess ||
+                cudaStreamWaitEvent(r.prep, entry[d], 0) != cudaSuccess))
+      fail(set_error(ELV_ECUDA, "gemm_rowshard_pipelined: entry event"));
+  }
+  // root: pack each chunk; every device: broadcast it (one NCCL group per chunk)
+  std::vector<std::vector<cudaEvent_t>> landed(ndev, std::vector<cudaEvent_t>(nch));
+  for (int c = 0; c < nch && !rc; ++c) {
+    const int n0 = ch[c].first, nc = ch[c].second - ch[c].first;
+    const size_t panel = (size_t)(n0 / 32) * K * 32, count = (size_t)((nc + 255) / 256) * 256 * K;
+    cudaSetDevice(devs[0]);
+    cudaEvent_t packed;
+    if ((rc = launch_pack_b(B_root + n0, packedB_per_dev[0] + panel, K, nc, N, (cudaStream_t)streams[0]))) break;
+    if (!event(&packed) || cudaEventRecord(packed, (cudaStream_t)streams[0]) != cudaSuccess) {
+      fail(set_error(ELV_ECUDA, "gemm_rowshard_pipelined: pack event"));
+      break;
+    }
+    for (int d = 0; d < ndev; ++d) {
+      cudaSetDevice(devs[d]);
+      cudaStreamWaitEvent(S[d].comm, packed, 0);
+    }
+    ncclResult_t_ r = g_nccl.GroupStart();
+    if (r != 0) { fail(nccl_err(r, "ncclGroupStart")); break; }
+    for (int d = 0; d < ndev && !r; ++d) {
+      cudaSetDevice(devs[d]);
+      r = g_nccl.Broadcast(packedB_per_dev[0] + panel, packedB_per_dev[d] + panel, count, ncclFloat32_, 0, g_comms[d],
+                           S[d].comm);
+    }
+    const ncclResult_t_ r2 = g_nccl.GroupEnd();
+    if (r != 0 || r2 != 0) { fail(nccl_err(r ? r : r2, "ncclBroadcast")); break; }
+    for (int d = 0; d < ndev && !rc; ++d) {
+      cudaSetDevice(devs[d]);
+      if (!event(&landed[d][c]) || cudaEventRecord(landed[d][c], S[d].comm) != cudaSuccess)
+        fail(set_error(ELV_ECUDA, "gemm_rowshard_pipelined: broadcast event"));
+    }
+  }
+  // every device: (split chunk c on the side stream) -> GEMM chunk c (+ fix-up)
+  for (int d = 0; d < ndev && !rc; ++d) {
+    cudaSetDevice(devs[d]);
+    cudaStream_t st = (cudaStream_t)streams[d];
+    const int m = rows[d];
+    if (m <= 0) {
+      for (int c = 0; c < nch; ++c) cudaStreamWaitEvent(st, landed[d][c], 0);
+      continue;
+    }
+    const float* P = packedB_per_dev[d];
+    float* Cd = C_shards[d];
+    if (!tc) {
+      for (int c = 0; c < nch && !rc; ++c) {
+        const int n0 = ch[c].first, nc = ch[c].second - ch[c].first;
+        cudaStreamWaitEvent(st, landed[d][c], 0);
+        rc = launch_simt(variant, A_shards[d], nullptr, P + (size_t)(n0 / 32) * K * 32, Cd + n0, m, nc, K, K, 0, N,
+                         st);
+      }
+      continue;
+    }
+    uint8_t* ws = static_cast<uint8_t*>(workspaces[d]);
+    void* ap = ws;
+    size_t off = up256(f16 ? fp16x3_a_planes_bytes(max_rows, K) : tf32x3_a_planes_bytes(max_rows, K));
+    std::vector<void*> bp(nch);
+    std::vector<cudaEvent_t> split(nch);
+    for (int c = 0; c < nch && !rc; ++c) {
+      const int n0 = ch[c].first, nc = ch[c].second - ch[c].first;
+      bp[c] = ws + off;
+      off += up256(f16 ? fp16x3_b_planes_bytes(nc, K) : tf32x3_b_planes_bytes(nc, K));
+      cudaStreamWaitEvent(S[d].prep, landed[d][c], 0);
+      const float* Pc = P + (size_t)(n0 / 32) * K * 32;
+      rc = f16 ? fp16x3_split_b(Pc, K, nc, 0, bp[c], S[d].prep, 0, 0, true)
+               : tf32x3_split_b(Pc, K, nc, 0, true, bp[c], S[d].prep);
+      if (!rc && (!event(&split[c]) || cudaEventRecord(split[c], S[d].prep) != cudaSuccess))
+        fail(set_error(ELV_ECUDA, "gemm_rowshard_pipelined: split event"));
+    }
+    if (rc) break;
+    rc = f16 ? fp16x3_split_a(A_shards[d], m, K, K, ap, st) : tf32x3_split_a(A_shards[d], m, K, K, ap, st);
+    for (int c = 0; c < nch && !rc; ++c) {
+      const int n0 = ch[c].first, nc = ch[c].second - ch[c].first;
+      cudaStreamWaitEvent(st, split[c], 0);
+      rc = f16 ? fp16x3_gemm_planes(ap, bp[c], Cd + n0, m, nc, K, N, st)
+               : tf32x3_gemm_planes(ap, bp[c], Cd + n0, m, nc, K, N, st);
+      if (!rc)
+        rc = tc_fixup_planes(f16, ap, bp[c], A_shards[d], K, P + (size_t)(n0 / 32) * K * 32, 0, true, Cd + n0, N, m,
+                             nc, K, st);
+    }
+  }
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  cudaSetDevice(prev);
+  return rc;
+}
 }  // extern "C"

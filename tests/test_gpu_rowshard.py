@@ -398,3 +398,74 @@ def test_bench_gpus_flag_launches_ranks_itself(cuda):
     assert abs(max(d["ranks"]["per_rank_ms_per_step"]) - d["ms_per_step"]) < 1e-6
     assert d["ranks"]["broadcast_bytes_per_step"] == 4096 * 1024 * 4
     assert "with 2 ranks" in r.stderr
+
+
+def _rowshard_pipelined(lib, variant, devs, A_list, B_root, rows, N, K, chunks, streams):
+    """Call elv_gemm_rowshard_pipelined over len(devs) devices; returns the C shards."""
+    import ctypes
+    from paper_2002_02268_b200 import _lib
+    nd = len(devs)
+    vp = ctypes.c_void_p
+    cdevs = (ctypes.c_int * nd)(*devs)
+    P = [torch.empty(lib.elv_pack_b_bytes(K, N) // 4, device=torch.device("cuda", d)) for d in devs]
+    C = [torch.empty((r, N), device=torch.device("cuda", d)) for r, d in zip(rows, devs)]
+    wsb = lib.elv_gemm_rowshard_workspace_bytes(variant, max(rows), N, K, chunks)
+    W = [torch.empty(max(wsb, 1), dtype=torch.uint8, device=torch.device("cuda", d)) for d in devs]
+    arr = lambda xs: (vp * nd)(*[x.data_ptr() for x in xs])  # noqa: E731
+    rc = lib.elv_gemm_rowshard_pipelined(variant, nd, cdevs, arr(A_list), B_root.data_ptr(), arr(P), arr(C),
+                                         (ctypes.c_int * nd)(*rows), N, K, chunks, arr(W), wsb,
+                                         (vp * nd)(*streams))
+    _lib.check(rc, "elv_gemm_rowshard_pipelined")
+    for d in devs:
+        torch.cuda.synchronize(d)
+    return C
+
+
+@pytest.mark.parametrize("variant", [6, 7, 8])
+@pytest.mark.parametrize("chunks", [1, 4])
+def test_c_abi_pipelined_rowshard_bitwise(cuda, variant, chunks):
+    """elv_gemm_rowshard_pipelined (one process, ncclCommInitAll, chunked
+    packedB broadcast, split-on-arrival, GEMM + range-guard fix-up per chunk)
+    at ndev = 1: bitwise elv_gemm of the same variant, also with a guarded
+    row (the fix-up reads the broadcast packedB chunk)."""
+    import ctypes
+    from paper_2002_02268_b200 import _lib
+    lib = _lib.load()
+    devs = [0]
+    _lib.check(lib.elv_nccl_init(1, (ctypes.c_int * 1)(0)), "elv_nccl_init")
+    try:
+        M, N, K = 768, 2304, 1024
+        A = torch.empty((M, K), device=cuda); synth.fill_device(A, 8, 0)
+        B = torch.empty((K, N), device=cuda); synth.fill_device(B, 8, 1)
+        A[17, 5] = 2.0 ** -110                        # a range-guarded row for 7 / 8
+        st = torch.cuda.current_stream().cuda_stream
+        (C,) = _rowshard_pipelined(lib, variant, devs, [A], B, [M], N, K, chunks, [st])
+        ref = interp.gemm(_plan16(M, N, K) if variant == 8 else _plan(variant, M, N, K), A, B)
+        torch.cuda.synchronize()
+        assert torch.equal(C, ref)
+    finally:
+        lib.elv_nccl_destroy()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+@pytest.mark.parametrize("variant", [6, 7, 8])
+def test_c_abi_pipelined_rowshard_two_devices(cuda, variant):
+    """Two devices in one process: each shard bitwise equal to elv_gemm on it."""
+    import ctypes
+    from paper_2002_02268_b200 import _lib
+    lib = _lib.load()
+    devs = [0, 1]
+    _lib.check(lib.elv_nccl_init(2, (ctypes.c_int * 2)(*devs)), "elv_nccl_init")
+    try:
+        M, N, K = 1024, 4096, 1024
+        rows = [512, 512]
+        A = torch.empty((M, K), device=cuda); synth.fill_device(A, 9, 0)
+        B = torch.empty((K, N), device=cuda); synth.fill_device(B, 9, 1)
+        A_list = [A[:512].contiguous(), A[512:].to("cuda:1")]
+        streams = [torch.cuda.current_stream(0).cuda_stream, torch.cuda.current_stream(1).cuda_stream]
+        C0, C1 = _rowshard_pipelined(lib, variant, devs, A_list, B, rows, N, K, 4, streams)
+        ref = interp.gemm(_plan16(M, N, K) if variant == 8 else _plan(variant, M, N, K), A, B)
+        torch.cuda.synchronize()
+        assert torch.equal(C0, ref[:512]) and torch.equal(C1.cpu(), ref[512:].cpu())
+    finally:
+        lib.elv_nccl_destroy()
