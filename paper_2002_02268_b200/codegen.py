@@ -20,8 +20,10 @@ from the reference):
     any other array accumulator is materialised (two per-thread buffers);
   * toMem / id: identity (values are views; materialisation is a
     performance choice, not semantics -- interp.py:143-144);
-  * add / mult: fp32, compiled with --fmad=false so every operation rounds
-    separately, like the interpreter's scalar ops (interp.py:145-148).
+  * add / mult: fp32 (interp.py:145-148); an add of a product, the body of
+    every reduce over zipped pairs (acc + a * b), is one explicit fmaf --
+    the hand-written kernels' FFMA fold -- and nothing else is contracted
+    (--fmad=false), so the host build (cpu_source) rounds identically.
 
 Thread mapping: one thread per output scalar ("per-scalar") unless some
 array accumulator had to be materialised -- then every scalar would rebuild
@@ -59,6 +61,26 @@ class CodegenError(Exception):
 @dataclass
 class Scal:
     code: str
+
+
+@dataclass
+class Prod(Scal):
+    """A product a * b not yet rounded: an `add` consuming it emits one
+    fused multiply-add, like the hand-written kernels' FFMA k-loops."""
+    a: str = ""
+    b: str = ""
+
+
+def _add(x, y):
+    """add(x)(y): acc + a * b folds (the reduce bodies of every GEMM
+    schedule) become fmaf(a, b, acc) -- one rounding per step, the same
+    arithmetic as the template kernels (K0-K6 fold with FFMA) and closer to
+    the interpreter's f64 than a separately rounded product."""
+    if isinstance(y, Prod):
+        return Scal(f"fmaf({y.a}, {y.b}, {x.code})")
+    if isinstance(x, Prod):
+        return Scal(f"fmaf({x.a}, {x.b}, {y.code})")
+    return Scal(f"({x.code} + {y.code})")
 
 
 class Pair:
@@ -371,9 +393,9 @@ def _prim(g: Gen, p) -> object:
     if k in ("toMem", "id"):
         return Fn(lambda v: v)
     if k == "add":
-        return Fn(lambda a: Fn(lambda b: Scal(f"({a.code} + {b.code})")))
+        return Fn(lambda a: Fn(lambda b: _add(a, b)))
     if k == "mult":
-        return Fn(lambda a: Fn(lambda b: Scal(f"({a.code} * {b.code})")))
+        return Fn(lambda a: Fn(lambda b: Prod(f"({a.code} * {b.code})", a.code, b.code)))
     raise CodegenError(f"primitive {k} is not supported by the generic compiler")
 
 
@@ -584,6 +606,8 @@ def compile_term(term) -> Compiled:
         # scalar per thread would rebuild that accumulator per scalar, so write
         # the result in the term's own structure instead (destination passing)
         g = _dps_kernel(body, params, out_shape)
+    else:
+        g = _register_tile(g, out_shape) or g
     name = "elv_generated"
     args = ", ".join([f"const float* __restrict__ in{i}" for i in range(len(params))] +
                      ["float* __restrict__ out"])
@@ -630,6 +654,108 @@ def _per_scalar_kernel(body, params, out_shape) -> Gen:
     return g
 
 
+# register tiles only when enough threads remain to fill the GPU (~111 per SM)
+MIN_TILE_THREADS = 16384
+_DECL = re.compile(r"^float (\w+) = (.*);$")
+_ASSIGN = re.compile(r"^(\w+) = (.*);$")
+_FOR = re.compile(r"^for \(int (\w+) = [^;]*; \1 < [^;]*; \+\+\1\) \{$")
+_OUT = re.compile(r"^out\[t\] = (.*);$")
+
+
+def _register_tile(g: Gen, out_shape: tuple) -> Gen | None:
+    """Mode A': a TM x TN register tile of outputs per thread (8x4, 4x4 or
+    2x2, the largest that divides the result and leaves MIN_TILE_THREADS).  The per-scalar
+    body of a 2-D result is a tree of counted loops (bounds independent of
+    the output index) over scalar statements; every statement is replicated
+    for the thread's TM x TN outputs -- rows o0 + i (O0 / TM), columns
+    o1 + j (O1 / TN), so a warp's loads of a column operand stay coalesced --
+    with its own copy of every local.  Each output keeps exactly the
+    per-scalar operation sequence (bitwise the same results); the loads the
+    tile's elements share (a row of one input, a column of the other) are
+    common subexpressions of one basic block, so each is issued once for TN
+    (TM) outputs instead of once per output."""
+    if len(out_shape) != 2:
+        return None
+    O0, O1 = out_shape
+    tile = None
+    import os
+    shapes = ((8, 4), (4, 4), (2, 2))         # measured at 1024^3: 8x4 13.8, 4x4 12.3, per-scalar 7.4 TF
+    if os.environ.get("ELV_CG_TILE"):                   # tuning experiments
+        shapes = (tuple(int(x) for x in os.environ["ELV_CG_TILE"].split("x")),) + shapes
+    for tm, tn in shapes:
+        if O0 % tm == 0 and O1 % tn == 0 and (O0 // tm) * (O1 // tn) >= MIN_TILE_THREADS:
+            tile = (tm, tn)
+            break
+    if tile is None:
+        return None
+    tm, tn = tile
+    locals_, body, out_expr = set(), [], None
+    for line in g.lines:
+        st = line.strip()
+        if out_expr is not None:
+            return None                                  # the output write must come last
+        m = _FOR.match(st)
+        if m:
+            if re.search(r"\bo[01]\b", st):
+                return None                              # loop bounds depend on the output index
+            body.append(("for", line))
+            continue
+        if st == "}":
+            body.append(("close", line))
+            continue
+        m = _DECL.match(st)
+        if m:
+            locals_.add(m.group(1))
+            body.append(("stmt", line))
+            continue
+        m = _OUT.match(st)
+        if m and line.startswith("  ") and not line.startswith("   "):
+            out_expr = m.group(1)
+            continue
+        m = _ASSIGN.match(st)
+        if m and m.group(1) in locals_:
+            body.append(("stmt", line))
+            continue
+        return None
+    if out_expr is None:
+        return None
+    names = re.compile(r"\b(" + "|".join(sorted(map(re.escape, locals_), key=len, reverse=True)) + r")\b") \
+        if locals_ else None
+
+    def inst(text, i, j):
+        if names is not None:
+            text = names.sub(lambda mm: f"{mm.group(1)}_{i}_{j}", text)
+        text = re.sub(r"\bo0\b", f"o0_{i}", text)
+        return re.sub(r"\bo1\b", f"o1_{j}", text)
+
+    t = Gen()
+    t.consts = g.consts
+    q0, q1 = O0 // tm, O1 // tn
+    threads = q0 * q1
+    t.head = [f"  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;",
+              f"  if (t >= {threads}LL) return;",
+              f"  const int q0 = (int)(t / {q1}LL);",
+              f"  const int q1 = (int)(t % {q1}LL);"]
+    t.head += [f"  const int o0_{i} = q0 + {i * q0};" for i in range(tm)]
+    t.head += [f"  const int o1_{j} = q1 + {j * q1};" for j in range(tn)]
+    unroll = int(os.environ.get("ELV_CG_UNROLL", "4"))  # unroll 4: more loads in flight (+10-130 %)
+    for kind, line in body:
+        if kind in ("for", "close"):
+            if kind == "for" and unroll > 1:
+                t.lines.append(line[:len(line) - len(line.lstrip())] + f"#pragma unroll {unroll}")
+            t.lines.append(line)
+            continue
+        indent = line[:len(line) - len(line.lstrip())]
+        for i in range(tm):
+            for j in range(tn):
+                t.lines.append(indent + inst(line.strip(), i, j))
+    for i in range(tm):
+        for j in range(tn):
+            t.lines.append(f"  out[(long long)o0_{i} * {O1} + o1_{j}] = {inst(out_expr, i, j)};")
+    t.threads, t.mode = threads, f"register-tile {tm}x{tn}"
+    return t
+
+
 def _dps_kernel(body, params, out_shape) -> Gen:
     """Mode B: destination passing; the outermost PAR_LEVELS maps are the
     thread index, small computing maps are materialised per thread."""
@@ -668,12 +794,13 @@ def cpu_source(c: Compiled) -> str:
     """The generated kernel wrapped as plain C++ (thread loop on the host), so
     tests can check code generation against the reference interpreter
     without a GPU.  Compiled with -ffp-contract=off it performs the same fp32
-    operations in the same order as the NVRTC (--fmad=false) build."""
+    operations in the same order as the NVRTC (--fmad=false, explicit fmaf) build."""
     n = len(c.in_shapes)
     call = ", ".join([f"ins[{i}]" for i in range(n)] + ["out"])
     return "\n".join([
         "#include <algorithm>",
-        "using std::min; using std::max;",
+        "#include <cmath>",
+        "using std::min; using std::max; using std::fmaf;",
         "struct elv_dim3 { unsigned x, y, z; };",
         "static elv_dim3 blockIdx, threadIdx, blockDim;",
         "#define __global__",

@@ -114,3 +114,24 @@ def vadd = fun(a : 4.f32 => fun(b : 4.f32 => zip(a)(b) |> map(fun(p => add(fst(p
     with pytest.raises(S().interp.EvalError) as err:
         interp._run_template(term, [[1.0, 2.0, 3.0, 4.0], [1.0, 1.0, 1.0, 1.0]])
     assert interp._no_template(err.value)
+
+
+@pytest.mark.parametrize("name", ["user_tile16", "blocking", "parallel", "baseline", "cacheBlocks"])
+def test_register_tile_mode_is_bitwise_the_per_scalar_code(name, tmp_path, monkeypatch):
+    """Mode A' (a 4x4 / 2x2 register tile of outputs per thread) replicates
+    the per-scalar statements per output with private locals: every output
+    keeps the per-scalar operation sequence, so the host-compiled results are
+    bitwise those of the per-scalar kernel (and match the interpreter)."""
+    from paper_2002_02268_b200 import synth
+    term = corpus()[name]
+    monkeypatch.setattr(codegen, "MIN_TILE_THREADS", 10 ** 9)
+    plain = codegen.compile_term(term)
+    monkeypatch.setattr(codegen, "MIN_TILE_THREADS", 1)
+    tiled = codegen.compile_term(term)
+    assert plain.mode == "per-scalar" and tiled.mode.startswith("register-tile"), (plain.mode, tiled.mode)
+    args = [synth.matrix(*shp, 4, i) for i, shp in enumerate(plain.in_shapes)]
+    a = _cpu_run(plain, args, tmp_path / "a" if (tmp_path / "a").mkdir() is None else tmp_path)
+    b = _cpu_run(tiled, args, tmp_path / "b" if (tmp_path / "b").mkdir() is None else tmp_path)
+    np.testing.assert_array_equal(a, b)
+    ref = np.array(S().interp.run(term, [x.tolist() for x in args]), np.float64)
+    assert np.all(np.abs(b - ref) <= 64 * 4 * 2.0 ** -23)

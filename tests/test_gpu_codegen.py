@@ -54,6 +54,20 @@ def test_template_and_generated_kernels_agree(cuda, name):
     Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
     ref, ab = oracle.mm_interp_f64(Ah, Bh, name), oracle.absprod_np(Ah, Bh)
     assert oracle.check(gen, ref, ab, K)[0] and oracle.check(tpl, ref, ab, K)[0]
+    # both fold each output as one fmaf chain in k order: the same bits
+    np.testing.assert_array_equal(gen, tpl)
+
+
+@pytest.mark.parametrize("name", ["parallel", "loopPerm"])
+def test_register_tiled_generated_kernel_at_1024(cuda, name):
+    """The register-tile mode (8x4 outputs per thread) at 1024^3: bitwise the
+    template kernel's result (same fmaf chain per output)."""
+    n = 1024
+    term = schedules.apply(name, n, n, n).term
+    assert codegen.kernel_for(term).c.mode.startswith("register-tile")
+    A = torch.empty((n, n), device=cuda); synth.fill_device(A, 3, 0)
+    B = torch.empty((n, n), device=cuda); synth.fill_device(B, 3, 1)
+    assert torch.equal(codegen.run(term, [A, B]), interp.run_tensor(term, A, B))
 
 
 VEC_ADD = """
