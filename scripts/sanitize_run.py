@@ -36,6 +36,45 @@ def main():
             ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
             print(f"{v:16s} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
             assert ok
+    # range guard: marked rows / columns recomputed by the fix-up (both encodings)
+    M, N, K = 160, 200, 576
+    A = synth.matrix(M, K, 8, 0)
+    B = synth.matrix(K, N, 8, 1)
+    A[7, 3] = 2.0 ** -110
+    B[9, 11] = 2.0 ** -110
+    ref, ab = oracle.mm_f64(A, B), oracle.absprod_np(A, B)
+    for enc in ("tf32", "fp16"):
+        term = schedules.apply_padded("parallel", M, N, K).term
+        C = interp.run_tensor(term, torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), tf32x3=True,
+                              tc_encoding=enc)
+        torch.cuda.synchronize()
+        ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
+        print(f"guarded {enc} ok={ok} worst={worst:.3f}", flush=True)
+        assert ok
+    # the C-ABI pipelined row shard at ndev = 1 (NCCL broadcast in chunks, split on arrival)
+    import ctypes
+    from paper_2002_02268_b200 import _lib
+    lib = _lib.load()
+    _lib.check(lib.elv_nccl_init(1, (ctypes.c_int * 1)(0)), "nccl_init")
+    try:
+        Ad, Bd = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+        for v in (6, 7, 8):
+            P = torch.empty(lib.elv_pack_b_bytes(K, N) // 4, device=dev)
+            C = torch.empty((M, N), device=dev)
+            wsb = lib.elv_gemm_rowshard_workspace_bytes(v, M, N, K, 2)
+            W = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+            vp = ctypes.c_void_p
+            rc = lib.elv_gemm_rowshard_pipelined(v, 1, (ctypes.c_int * 1)(0), (vp * 1)(Ad.data_ptr()), Bd.data_ptr(),
+                                                 (vp * 1)(P.data_ptr()), (vp * 1)(C.data_ptr()),
+                                                 (ctypes.c_int * 1)(M), N, K, 2, (vp * 1)(W.data_ptr()), wsb,
+                                                 (vp * 1)(torch.cuda.current_stream().cuda_stream))
+            _lib.check(rc, "rowshard_pipelined")
+            torch.cuda.synchronize()
+            ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
+            print(f"rowshard_pipelined v{v} ok={ok} worst={worst:.3f}", flush=True)
+            assert ok
+    finally:
+        lib.elv_nccl_destroy()
     # host pipeline (elv_gemm_host) with ragged tiles
     os.environ["ELV_HOST_TILES"] = "96,160"
     M, N, K = 200, 300, 70
