@@ -116,6 +116,26 @@ int elv_tf32x3_split_b_packed(const float* packedB, int K, int N, void* b_planes
 int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
                            int M, int N, int K, int ldc, void* stream);
 
+/* 3xTF32 with the split fused into the GEMM (no preparation pass): one
+ * tcgen05 pair kernel reads raw fp32 A (M x K, lda) and B (K x N row-major,
+ * ldb) by TMA and splits them in shared memory; bitwise the result of
+ * split_a ; split_b ; gemm_planes.  Applicable (elv_tf32x3_fused_ok) when the
+ * problem has >= 148 256x256 tiles and A, B, lda, ldb are 16-byte aligned;
+ * elv_gemm / elv_gemm_compute (variant 7) use it then only with
+ * ELV_TF32X3_FUSED=1 (measured slower than the planes path).  `flags` is caller
+ * scratch of (M + N) u32: zeroed and filled with the range-guard marks, and
+ * the range-guard fix-up is run before returning (asynchronously on
+ * `stream`). */
+int elv_tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N);
+int elv_tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+                          int M, int N, int K, unsigned int* flags, void* stream);
+/* The same kernel with B already split (elv_tf32x3_split_b / _split_b_packed
+ * planes of these N columns, e.g. a broadcast chunk split on arrival): only
+ * A is split in the kernel.  B (row-major, ldb) is read only by the
+ * range-guard fix-up; flags_a is caller scratch of M u32. */
+int elv_tf32x3_gemm_fused_a(const float* A, int lda, const void* b_planes, const float* B, int ldb,
+                            float* C, int ldc, int M, int N, int K, unsigned int* flags_a, void* stream);
+
 /* Host-resident operands (the reference's own calling convention:
  * interp.run takes and returns host values, interp.py:157-162).
  * C_h = A_h . B_h; A_h, B_h, C_h are HOST pointers (pinned for overlap).

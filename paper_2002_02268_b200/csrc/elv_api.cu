@@ -348,6 +348,43 @@ int elv_fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
   return fp16x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
 }
 
+int elv_tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N) {
+  if (bad_ptr(A) || bad_ptr(B) || M < 1 || N < 1) return 0;
+  return tf32x3_fused_ok(A, lda, B, ldb, M, N) ? 1 : 0;
+}
+
+int elv_tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N, int K,
+                          unsigned int* flags, void* stream) {
+  int rc = check_args(A, B, C, M, N, K, lda, ldb, ldc, true);
+  if (rc) return rc;
+  if (bad_ptr(flags)) return set_error(ELV_EINVAL, "tf32x3_gemm_fused: null flags");
+  if (!tf32x3_fused_ok(A, lda, B, ldb, M, N))
+    return set_error(ELV_EINVAL, "tf32x3_gemm_fused: not applicable (needs >= 148 pair tiles, 16 B alignment)");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(flags, 0, (size_t)(M + N) * 4, st) != cudaSuccess)
+    return set_error(ELV_ECUDA, "tf32x3_gemm_fused: memset");
+  rc = tf32x3_gemm_fused(A, lda, B, ldb, C, ldc, M, N, K, flags, flags + M, st);
+  if (rc) return rc;
+  return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, flags, flags + M, st);
+}
+
+int elv_tf32x3_gemm_fused_a(const float* A, int lda, const void* b_planes, const float* B, int ldb, float* C,
+                            int ldc, int M, int N, int K, unsigned int* flags_a, void* stream) {
+  int rc = check_args(A, B, C, M, N, K, lda, ldb, ldc, true);
+  if (rc) return rc;
+  if (bad_ptr(flags_a) || bad_ptr(b_planes)) return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: null pointer");
+  if (!tf32x3_fused_ok(A, lda, A, 4, M, N))
+    return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: not applicable (needs >= 148 pair tiles, 16 B alignment)");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(flags_a, 0, (size_t)M * 4, st) != cudaSuccess)
+    return set_error(ELV_ECUDA, "tf32x3_gemm_fused_a: memset");
+  const unsigned int* flag_b = tf32x3_b_planes_flags(b_planes, N, K);
+  rc = tf32x3_gemm_fused(A, lda, nullptr, 0, C, ldc, M, N, K, flags_a, const_cast<unsigned int*>(flag_b), st,
+                         b_planes, N, 0);
+  if (rc) return rc;
+  return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, flags_a, flag_b, st);
+}
+
 int elv_tc_fixup(int encoding, const void* a_planes, const void* b_planes, const float* A, int lda, const float* B,
                  int ldb, int b_packed, float* C, int ldc, int M, int N, int K, void* stream) {
   if (encoding != ELV_PARALLEL_TF32X3 && encoding != ELV_PARALLEL_FP16X3)

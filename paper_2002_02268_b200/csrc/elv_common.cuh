@@ -94,6 +94,13 @@ int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_p
                    int total = 0, int c0 = 0);
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                        cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0);
+const unsigned int* tf32x3_b_planes_flags(const void* b_planes, int N, int K);
+bool tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N);
+int tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N, int K,
+                      unsigned int* flag_a, unsigned int* flag_b, cudaStream_t st, const void* b_planes = nullptr,
+                      int b_total = 0, int c0 = 0);
+int tc_fixup(const float* A, int lda, const float* B, int ldb, bool b_packed, float* C, int ldc, int M, int N, int K,
+             const unsigned int* flag_a, const unsigned int* flag_b, cudaStream_t st);
 int launch_split_tf32(const float* X, float* hi, float* lo, long long n, cudaStream_t st);
 // 3xFP16 encoding of the parallel schedule's tcgen05 kernel (tf32x3_gemm.cu)
 bool fp16x3_applicable(int M, int N, int K);

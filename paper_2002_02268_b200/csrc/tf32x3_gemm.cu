@@ -1093,6 +1093,408 @@ k_tc_fixup(const float* __restrict__ A, int lda, const float* __restrict__ B, in
 }
 
 // ----------------------------------------------------------------------------
+// K7F: 3xTF32 with the operand split fused into the pair kernel -- no
+// preparation pass.  The producers TMA the RAW fp32 tiles: A (K-major, as
+// the planes kernel's A_hi box) into the A_hi slot, B (row-major K x N, four
+// [32 k][32 n] boxes, 128B swizzle) into the B_lo slot.  Dedicated converter
+// warps split each landed stage -- A in place (hi over the raw tile, lo into
+// A_lo, same swizzled offsets), B transposed into the K-major B_hi / B_lo
+// rows the MMA reads (kind::tf32 takes K-major operands only: an MN-major B
+// descriptor produced no result, scripts/probes/tf32_mn_probe.cu) -- with the
+// planes split's arithmetic, so the result is bitwise the planes path's.
+// The range guard (tf32_out_of_window) is applied to the converted elements
+// (every tile sees the full K of its rows and columns).  Barriers per stage:
+// full[s] (local TMA), conv[s] (leader: its converters + the peer's
+// converted stage, relayed by the peer's warp 2 with a cluster release),
+// empty[s] (MMA done, multicast commit).
+// Measured: the conversion sits between TMA landing
+// and the MMA with only three 64 KB stages of slack in 227 KB of SMEM, and
+// the pipeline has none to spare -- the same kernel with the conversion
+// skipped runs at 261 TF (planes path 250 TF) but converting A alone costs
+// ~17 % and A and B ~30-45 % at 32768^2 x 8192 -- so variant 7 keeps the
+// planes path by default (ELV_TF32X3_FUSED=1 selects this one).
+constexpr int F_STAGES = 3;
+constexpr int F_A_TILE = P_BM * 128;                       // 128 rows x 32 k fp32 (128 B rows)
+constexpr int F_B_TILE = (P_BN / 2) * 128;                 // this CTA's 128 columns x 32 k
+constexpr int F_STAGE = 2 * F_A_TILE + 2 * F_B_TILE;       // [A_hi | A_lo | B_hi | B_lo]
+constexpr int F_EPI = 8 * 32 * 32 * 4;
+constexpr int F_SMEM = F_STAGES * F_STAGE + F_EPI + 256 + 1024;
+constexpr uint32_t F_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(a), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// 16 warps: warpgroup 0 = TMA producer (w0), MMA issuer (w1, leader), the
+// cross-CTA relay (w2), a converter (w3); warpgroups 1-2 = epilogue (w4..w11,
+// TMEM lane group w & 3, column half (w - 4) >> 2); warpgroup 3 = converters
+// (w12..w15).  setmaxnreg gives the epilogue 168 registers (128 running sums
+// per thread) and the other warpgroups 88.
+constexpr int F_NUM_THREADS = 512;
+constexpr int F_CONV_WARPS = 5;
+constexpr int F_EPI_W0 = 4;
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+// the planes split (split_a_block): hi = rna_tf32(x), lo = rna_tf32(x - hi).
+// (A truncated hi -- what kind::tf32 MMAs read from a raw fp32 operand,
+// scripts/probes/tf32_mn_probe.cu -- would let the raw TMA tile serve as the
+// hi operand without a write, but leaves |x - hi - lo| up to 2^-21 |x| instead
+// of 2^-23: 3.5x the tau = 2 bound at K = 1, tests/test_gpu_parity.py.)
+// Range-guard accumulators over a group of elements: `tiny` = min over
+// (2|x| bits - 2) (wraps for zeros, so only 0 < |x| < 2^-100 can land below
+// 2 * 0x0d800000 - 2), `fin` = sum of the lo parts (NaN iff some element is
+// inf / NaN: inf - trunc(inf) = NaN; finite lo sums cannot overflow).
+struct Guard {
+  uint32_t tiny = 0xffffffffu;
+  float fin = 0.f;
+  __device__ __forceinline__ void add(float x, float lo) {
+    tiny = min(tiny, (__float_as_uint(x) << 1) - 2u);
+    fin += lo;
+  }
+  __device__ __forceinline__ bool bad() const { return tiny < 2u * 0x0d800000u - 2u || !(fabsf(fin) <= 3.402823466e38f); }
+};
+
+// One launch per GEMM.  FUSE_B: B is split (and transposed) in the kernel
+// from raw row-major B; otherwise ("A-fused") B arrives as tf32 hi/lo planes
+// (map_b, map_b2: the planes kernel's K-major Bt boxes, e.g. a broadcast
+// chunk split on arrival) and only A is split here.
+template <bool TMA_C, bool FUSE_B>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F_NUM_THREADS, 1)
+k7f_tf32x3_fused(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_b2, const __grid_constant__ CUtensorMap map_c,
+                 float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
+                 unsigned int* __restrict__ wave_ctr, unsigned int* __restrict__ flag_a,
+                 unsigned int* __restrict__ flag_b, int dbg) {
+  constexpr int NC = P_BN / 2 / 32;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_stage = smem + F_STAGES * F_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + F_EPI);   // this CTA's TMA landed
+  uint64_t* conv = full + F_STAGES;                  // converted (leader: + the peer's relayed arrival)
+  uint64_t* empty = conv + F_STAGES;
+  uint64_t* tfull = empty + F_STAGES;                // [2]
+  uint64_t* tempty = tfull + 2;                      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int tiles_m = (M + 2 * P_BM - 1) / (2 * P_BM), tiles_n = (N + P_BN - 1) / P_BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+  constexpr int TX = F_A_TILE + (FUSE_B ? 1 : 2) * F_B_TILE;   // bytes per full[s] phase
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a); tma_prefetch_desc(&map_b);
+    if (!FUSE_B) tma_prefetch_desc(&map_b2);
+    if (TMA_C) tma_prefetch_desc(&map_c);
+    for (int s = 0; s < F_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], F_CONV_WARPS + (leader ? 1 : 0));
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * P_EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  griddep_wait();                                   // flags zeroed / operands written by preceding work
+  griddep_launch_dependents();                      // the range-guard fix-up may be scheduled (it waits for us)
+
+  auto coords = [&](int t, int& m0, int& n0) {
+    const int per_group = group * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * group;
+    const int gm = min(tiles_m - first_m, group);
+    const int in = t - g * per_group;
+    m0 = (first_m + in % gm) * 2 * P_BM;
+    n0 = (in / gm) * P_BN;
+  };
+
+  if (warp >= F_EPI_W0 && warp < F_EPI_W0 + P_EPI_WARPS) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
+    // ---------------- epilogue (w4..w11, both CTAs): as k7_tf32x3_pair ----------------
+    const int g = warp & 3;
+    const int h = (warp - F_EPI_W0) >> 2;
+    const bool vecC = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (ldc & 3) == 0;
+    const uint32_t tempty0 = mapa_rank(smem_u32(&tempty[0]), 0);
+    uint32_t q = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      int m0, n0;
+      coords(t, m0, n0);
+      const int row = m0 + (int)rank * P_BM + g * 32 + lane;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (P_BN / 2));
+      float acc[NC * 32];
+#pragma unroll
+      for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
+#pragma unroll 1
+      for (int kb = 0; kb < num_kb; ++kb, ++q) {
+        const uint32_t b = q & 1;
+        mbar_wait(&tfull[b], (q >> 1) & 1);
+        tc_fence_after();
+        drain_add<NC>(lane_base + b * (uint32_t)P_BN, acc);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + b * 8);
+      }
+      float* crow = C + (size_t)row * ldc;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int col = n0 + h * (P_BN / 2) + c * 32;
+        float* v = acc + c * 32;
+        if (TMA_C) {
+          const uint32_t tile = smem_u32(epi_stage + (warp - F_EPI_W0) * 4096);
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            sts128(tile + (uint32_t)(lane * 128 + ((j ^ (lane & 7)) << 4)), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                   v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&map_c)),
+                "r"(col), "r"(row - lane), "r"(tile)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else if (row < M && col < N) {
+          if (vecC && col + 31 < N) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(crow + col + 4 * j) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < N) crow[col + j] = v[j];
+          }
+        }
+      }
+    }
+    if (TMA_C && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+    if (warp == 0) {
+      if (lane == 0) {
+        // ---------------- TMA producer (both CTAs) ----------------
+        // raw A -> A_hi slot; FUSE_B: raw B (4 boxes [32 k][32 n], 128B swizzle)
+        // -> B_lo slot, else the B planes -> B_hi / B_lo; on this CTA's barrier
+        int s = 0; uint32_t ph = 0;
+        int wave = 0;
+        for (int t = cluster_id; t < num_tiles; t += num_clusters, ++wave) {
+          int m0, n0;
+          coords(t, m0, n0);
+          if (wave_ctr != nullptr && wave > 0) wave_sync_wait(wave_ctr, (unsigned)(wave * gridDim.x));
+          const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (P_BN / 2);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* st = smem + s * F_STAGE;
+            const int k0 = kb * 32;
+            mbar_expect_tx(&full[s], TX);
+            tma_load_2d(&map_a, &full[s], st, k0, ma);
+            if (FUSE_B) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                tma_load_2d(&map_b, &full[s], st + 2 * F_A_TILE + F_B_TILE + j * 4096, nb + 32 * j, k0);
+            } else {
+              tma_load_2d(&map_b, &full[s], st + 2 * F_A_TILE, k0, nb);
+              tma_load_2d(&map_b2, &full[s], st + 2 * F_A_TILE + F_B_TILE, k0, nb);
+            }
+            if (++s == F_STAGES) { s = 0; ph ^= 1; }
+          }
+          if (wave_ctr != nullptr) atomicAdd(wave_ctr, 1u);
+        }
+      }
+    } else if (warp == 1) {
+      if (leader && lane == 0) {
+        // ---------------- MMA issuer (leader CTA): one chunk per k-block ----------------
+        // the k7_tf32x3_pair chunk (hi.lo, lo.hi, [lo.lo], hi.hi; same order, same bits)
+        int s = 0; uint32_t ph = 0;
+        uint32_t q = 0;
+        for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+          for (int kb = 0; kb < num_kb; ++kb, ++q) {
+            const uint32_t b = q & 1, d = tmem_base + b * (uint32_t)P_BN;
+            mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
+            const uint32_t st = smem_u32(smem + s * F_STAGE);
+            const uint64_t ahi = umma_desc_sw128(st), alo = umma_desc_sw128(st + F_A_TILE);
+            const uint64_t bhi = umma_desc_sw128(st + 2 * F_A_TILE);
+            const uint64_t blo = umma_desc_sw128(st + 2 * F_A_TILE + F_B_TILE);
+            mbar_wait_cluster(&conv[s], ph);     // both CTAs' stages converted
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tc_mma_pair<false>(d, ahi + 2 * k, blo + 2 * k, F_IDESC, k != 0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tc_mma_pair<false>(d, alo + 2 * k, bhi + 2 * k, F_IDESC, 1u);
+            if (with_lolo) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) tc_mma_pair<false>(d, alo + 2 * k, blo + 2 * k, F_IDESC, 1u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tc_mma_pair<false>(d, ahi + 2 * k, bhi + 2 * k, F_IDESC, 1u);
+            tc_commit_pair(&empty[s]);
+            tc_commit_pair(&tfull[b]);
+            if (++s == F_STAGES) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    } else if (warp == 2) {
+      if (lane == 0) {
+        // ---------------- cross-CTA relay (peer): "my stage is converted" ----------------
+        // -> the leader's conv[s] with cluster release (one thread pays the
+        // release fence, off the converters' path)
+        int s = 0; uint32_t ph = 0;
+        const uint32_t conv0 = mapa_rank(smem_u32(&conv[0]), 0);
+        if (!leader) {
+          for (int t = cluster_id; t < num_tiles; t += num_clusters)
+            for (int kb = 0; kb < num_kb; ++kb) {
+              mbar_wait(&conv[s], ph);
+              mbar_arrive_release_cluster(conv0 + (uint32_t)(s * 8));
+              if (++s == F_STAGES) { s = 0; ph ^= 1; }
+            }
+        }
+      }
+    } else {
+      // ---------------- converters (w3, w12..w15; both CTAs) ----------------
+      // Work per stage: B = 8 items of 32 lanes x (4 n x 4 k) (FUSE_B), A = 32
+      // items of 32 float4.  Converter c takes B items {c, c + 5} and A items
+      // [start[c], start[c + 1]) -- ~52 elements per lane each (A-fused: 6-7 A
+      // items).  All loads of a stage are issued before any arithmetic.
+      const int cw = warp == 3 ? 0 : warp - 11;            // 0..4
+      constexpr uint64_t kAStart = 0ull | (5ull << 6) | (10ull << 12) | (15ull << 18) | (23ull << 24) |
+                                   (32ull << 30);
+      const int a_lo = FUSE_B ? (int)((kAStart >> (6 * cw)) & 63) : (32 * cw) / F_CONV_WARPS;
+      const int a_hi = FUSE_B ? (int)((kAStart >> (6 * cw + 6)) & 63) : (32 * (cw + 1)) / F_CONV_WARPS;
+      // B lane mapping (lane = 8 Q + e): k chunk kc = 4 (Q & 1) + (e >> 1), column
+      // group cg (n = 4 cg .. 4 cg + 3) from e & 1, (e >> 2) ^ (item >> 2), Q >> 1,
+      // item & 3.  Every quarter-warp of a 128-bit access then touches 8
+      // distinct 16-byte bank groups both in the raw tile (128B-swizzled TMA
+      // boxes) and in the K-major hi/lo rows: conflict-free reads and writes.
+      const int Q = lane >> 3, e = lane & 7;
+      const int kc = 4 * (Q & 1) + (e >> 1);
+      int s = 0; uint32_t ph = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int m0, n0;
+        coords(t, m0, n0);
+        const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (P_BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          const uint32_t st = smem_u32(smem + s * F_STAGE);
+          const uint32_t b_raw = st + 2 * F_A_TILE + F_B_TILE;
+          float4 r[2][4];
+          if (FUSE_B && !(dbg & 2)) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int item = cw + 5 * u;
+              if (item < 8) {
+                const int cg = (e & 1) | ((((e >> 2) ^ (item >> 2)) & 1) << 1) | ((Q >> 1) << 2) | ((item & 3) << 3);
+                const uint32_t box = b_raw + (uint32_t)((cg >> 3) * 4096);
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                  const int k = 4 * kc + qq;
+                  r[u][qq] = lds128(box + (uint32_t)(k * 128 + (((cg & 7) ^ (k & 7)) << 4)));
+                }
+              }
+            }
+          }
+          // A: hi (in place) and lo from the raw tile at the same (swizzled) offsets
+          if (!(dbg & 1)) {
+            constexpr int AMAX = FUSE_B ? 9 : 7;           // most A items of one converter
+            float4 xa[AMAX];
+#pragma unroll
+            for (int j = 0; j < AMAX; ++j)
+              if (a_lo + j < a_hi) xa[j] = lds128(st + (uint32_t)(((a_lo + j) * 32 + lane) * 16));
+#pragma unroll
+            for (int j = 0; j < AMAX; ++j) {
+              if (a_lo + j < a_hi) {
+                const int i = (a_lo + j) * 32 + lane;             // float4 index; tile row i / 8
+                const float4 x = xa[j];
+                const float h0 = tf32_rna(x.x), h1 = tf32_rna(x.y), h2 = tf32_rna(x.z), h3 = tf32_rna(x.w);
+                const float l0 = tf32_rna(x.x - h0), l1 = tf32_rna(x.y - h1), l2 = tf32_rna(x.z - h2),
+                            l3 = tf32_rna(x.w - h3);
+                sts128(st + (uint32_t)(i * 16), h0, h1, h2, h3);
+                sts128(st + F_A_TILE + (uint32_t)(i * 16), l0, l1, l2, l3);
+                Guard gd;
+                gd.add(x.x, l0); gd.add(x.y, l1); gd.add(x.z, l2); gd.add(x.w, l3);
+                if (gd.bad()) flag_a[ma + (i >> 3)] = 1u;
+              }
+            }
+          }
+          if (FUSE_B) {
+            asm volatile("bar.sync 1, 160;" ::: "memory");   // every raw B element read before the slot is overwritten
+            if (!(dbg & 2)) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int item = cw + 5 * u;
+                if (item < 8) {
+                  const int cg = (e & 1) | ((((e >> 2) ^ (item >> 2)) & 1) << 1) | ((Q >> 1) << 2) | ((item & 3) << 3);
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const int n = 4 * cg + i;
+                    const float x0 = (&r[u][0].x)[i], x1 = (&r[u][1].x)[i], x2 = (&r[u][2].x)[i], x3 = (&r[u][3].x)[i];
+                    const float h0 = tf32_rna(x0), h1 = tf32_rna(x1), h2 = tf32_rna(x2), h3 = tf32_rna(x3);
+                    const float l0 = tf32_rna(x0 - h0), l1 = tf32_rna(x1 - h1), l2 = tf32_rna(x2 - h2),
+                                l3 = tf32_rna(x3 - h3);
+                    const uint32_t off = st + 2 * F_A_TILE + (uint32_t)(n * 128 + ((kc ^ (n & 7)) << 4));
+                    sts128(off, h0, h1, h2, h3);
+                    sts128(off + F_B_TILE, l0, l1, l2, l3);
+                    Guard gd;
+                    gd.add(x0, l0); gd.add(x1, l1); gd.add(x2, l2); gd.add(x3, l3);
+                    if (gd.bad()) flag_b[nb + n] = 1u;
+                  }
+                }
+              }
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);
+          if (++s == F_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ----------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1272,6 +1674,87 @@ static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, con
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
   return check_launch("gemm_parallel_tf32x3_pair");
 }
+// K7F (the split fused into the GEMM, one launch) is bitwise the planes path
+// (split prepass + pair kernel) but measured slower at every shape it applies
+// to (>= 148 pair tiles: 32768^2 x 8192 138-181 TF vs 250 TF, DESIGN.md
+// section 12), so variant 7 uses it only with ELV_TF32X3_FUSED=1 (read per
+// call); elv_tf32x3_gemm_fused / _fused_a call it directly.
+static bool fused_enabled() { return env_int("ELV_TF32X3_FUSED", 0) != 0; }
+static bool fused_shape_ok(const float* A, int lda, const float* B, int ldb, int M, int N) {
+  const bool al = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 &&
+                  (lda & 3) == 0 && (ldb & 3) == 0;
+  return al && pair_mode(M, N) == 32;
+}
+bool tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N) {
+  return fused_shape_ok(A, lda, B, ldb, M, N);
+}
+
+static int make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+                       uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer}, estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ELV_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ELV_OK;
+}
+
+// C = A B on raw fp32 operands (A row-major M x K, B row-major K x N) in one
+// launch; flag_a[M], flag_b[N] must be zero (the caller's memset) and are
+// read by the range-guard fix-up that follows.
+static inline float* align128(const void* p);
+// b_planes == nullptr: B is split inside the kernel (K7F, one launch);
+// otherwise b_planes holds tf32x3_split_b's planes of B (the columns
+// [c0, c0 + N) of b_total) and the kernel splits only A.
+int tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N, int K,
+                      unsigned int* flag_a, unsigned int* flag_b, cudaStream_t st, const void* b_planes, int b_total,
+                      int c0) {
+  CUtensorMap ma, mb, mb2{}, mc{};
+  const bool fuse_b = b_planes == nullptr;
+  int rc = make_map_2d(&ma, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 4, 32, P_BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) {
+    if (fuse_b) {
+      rc = make_map_2d(&mb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+      const int Kp = (int)kpad(K);
+      if (b_total <= 0) b_total = N;
+      const float* b_hi = align128(b_planes) + (size_t)c0 * Kp;
+      rc = make_map(&mb, b_hi, N, Kp, P_BN / 2, 32);
+      if (!rc) rc = make_map(&mb2, b_hi + (size_t)b_total * Kp, N, Kp, P_BN / 2, 32);
+    }
+  }
+  if (rc) return rc;
+  bool tma_c = c_store_tma() && (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && (ldc & 3) == 0;
+  if (tma_c) tma_c = make_map_2d(&mc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * 4, 32, 32,
+                                 CU_TENSOR_MAP_SWIZZLE_128B) == ELV_OK;
+  if (!tma_c) cudaGetLastError();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto kern = tma_c ? (fuse_b ? k7f_tf32x3_fused<true, true> : k7f_tf32x3_fused<true, false>)
+                    : (fuse_b ? k7f_tf32x3_fused<false, true> : k7f_tf32x3_fused<false, false>);
+  const int ki = (tma_c ? 2 : 0) + (fuse_b ? 1 : 0);
+  static int attr_dev[4] = {-1, -1, -1, -1};
+  if (attr_dev[ki] != dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 fused smem attribute: %s", cudaGetErrorString(e));
+    attr_dev[ki] = dev;
+  }
+  const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
+  int clusters = num_sms() / 2;
+  if (clusters > tiles) clusters = tiles;
+  unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;
+  const int num_kb = (K + 31) / 32;
+  cudaError_t e = launch_pdl(kern, dim3(2 * clusters), dim3(F_NUM_THREADS), (size_t)F_SMEM, st, ma, mb, mb2, mc, C, M,
+                             N, ldc, num_kb, with_lolo(K), tile_group(pair_group<false>()), ctr, flag_a, flag_b,
+                             env_int("ELV_K7F_DBG", 0));
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_fused: %s", cudaGetErrorString(e));
+  return check_launch("gemm_parallel_tf32x3_fused");
+}
+
 // tf32 plane buffers: [hi rows x Kp | lo rows x Kp] fp32 | range-guard flags (rows u32)
 static inline size_t up128(size_t x) { return (x + 127) / 128 * 128; }
 static inline size_t planes_bytes(int rows, int K) {
@@ -1285,6 +1768,7 @@ static inline unsigned int* planes_flags(const void* buf, int total, int K) {
 }
 
 size_t tf32x3_a_planes_bytes(int M, int K) { return planes_bytes(M, K); }
+const unsigned int* tf32x3_b_planes_flags(const void* b_planes, int N, int K) { return planes_flags(b_planes, N, K); }
 size_t tf32x3_b_planes_bytes(int N, int K) { return planes_bytes(N, K); }
 
 // elv_gemm workspace for variant 7 = [A planes | B planes | flags A (M) | flags B (N)]:
@@ -1449,6 +1933,7 @@ int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
                    size_t ws_bytes, cudaStream_t st) {
   if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
+  if (fused_enabled() && tf32x3_fused_ok(A, lda, B, ldb, M, N)) return ELV_OK;   // K7F splits inside the GEMM
   const int Kp = (int)kpad(K);
   float* ahi = align128(ws);
   float* alo = ahi + (size_t)M * Kp;
@@ -1471,6 +1956,14 @@ int tf32x3_compute(const float* A, const float* B, int lda, int ldb, float* C, i
                    size_t ws_bytes, cudaStream_t st) {
   if (ws == nullptr || ws_bytes < tf32x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "tf32x3: workspace too small");
+  if (fused_enabled() && tf32x3_fused_ok(A, lda, B, ldb, M, N)) {
+    unsigned int* flags = ws_tail_flags(ws, M, N, K);
+    if (cudaMemsetAsync(flags, 0, (size_t)(M + N) * 4, st) != cudaSuccess)
+      return set_error(ELV_ECUDA, "tf32x3: memset");
+    const int rc = tf32x3_gemm_fused(A, lda, B, ldb, C, ldc, M, N, K, flags, flags + M, st);
+    if (rc) return rc;
+    return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, flags, flags + M, st);
+  }
   const int rc = tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
   if (rc) return rc;
   const unsigned int* flags = ws_tail_flags(ws, M, N, K);
