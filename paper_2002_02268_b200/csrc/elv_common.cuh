@@ -92,8 +92,24 @@ int tf32x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaSt
                    int r0 = 0);
 int tf32x3_split_b(const float* B, int K, int N, int ldb, bool packed, void* b_planes, cudaStream_t st,
                    int total = 0, int c0 = 0);
+// The range-guard fix-up folded into the GEMM launch: the fp32 operands and
+// the split's flags, handed to the 1-CTA tensor-core kernel (small problems),
+// which recomputes its own flagged outputs after storing them -- one launch
+// fewer.  `applied` is set when the launched kernel took it (the pair kernel
+// does not: the caller then runs tc_fixup).
+struct FixArgs {
+  const float* A;
+  int lda;
+  const float* B;
+  int ldb;
+  const unsigned int* flag_a;
+  const unsigned int* flag_b;
+  int applied;
+};
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0);
+                       cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0,
+                       FixArgs* fix = nullptr);
+bool tc_fixup_enabled();
 const unsigned int* tf32x3_b_planes_flags(const void* b_planes, int N, int K);
 bool tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N);
 int tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N, int K,
@@ -116,7 +132,8 @@ int fp16x3_split_a(const float* A, int M, int K, int lda, void* a_planes, cudaSt
 int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaStream_t st, int total = 0,
                    int c0 = 0, bool packed = false);
 int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0);
+                       cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0,
+                       FixArgs* fix = nullptr);
 unsigned int* fp16x3_planes_flags(const void* buf, int total, int K);
 // Range-guard fix-up after a planes GEMM (tf32x3_gemm.cu, k_tc_fixup): the
 // rows / columns the splits marked are recomputed from the fp32 operands A

@@ -318,7 +318,7 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
           float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
           unsigned int* __restrict__ wave_ctr, const float* __restrict__ inv_s,
-          const float* __restrict__ inv_t) {
+          const float* __restrict__ inv_t, const FixArgs fix, int K) {
   using Cfg = OneCfg<TBN, TBK, F16>;
   constexpr int STAGES = Cfg::NST;
   constexpr int STAGE_BYTES = Cfg::STAGE;
@@ -456,6 +456,29 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (col + j < N) crow[col + j] = v[j];
+          }
+        }
+      }
+      if (fix.A != nullptr) {
+        // range-guard fix-up of this thread's outputs (its row x its columns):
+        // flagged rows / columns are recomputed with the SIMT arithmetic of
+        // k_tc_fixup -- an fmaf chain over k ascending from 0 -- after the
+        // thread's own stores above (program order; flags are complete: the
+        // split finished before griddepcontrol.wait returned)
+        const bool frow = row < M && __ldg(fix.flag_a + row) != 0u;
+#pragma unroll 1
+        for (int c = 0; c < NC; ++c) {
+          const int col0 = n0 + h * (BN / 2) + c * 32;
+          const unsigned int fcol =
+              __ballot_sync(0xffffffffu, col0 + lane < N && __ldg(fix.flag_b + col0 + lane) != 0u);
+          if (row >= M || (!frow && fcol == 0u)) continue;
+          for (int j = 0; j < 32 && col0 + j < N; ++j) {
+            if (!frow && !((fcol >> j) & 1u)) continue;
+            const float* a = fix.A + (size_t)row * fix.lda;
+            const float* b = fix.B + col0 + j;
+            float acc = 0.f;
+            for (int k = 0; k < K; ++k) acc = fmaf(__ldg(a + k), __ldg(b + (size_t)k * fix.ldb), acc);
+            crow[col0 + j] = acc;
           }
         }
       }
@@ -1781,14 +1804,22 @@ static unsigned int* ws_tail_flags(void* ws, int M, int N, int K) {
       align128(static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K) + tf32x3_b_planes_bytes(N, K)));
 }
 
+bool tc_fixup_enabled() {
+  static int enabled = -1;                          // ELV_TC_FIXUP=0: tuning measurements only (unguarded)
+  if (enabled < 0) enabled = env_int("ELV_TC_FIXUP", 1) != 0;
+  return enabled != 0;
+}
+
+// elv_gemm hands the fix-up to the 1-CTA GEMM (ELV_TC_FIXUP_INKERNEL=0, read
+// per call: always the separate k_tc_fixup launch -- same bits, tested)
+static bool fix_in_kernel() { return tc_fixup_enabled() && env_int("ELV_TC_FIXUP_INKERNEL", 1) != 0; }
+
 // The fix-up after a tensor-core GEMM of a row window of A planes (flags
 // flag_a[0, M)) and a column window of B planes (flag_b[0, N)); A, B are the
 // fp32 operands of the same windows (B row-major, or packedB panels).
 int tc_fixup(const float* A, int lda, const float* B, int ldb, bool b_packed, float* C, int ldc, int M, int N, int K,
              const unsigned int* flag_a, const unsigned int* flag_b, cudaStream_t st) {
-  static int enabled = -1;                          // ELV_TC_FIXUP=0: tuning measurements only (unguarded)
-  if (enabled < 0) enabled = env_int("ELV_TC_FIXUP", 1) != 0;
-  if (!enabled) return ELV_OK;
+  if (!tc_fixup_enabled()) return ELV_OK;
   const long long blocks = (long long)(M + FIX_SEG - 1) / FIX_SEG + (N + FIX_SEG - 1) / FIX_SEG;
   if (blocks <= 0) return ELV_OK;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tc_fixup: problem too large");
@@ -1865,7 +1896,7 @@ static int one_cta_bn(int M, int N) {
 template <int TBN, int TBK, bool F16 = false>
 static int launch_one(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C,
                       int M, int N, int K, int Kp, int ldc, int dev, cudaStream_t st,
-                      const float* inv_s = nullptr, const float* inv_t = nullptr) {
+                      const float* inv_s = nullptr, const float* inv_t = nullptr, FixArgs* fix = nullptr) {
   using Cfg = OneCfg<TBN, TBK, F16>;
   CUtensorMap m_ahi, m_alo, m_bhi, m_blo;
   int rc = make_map(&m_ahi, a_hi, M, Kp, BM, TBK, F16);
@@ -1885,8 +1916,9 @@ static int launch_one(const void* a_hi, const void* a_lo, const void* b_hi, cons
   unsigned int* ctr = tiles > grid ? wave_counter(dev, st) : nullptr;
   cudaError_t e = launch_pdl(k7_tf32x3<TBN, TBK, F16>, dim3(grid), dim3(NUM_THREADS), (size_t)Cfg::SMEM, st, m_ahi,
                              m_alo, m_bhi, m_blo, C, M, N, ldc, Kp / TBK, F16 ? 0 : with_lolo(K), tile_group(16), ctr, inv_s,
-                             inv_t);
+                             inv_t, fix != nullptr ? *fix : FixArgs{}, K);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3: %s", cudaGetErrorString(e));
+  if (fix != nullptr) fix->applied = 1;
   return check_launch("gemm_parallel_tf32x3");
 }
 
@@ -1904,7 +1936,7 @@ static int one_cta_bk(int bn) {
 }
 
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st, int a_total, int r0, int b_total, int c0) {
+                       cudaStream_t st, int a_total, int r0, int b_total, int c0, FixArgs* fix) {
   const int Kp = (int)kpad(K);
   if (a_total <= 0) a_total = M;
   if (b_total <= 0) b_total = N;
@@ -1919,13 +1951,14 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   if (pm == 32) return launch_pair<32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   const int bn = one_cta_bn(M, N);
   if (one_cta_bk(bn) == 32) {
-    if (bn == 64) return launch_one<64, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-    if (bn == 128) return launch_one<128, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-    return launch_one<256, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+    if (bn == 64) return launch_one<64, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
+    if (bn == 128)
+      return launch_one<128, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
+    return launch_one<256, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
   }
-  if (bn == 64) return launch_one<64, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  if (bn == 128) return launch_one<128, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
-  return launch_one<256, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  if (bn == 64) return launch_one<64, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
+  if (bn == 128) return launch_one<128, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
+  return launch_one<256, 16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
 }
 
 // elv_gemm workspace for variant 7 = [A planes | B planes]
@@ -1964,9 +1997,11 @@ int tf32x3_compute(const float* A, const float* B, int lda, int ldb, float* C, i
     if (rc) return rc;
     return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, flags, flags + M, st);
   }
-  const int rc = tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st);
-  if (rc) return rc;
   const unsigned int* flags = ws_tail_flags(ws, M, N, K);
+  FixArgs fx{A, lda, B, ldb, flags, flags + M, 0};
+  const int rc = tf32x3_gemm_planes(ws, static_cast<uint8_t*>(ws) + tf32x3_a_planes_bytes(M, K), C, M, N, K, ldc, st,
+                                    0, 0, 0, 0, fix_in_kernel() ? &fx : nullptr);
+  if (rc || fx.applied) return rc;
   return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, flags, flags + M, st);
 }
 
@@ -2197,6 +2232,111 @@ k16_prep_ab(const float* __restrict__ A, int M, int K, int lda, int Kp, float* _
   }
 }
 
+// Short reductions (K <= K16_FUSED_PREP_K), ELV_FP16X3_FUSED_PREP=1 (read per
+// call): the whole variant-8 prepare in ONE launch and no memset -- A rows as
+// k16_prep_ab, and B in slabs of 16 columns x all K held in shared memory, so
+// each block takes its columns' maxima and splits / transposes them without a
+// grid-wide pass between.  Same scales, planes, maxima and flags as
+// k16_prep_ab + k16_split_transpose_b (tested bitwise).  Not the default:
+// measured slower at 1024^3 (single call 32.8 vs 29.7 us) -- the 64 slab
+// blocks each stream 64 KB in and 64 KB out and set the time, while the two
+// PDL-chained kernels spread the same bytes over 640 + 512 blocks.
+constexpr int K16_FUSED_PREP_K = 1024;
+constexpr int K16_SLAB_N = 16;
+__global__ void __launch_bounds__(256)
+k16_prep_fused(const float* __restrict__ A, int M, int K, int lda, int Kp, float* __restrict__ s,
+               float* __restrict__ inv, __half* __restrict__ hi, __half* __restrict__ lo,
+               const float* __restrict__ B, int N, int ldb, unsigned int* __restrict__ maxbits,
+               float* __restrict__ inv_t, __half* __restrict__ bhi, __half* __restrict__ blo, int warp_rows,
+               unsigned int* __restrict__ flag_a, unsigned int* __restrict__ flag_b, int vec_b) {
+  extern __shared__ float slab[];                 // [K][K16_SLAB_N + 1]
+  __shared__ float red[K16_SLAB_N][17];
+  __shared__ float scale[K16_SLAB_N];
+  griddep_launch_dependents();                    // the GEMM waits (griddepcontrol.wait) for our completion
+  const int ga = (M + 7) / 8;
+  const int b = blockIdx.x;
+  if (b < ga) {
+    const int r = b * 8 + (threadIdx.x >> 5);
+    if (warp_rows == 2) split_a_row_warp_vec(A, M, K, lda, Kp, r, s, inv, hi, lo, flag_a);
+    else split_a_row_warp(A, M, K, lda, Kp, r, s, inv, hi, lo, flag_a);
+    return;
+  }
+  constexpr int W = K16_SLAB_N + 1;
+  const int n0 = (b - ga) * K16_SLAB_N;
+  const int tid = threadIdx.x;
+  // stage B[0:K][n0:n0+16] (rows of 64 B: 4 threads x float4 per row when
+  // aligned, every load of the slab in flight at once)
+  if (vec_b && n0 + K16_SLAB_N <= N) {
+    constexpr int PER = K16_FUSED_PREP_K * K16_SLAB_N / 4 / 256;       // float4 per thread (K = 1024)
+    float4 v[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = tid + 256 * j, k = i >> 2, c = (i & 3) * 4;
+      v[j] = k < K ? __ldg(reinterpret_cast<const float4*>(B + (size_t)k * ldb + n0 + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = tid + 256 * j, k = i >> 2, c = (i & 3) * 4;
+      if (k < K) {
+        slab[k * W + c] = v[j].x; slab[k * W + c + 1] = v[j].y;
+        slab[k * W + c + 2] = v[j].z; slab[k * W + c + 3] = v[j].w;
+      }
+    }
+  } else {
+#pragma unroll 8
+    for (int i = tid; i < K * K16_SLAB_N; i += 256) {
+      const int k = i / K16_SLAB_N, c = i % K16_SLAB_N;
+      slab[k * W + c] = n0 + c < N ? __ldg(B + (size_t)k * ldb + n0 + c) : 0.f;
+    }
+  }
+  __syncthreads();
+  // column maxima: 16 threads per column
+  {
+    const int c = tid >> 4, part = tid & 15;
+    float m = 0.f;
+    for (int k = part; k < K; k += 16) m = fmaxf(m, fabsf(slab[k * W + c]));
+    red[c][part] = m;
+  }
+  __syncthreads();
+  if (tid < K16_SLAB_N) {
+    float m = red[tid][0];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) m = fmaxf(m, red[tid][q]);
+    float sc, iv;
+    pow2_scale(m, &sc, &iv);
+    scale[tid] = sc;
+    if (n0 + tid < N) {
+      maxbits[n0 + tid] = __float_as_uint(m);
+      inv_t[n0 + tid] = iv;
+    }
+  }
+  __syncthreads();
+  // split + transpose: warp w takes columns w and w + 8; lane j the k pairs 2j + 64 i
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int c = warp + 8 * cc, n = n0 + c;
+    if (n >= N) continue;
+    const float sc = scale[c];
+    bool bad = false;
+    __half2* h2 = reinterpret_cast<__half2*>(bhi + (size_t)n * Kp);
+    __half2* l2 = reinterpret_cast<__half2*>(blo + (size_t)n * Kp);
+    for (int k2 = lane; k2 < Kp / 2; k2 += 32) {
+      const int k = 2 * k2;
+      const float x0 = k < K ? slab[k * W + c] : 0.f, x1 = k + 1 < K ? slab[(k + 1) * W + c] : 0.f;
+      const float y0 = x0 * sc, y1 = x1 * sc;
+      bad |= f16_out_of_window(x0, y0) || f16_out_of_window(x1, y1);
+      __half a0, a1, b0, b1;
+      split16(y0, &a0, &b0);
+      split16(y1, &a1, &b1);
+      h2[k2] = __halves2half2(a0, a1);
+      l2[k2] = __halves2half2(b0, b1);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) flag_b[n] = bad ? 1u : 0u;
+  }
+}
+
 // B planes: [N][Kp] (B transposed to K-major) through 64(k) x 32(n) SMEM
 // tiles: coalesced 128 B reads along B's rows, 128 B half2 writes along the
 // planes' rows.  Each block turns its 32 columns' maxima (k16_col_max) into
@@ -2296,7 +2436,7 @@ int fp16x3_split_b(const float* B, int K, int N, int ldb, void* b_planes, cudaSt
 }
 
 int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
-                       cudaStream_t st, int a_total, int r0, int b_total, int c0) {
+                       cudaStream_t st, int a_total, int r0, int b_total, int c0, FixArgs* fix) {
   if (!fp16x3_applicable(M, N, K))
     return set_error(ELV_EINVAL, "fp16x3: needs K >= 512 (got %dx%dx%d)", M, N, K);
   const Planes16 A = planes16_at(a_planes, M, K, a_total, r0), B = planes16_at(b_planes, N, K, b_total, c0);
@@ -2308,10 +2448,11 @@ int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   // fewer pair tiles than SMs: the 1-CTA kernel, 128 B stage rows for the
   // narrow N tiles, 64 B for N = 256 (keeps 4 stages)
   const int bn = one_cta_bn(M, N);
-  if (bn == 64) return launch_one<64, 64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
+  if (bn == 64)
+    return launch_one<64, 64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
   if (bn == 128)
-    return launch_one<128, 64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
-  return launch_one<256, 32, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
+    return launch_one<128, 64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
+  return launch_one<256, 32, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
 }
 
 // The fp16 encoding has no lo.lo term (lo is pre-scaled by 2^11, so lo.lo
@@ -2335,10 +2476,30 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   if (ws == nullptr || ws_bytes < fp16x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
   // memset + [A rows | B column maxima] + B split-transpose: two launches
+  // (K <= K16_FUSED_PREP_K: one, k16_prep_fused)
   const Planes16 PA = planes16(ws, M, K);
   const Planes16 PB = planes16(static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K), N, K);
   const int Kp = (int)kpad16(K);
   unsigned int* tmax = reinterpret_cast<unsigned int*>(PB.s);
+  const bool vec_ok0 = K % 4 == 0 && lda % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  if (K <= K16_FUSED_PREP_K && env_int("ELV_FP16X3_FUSED_PREP", 0) != 0) {
+    const int warp_rows = min(env_int("ELV_FP16X3_WARP_ROWS", 2), vec_ok0 ? 2 : 1) == 2 ? 2 : 1;
+    const size_t smem = (size_t)K * (K16_SLAB_N + 1) * sizeof(float);
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      const cudaError_t ea = cudaFuncSetAttribute(k16_prep_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)((size_t)K16_FUSED_PREP_K * (K16_SLAB_N + 1) * sizeof(float)));
+      if (ea != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3 prepare smem attribute: %s", cudaGetErrorString(ea));
+      attr_dev = dev;
+    }
+    const unsigned blocks = (unsigned)((M + 7) / 8 + (N + K16_SLAB_N - 1) / K16_SLAB_N);
+    k16_prep_fused<<<blocks, 256, smem, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, tmax, PB.inv,
+                                              PB.hi, PB.lo, warp_rows, PA.flag, PB.flag,
+                                              (int)(ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0));
+    return check_launch("fp16x3_prepare_fused");
+  }
   if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
   // Short rows: one warp per A row (2: row in registers, when float4 loads
   // are legal; 1: two scalar passes); ELV_FP16X3_WARP_ROWS caps the mode
@@ -2372,9 +2533,11 @@ int fp16x3_compute(const float* A, const float* B, int lda, int ldb, float* C, i
   if (ws == nullptr || ws_bytes < fp16x3_workspace_bytes(M, N, K))
     return set_error(ELV_EWORKSPACE, "fp16x3: workspace too small");
   void* bp = static_cast<uint8_t*>(ws) + fp16x3_a_planes_bytes(M, K);
-  const int rc = fp16x3_gemm_planes(ws, bp, C, M, N, K, ldc, st);
-  if (rc) return rc;
-  return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, planes16(ws, M, K).flag, planes16(bp, N, K).flag, st);
+  const unsigned int *fa = planes16(ws, M, K).flag, *fb = planes16(bp, N, K).flag;
+  FixArgs fx{A, lda, B, ldb, fa, fb, 0};
+  const int rc = fp16x3_gemm_planes(ws, bp, C, M, N, K, ldc, st, 0, 0, 0, 0, fix_in_kernel() ? &fx : nullptr);
+  if (rc || fx.applied) return rc;
+  return tc_fixup(A, lda, B, ldb, false, C, ldc, M, N, K, fa, fb, st);
 }
 
 }  // namespace elv

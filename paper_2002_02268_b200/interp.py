@@ -123,6 +123,20 @@ class GemmCall:
     PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 2}   # 8: [A rows | B max], B split
     COMPUTE_LAUNCHES = {7: 2, 8: 2}     # tensor-core GEMM + range-guard fix-up; others: 1
 
+    @classmethod
+    def count_launches(cls, p) -> int:
+        """Kernel launches of one call (the library's defaults): the
+        tensor-core variants fold the range-guard fix-up into the 1-CTA GEMM
+        (fewer 256x256 tiles than SMs); the 3xFP16 prepare is two launches;
+        K < 512 runs variant 8 as 7."""
+        if p.variant not in (7, 8):
+            return cls.PREPARE_LAUNCHES[p.variant] + 1
+        pair = ((p.M + 255) // 256) * ((p.N + 255) // 256) >= 148
+        compute = 2 if pair else 1
+        if p.variant == 8 and p.K >= 512:
+            return 2 + compute
+        return 1 + compute
+
     def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
         self.lib = _lib.load()
         self.p, self.A, self.B, self.C = p, A, B, C
@@ -130,7 +144,7 @@ class GemmCall:
         self.ws_bytes = self.lib.elv_gemm_workspace_bytes(p.variant, p.M, p.N, p.K)
         self.ws = (torch.empty(self.ws_bytes, device=A.device, dtype=torch.uint8)
                    if self.ws_bytes else None)
-        self.launches = self.PREPARE_LAUNCHES[p.variant] + self.COMPUTE_LAUNCHES.get(p.variant, 1)
+        self.launches = self.count_launches(p)
         # the buffers are fixed for the object's lifetime: build the C-ABI
         # argument tuples once (saves 1.5-3 us of host time per 1024^3 call,
         # 5-8 % of a single 3xTF32 / SIMT call; profiles/r1/small/gemmcall_args.jsonl)

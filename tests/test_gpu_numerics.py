@@ -183,3 +183,34 @@ def test_bench_shape_checksums_adversarial(cuda, enc, kind):
     # of its bound at most); it does not average out in a sum of 32768
     # elements: 4-6x the root-sum-square of the bounds, 0.02-0.04 of their
     # linear sum (profiles/r2/numerics_chunked.log)
+
+
+@pytest.mark.parametrize("enc", ENCODINGS)
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 1031, 777), (130, 70, 516), (640, 768, 1024)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_small_problem_paths_bitwise(cuda, enc, shape, monkeypatch):
+    """Small problems (fewer 256x256 tiles than SMs): the 1-CTA GEMM runs the
+    range-guard fix-up itself and, for 3xFP16 with K <= 1024, the prepare is
+    one launch (k16_prep_fused, B column slabs in shared memory).  Both give
+    the bits of the separate launches (ELV_TC_FIXUP_INKERNEL=0,
+    ELV_FP16X3_FUSED_PREP=0), with guarded rows and columns present."""
+    M, N, K = shape
+    A, B = make(M, N, K, "uniform", cuda, seed=4)
+    A[3, 1] = 2.0 ** -110
+    A[M - 1, K - 1] = float("inf")
+    B[0, 2] = -(2.0 ** -110)
+    B[K // 2, N - 1] = float("nan")
+    term = schedules.apply_padded("parallel", M, N, K).term
+    outs = []
+    for inker, fprep in (("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")):
+        monkeypatch.setenv("ELV_TC_FIXUP_INKERNEL", inker)
+        monkeypatch.setenv("ELV_FP16X3_FUSED_PREP", fprep)
+        outs.append(_tc(term, A, B, enc).view(torch.int32).clone())
+    torch.cuda.synchronize()
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    C6 = interp.run_tensor(term, A, B, tf32x3=False)
+    C = outs[0].view(torch.float32)
+    for r in (3, M - 1):
+        assert torch.equal(torch.nan_to_num(C[r], nan=7.0), torch.nan_to_num(C6[r], nan=7.0))
+    for c in (2, N - 1):
+        assert torch.equal(torch.nan_to_num(C[:, c], nan=7.0), torch.nan_to_num(C6[:, c], nan=7.0))
