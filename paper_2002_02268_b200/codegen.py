@@ -132,6 +132,7 @@ class Gen:
         self.elementwise = True          # mode A: lifted array reduces fold per element
         self.strict_maps = False         # mode B: materialise small computing maps
         self.materialised = 0            # array reduces that had to be materialised
+        self.grid: tuple = ()             # smem-tile mode: explicit 2-D grid of 256-thread blocks
         self.probing = 0                 # >0 inside shape probes
         self.fold_depth = 0              # >0 inside a per-element fold
 
@@ -578,7 +579,8 @@ class Compiled:
     in_shapes: tuple       # per input: array shape
     out_shape: tuple
     threads: int = 1       # threads launched
-    mode: str = ""         # "per-scalar" or "destination-passing"
+    mode: str = ""         # "per-scalar", "register-tile TMxTN", "smem-tile ..." or "destination-passing"
+    grid: tuple = ()       # explicit (x, y) grid of 256-thread blocks (smem-tile mode); else 1-D over `threads`
 
 
 def compile_term(term) -> Compiled:
@@ -607,13 +609,14 @@ def compile_term(term) -> Compiled:
         # the result in the term's own structure instead (destination passing)
         g = _dps_kernel(body, params, out_shape)
     else:
-        g = _register_tile(g, out_shape) or g
+        g = _smem_tile(g, out_shape) or _register_tile(g, out_shape) or g
     name = "elv_generated"
     args = ", ".join([f"const float* __restrict__ in{i}" for i in range(len(params))] +
                      ["float* __restrict__ out"])
-    src = "\n".join([f'extern "C" __global__ void __launch_bounds__(128) {name}({args}) {{'] + g.head +
+    block = 256 if g.grid else 128
+    src = "\n".join([f'extern "C" __global__ void __launch_bounds__({block}) {name}({args}) {{'] + g.head +
                     g.consts + g.lines + ["}"])
-    return Compiled(name, src, tuple(shp for _, shp in params), out_shape, g.threads, g.mode)
+    return Compiled(name, src, tuple(shp for _, shp in params), out_shape, g.threads, g.mode, g.grid)
 
 
 def _inputs_env(g: Gen, params) -> dict:
@@ -756,6 +759,269 @@ def _register_tile(g: Gen, out_shape: tuple) -> Gen | None:
     return t
 
 
+# ----------------------------------------------------------------------------
+# Mode A'': shared-memory tiles for contractions.  When the per-scalar body of
+# a 2-D result is one counted loop nest (constant trip counts, from 0) whose
+# loads of an input depend on only ONE output index -- in0 on o0 (a "row"
+# operand), in1 on o1 (a "column" operand), i.e. the lowered form of every
+# matmul schedule -- a 256-thread block computes a 64 x 64 output tile, 4 x 4
+# per thread, and stages each load site's values for CH iterations of the
+# outermost loop in shared memory: rows x TL (+1 pad) for row operands,
+# TL x columns for column operands (read as float4).  The per-output
+# statement sequence is the per-scalar one (locals replicated per output as in
+# the register-tile mode, values read from the staged copy instead of global
+# memory), so the results are bitwise the per-scalar kernel's.  Host
+# emulation (cpu_source) cannot run __syncthreads: this mode is GPU-only.
+SMEM_TILE = True
+SMEM_MIN_OUTPUTS = 1 << 16            # 256 x 256 outputs and up
+SMEM_TLMAX = 32                       # staged iterations per chunk and site
+_LOOP0 = re.compile(r"^for \(int (\w+) = 0; \1 < (\d+); \+\+\1\) \{$")
+
+
+def _load_sites(text: str, inp: str):
+    """(start, end, index expression) of every `inp[...]` in `text`."""
+    out, pos, key = [], 0, inp + "["
+    while True:
+        i = text.find(key, pos)
+        if i < 0:
+            return out
+        if i > 0 and (text[i - 1].isalnum() or text[i - 1] == "_"):
+            pos = i + 1
+            continue
+        depth, j = 1, i + len(key)
+        while depth:
+            if j >= len(text):
+                raise CodegenError("unbalanced index expression")
+            depth += {"[": 1, "]": -1}.get(text[j], 0)
+            j += 1
+        out.append((i, j, text[i + len(key):j - 1]))
+        pos = j
+
+
+def _eval_index(expr: str, env: dict) -> int:
+    """Value of a generated (non-negative) C integer index expression."""
+    py = expr.replace("/", "//")
+    return int(eval(py, {"__builtins__": {}}, dict(env)))   # generated text: names, ints, + * / % ( )
+
+
+def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
+    if not SMEM_TILE or len(out_shape) != 2:
+        return None
+    O0, O1 = out_shape
+    if O0 % 64 or O1 % 64 or O0 * O1 < SMEM_MIN_OUTPUTS:
+        return None
+    # parse the body: ("for", var, trip, children) / ("stmt", text); the output write last
+    root, stack, out_expr, locals_ = [], [], None, set()
+    cur = root
+    for line in g.lines:
+        st = line.strip()
+        if out_expr is not None:
+            return None
+        m = _LOOP0.match(st)
+        if m:
+            node = ("for", m.group(1), int(m.group(2)), [])
+            cur.append(node)
+            stack.append(cur)
+            cur = node[3]
+            continue
+        if st == "}":
+            if not stack:
+                return None
+            cur = stack.pop()
+            continue
+        m = _OUT.match(st)
+        if m and not stack:
+            out_expr = m.group(1)
+            continue
+        m = _DECL.match(st)
+        if m:
+            locals_.add(m.group(1))
+            cur.append(("stmt", st))
+            continue
+        m = _ASSIGN.match(st)
+        if m and m.group(1) in locals_:
+            cur.append(("stmt", st))
+            continue
+        return None
+    if out_expr is None or stack:
+        return None
+    loops = [n for n in root if n[0] == "for"]
+    if len(loops) != 1:
+        return None
+    top = loops[0]
+    inputs = sorted(set(re.findall(r"\b(in\d+)\[", "\n".join(g.lines))))
+    for n in root:
+        if n[0] == "stmt" and any(_load_sites(n[1], i) for i in inputs):
+            return None                                  # loads outside the loop nest
+    if any(_load_sites(out_expr, i) for i in inputs):
+        return None
+    # load sites: (input, expression, enclosing inner loops) -> staging buffer
+    sites, order = {}, []
+
+    def scan(nodes, path):
+        for n in nodes:
+            if n[0] == "for":
+                scan(n[3], path + [(n[1], n[2])])
+                continue
+            for inp in inputs:
+                for _, _, e in _load_sites(n[1], inp):
+                    r0, r1 = bool(re.search(r"\bo0\b", e)), bool(re.search(r"\bo1\b", e))
+                    if r0 == r1 or re.search(r"\b(in\d+|t|q0|q1)\b", e):
+                        raise CodegenError("not a contraction")
+                    key = (inp, e, tuple(path))
+                    if key not in sites:
+                        sites[key] = {"role": "r" if r0 else "c", "inner": path}
+                        order.append(key)
+    try:
+        scan(top[3], [])
+    except CodegenError:
+        return None
+    if not sites or len(sites) > 4:
+        return None
+    v0, T0 = top[1], top[2]
+    pmax = max(max(1, _prod(t for _, t in site["inner"])) for site in sites.values())
+    ch = 1
+    for c in range(1, T0 + 1):
+        if T0 % c == 0 and c * pmax <= SMEM_TLMAX:
+            ch = c
+    for idx, key in enumerate(order):
+        site = sites[key]
+        site["P"] = max(1, _prod(t for _, t in site["inner"]))
+        site["TL"] = ch * site["P"]
+        site["name"] = f"sm{idx}"
+        # which staging axis is contiguous in global memory (probe the index)
+        loopvars = [(v0, T0)] + site["inner"]
+
+        def env_at(tl, o, key=key, loopvars=loopvars, site=site):
+            env = {"o0": o, "o1": o}
+            rem = tl
+            for v, t in reversed(loopvars[1:]):
+                env[v] = rem % t
+                rem //= t
+            env[v0] = rem
+            return env
+        try:
+            e = key[1]
+            d_tl = _eval_index(e, env_at(1, 0)) - _eval_index(e, env_at(0, 0)) if site["TL"] > 1 else 0
+            site["tl_fast"] = d_tl == 1
+        except Exception:
+            return None
+    t = Gen()
+    t.consts = g.consts
+    t.head = [f"  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;",
+              f"  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;"]
+    t.head += [f"  const int o0_{i} = row0 + 4 * ty + {i};" for i in range(4)]
+    t.head += [f"  const int o1_{j} = col0 + 4 * tx + {j};" for j in range(4)]
+    for key in order:
+        site = sites[key]
+        size = 64 * (site["TL"] + 1) if site["role"] == "r" else site["TL"] * 64
+        t.head.append(f"  __shared__ __align__(16) float {site['name']}[{size}];")
+    names = re.compile(r"\b(" + "|".join(sorted(map(re.escape, locals_), key=len, reverse=True)) + r")\b") \
+        if locals_ else None
+
+    def inst(text, i, j, loaded):
+        # loads -> staged values (before any renaming: the index text names o0 / o1)
+        for key in (order if loaded is not None else ()):
+            inp, e, _ = key
+            site = sites[key]
+            if key[2] != tuple(loaded):
+                continue
+            rep = f"ra{site['name']}_{i}" if site["role"] == "r" else f"cb{site['name']}.{'xyzw'[j]}"
+            text = text.replace(f"{inp}[{e}]", rep)
+        if names is not None:
+            text = names.sub(lambda mm: f"{mm.group(1)}_{i}_{j}", text)
+        text = re.sub(r"\bo0\b", f"o0_{i}", text)
+        return re.sub(r"\bo1\b", f"o1_{j}", text)
+
+    def tl_expr(site):
+        terms, stride = [], 1
+        for v, tr in reversed(site["inner"]):
+            terms.append(f"{v} * {stride}" if stride != 1 else v)
+            stride *= tr
+        terms.append(f"({v0} - {v0}_b) * {stride}")
+        return " + ".join(reversed(terms))
+
+    def emit_nodes(nodes, indent, path):
+        for n in nodes:
+            if n[0] == "for":
+                t.lines.append(indent + "#pragma unroll")
+                t.lines.append(indent + f"for (int {n[1]} = 0; {n[1]} < {n[2]}; ++{n[1]}) {{")
+                emit_nodes(n[3], indent + "  ", path + [(n[1], n[2])])
+                t.lines.append(indent + "}")
+                continue
+            st = n[1]
+            used = [key for key in order if key[2] == tuple(path) and f"{key[0]}[{key[1]}]" in st]
+            for key in used:
+                site = sites[key]
+                tl = tl_expr(site)
+                if site["role"] == "r":
+                    for i in range(4):
+                        t.lines.append(indent + f"const float ra{site['name']}_{i} = "
+                                       f"{site['name']}[(4 * ty + {i}) * {site['TL'] + 1} + ({tl})];")
+                else:
+                    t.lines.append(indent + f"const float4 cb{site['name']} = *reinterpret_cast<const float4*>("
+                                   f"&{site['name']}[({tl}) * 64 + 4 * tx]);")
+            for i in range(4):
+                for j in range(4):
+                    t.lines.append(indent + inst(st, i, j, path))
+
+    for n in root:
+        if n is top:
+            t.lines.append(f"  for (int {v0}_b = 0; {v0}_b < {T0}; {v0}_b += {ch}) {{")
+            t.lines.append("    __syncthreads();")
+            for key in order:
+                inp, e, _ = key
+                site = sites[key]
+                TL = site["TL"]
+                total = 64 * TL
+                iters = (total + 255) // 256
+                loopvars = site["inner"]
+                t.lines.append("    #pragma unroll")
+                t.lines.append(f"    for (int q = 0; q < {iters}; ++q) {{")
+                t.lines.append(f"      const int idx = threadIdx.x + 256 * q;")
+                if total % 256:
+                    t.lines.append(f"      if (idx >= {total}) break;")
+                if site["tl_fast"]:
+                    t.lines.append(f"      const int tl = idx % {TL}, rr = idx / {TL};")
+                else:
+                    t.lines.append(f"      const int tl = idx / 64, rr = idx % 64;")
+                rem, stride = "tl", 1
+                for v, tr in reversed(loopvars):
+                    t.lines.append(f"      const int {v} = ({rem} / {stride}) % {tr};")
+                    stride *= tr
+                t.lines.append(f"      const int {v0} = {v0}_b + tl / {stride};")
+                o = "o0" if site["role"] == "r" else "o1"
+                base = "row0" if site["role"] == "r" else "col0"
+                ex = re.sub(rf"\b{o}\b", f"({base} + rr)", e)
+                dst = f"rr * {TL + 1} + tl" if site["role"] == "r" else "tl * 64 + rr"
+                t.lines.append(f"      {site['name']}[{dst}] = {inp}[{ex}];")
+                t.lines.append("    }")
+            t.lines.append("    __syncthreads();")
+            t.lines.append("    #pragma unroll 4")
+            t.lines.append(f"    for (int {v0} = {v0}_b; {v0} < {v0}_b + {ch}; ++{v0}) {{")
+            emit_nodes(top[3], "      ", [])
+            t.lines.append("    }")
+            t.lines.append("  }")
+        else:
+            for i in range(4):
+                for j in range(4):
+                    t.lines.append("  " + inst(n[1], i, j, None))
+    for i in range(4):
+        for j in range(4):
+            t.lines.append(f"  out[(long long)o0_{i} * {O1} + o1_{j}] = {inst(out_expr, i, j, None)};")
+    t.threads = O0 * O1 // 16
+    t.grid = (O1 // 64, O0 // 64)
+    t.mode = f"smem-tile 4x4 (64x64 block, {ch} x {pmax} iterations staged per chunk)"
+    return t
+
+
+def _prod(xs) -> int:
+    p = 1
+    for x in xs:
+        p *= x
+    return p
+
+
 def _dps_kernel(body, params, out_shape) -> Gen:
     """Mode B: destination passing; the outermost PAR_LEVELS maps are the
     thread index, small computing maps are materialised per thread."""
@@ -795,6 +1061,8 @@ def cpu_source(c: Compiled) -> str:
     tests can check code generation against the reference interpreter
     without a GPU.  Compiled with -ffp-contract=off it performs the same fp32
     operations in the same order as the NVRTC (--fmad=false, explicit fmaf) build."""
+    if c.grid:
+        raise CodegenError("the shared-memory tile mode needs a GPU (set codegen.SMEM_TILE = False for cpu_source)")
     n = len(c.in_shapes)
     call = ", ".join([f"ins[{i}]" for i in range(n)] + ["out"])
     return "\n".join([
@@ -856,6 +1124,10 @@ class Kernel:
         total = self.c.threads
         ptrs = [ctypes.c_void_p(t.data_ptr()) for t in list(inputs) + [out]]
         arg_ptrs = np.array([ctypes.addressof(p) for p in ptrs], dtype=np.uint64)
+        if self.c.grid:
+            gx, gy = self.c.grid
+            _check(d.cuLaunchKernel(self.fn, gx, gy, 1, 256, 1, 1, 0, d.CUstream(stream), arg_ptrs.ctypes.data, 0))
+            return
         block = 128
         grid = max(1, (total + block - 1) // block)
         _check(d.cuLaunchKernel(self.fn, grid, 1, 1, block, 1, 1, 0, d.CUstream(stream),

@@ -33,6 +33,9 @@ def main():
     user = st.seq(nf.dfnf_seq(tv.top_down(schedules.tile(16, 16)),
                               tv.top_down(st.seq(tv.is_reduce, rules.make_split(2)))), nf.LOWER_TO_C)
     terms = [("user_tile16_split2", st.run_strategy(user, schedules.mm(n, n, n))[0].term)]
+    user2 = st.seq(nf.dfnf_seq(tv.top_down(schedules.tile(32, 64)),
+                               tv.top_down(st.seq(tv.is_reduce, rules.make_split(8)))), nf.LOWER_TO_C)
+    terms += [("user_tile32x64_split8", st.run_strategy(user2, schedules.mm(n, n, n))[0].term)]
     terms += [(name, schedules.apply(name, n, n, n).term) for name in schedules.SCHEDULE_NAMES]
     for name, term in terms:
         t0 = time.perf_counter()

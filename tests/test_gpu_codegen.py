@@ -59,15 +59,53 @@ def test_template_and_generated_kernels_agree(cuda, name):
 
 
 @pytest.mark.parametrize("name", ["parallel", "loopPerm"])
-def test_register_tiled_generated_kernel_at_1024(cuda, name):
-    """The register-tile mode (8x4 outputs per thread) at 1024^3: bitwise the
-    template kernel's result (same fmaf chain per output)."""
+def test_tiled_generated_kernel_at_1024(cuda, name):
+    """The generated kernel at 1024^3 (shared-memory tile mode: a contraction)
+    is bitwise the template kernel's result (same fmaf chain per output)."""
     n = 1024
     term = schedules.apply(name, n, n, n).term
-    assert codegen.kernel_for(term).c.mode.startswith("register-tile")
+    assert codegen.kernel_for(term).c.mode.startswith("smem-tile")
     A = torch.empty((n, n), device=cuda); synth.fill_device(A, 3, 0)
     B = torch.empty((n, n), device=cuda); synth.fill_device(B, 3, 1)
     assert torch.equal(codegen.run(term, [A, B]), interp.run_tensor(term, A, B))
+
+
+def _user_terms(n):
+    from paper_2002_02268_b200._ref import S
+    st, nf, tv, rules = S().strategy, S().normal_forms, S().traversals, S().rules
+    out = {}
+    for name, (ti, tj, sp) in {"tile16_split2": (16, 16, 2), "tile32x64_split8": (32, 64, 8),
+                               "tile64_split4": (64, 64, 4)}.items():
+        strat = st.seq(nf.dfnf_seq(tv.top_down(schedules.tile(ti, tj)),
+                                   tv.top_down(st.seq(tv.is_reduce, rules.make_split(sp)))), nf.LOWER_TO_C)
+        out[name] = st.run_strategy(strat, schedules.mm(n, n, n))[0].term
+    return out
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_smem_tile_mode_is_bitwise_the_register_tile_mode(cuda, n, monkeypatch):
+    """Mode A'' stages each load site's values in shared memory and keeps every
+    output's per-scalar statement sequence: the same bits as the register-tile
+    (and per-scalar) kernels, for user schedules outside the templates and the
+    seven schedules."""
+    terms = _user_terms(n)
+    terms.update({name: schedules.apply(name, n, n, n).term for name in ("blocking", "cacheBlocks", "baseline")})
+    A = torch.empty((n, n), device=cuda); synth.fill_device(A, 7, 0)
+    B = torch.empty((n, n), device=cuda); synth.fill_device(B, 7, 1)
+    stream = torch.cuda.current_stream().cuda_stream
+    for name, term in terms.items():
+        outs = {}
+        for smem in (True, False):
+            monkeypatch.setattr(codegen, "SMEM_TILE", smem)
+            k = codegen.Kernel(codegen.compile_term(term))
+            assert k.c.mode.startswith("smem-tile") == smem, (name, k.c.mode)
+            C = torch.empty((n, n), device=cuda)
+            k([A, B], C, stream)
+            outs[smem] = C
+        torch.cuda.synchronize()
+        assert torch.equal(outs[True], outs[False]), name
+    ref = A.double() @ B.double()
+    assert (outs[True].double() - ref).abs().max().item() < 1e-3
 
 
 VEC_ADD = """
