@@ -1,7 +1,7 @@
 #!/bin/bash
 # compute-sanitizer over every kernel path (small shapes), round 2: chunked tcgen05 kernels
 # (1-CTA and, forced with ELV_TF32X3_PAIR=32, the cta_group::2 kernel), range-guard fix-up,
-# pipelined C-ABI row shard
+# pipelined C-ABI row shard; session 4: K7F fused split (pair pass) and the codegen shared-memory tile mode
 OUT=gpurun_out/${1:-r2_san}; mkdir -p $OUT
 S=$OUT/summary.txt
 timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/sanitize_run.py > $OUT/memcheck.log 2>&1; echo "memcheck rc=$?" >> $S

@@ -98,6 +98,48 @@ def main():
         refb = oracle.bf_interp_f64(img, name)
         assert np.all(np.abs(out.cpu().numpy() - refb) <= oracle.bf_bound(img)), name
         print(f"binomial {name} ok", flush=True)
+    # K7F: the 3xTF32 split inside the pair kernel (applies at >= 148 pair tiles,
+    # or at any shape under ELV_TF32X3_PAIR=32, which the pair sanitizer pass sets)
+    M, N, K = 384, 520, 200
+    A = synth.matrix(M, K, 9, 0)
+    B = synth.matrix(K, N, 9, 1)
+    A[5, 7] = 2.0 ** -110
+    ref, ab = oracle.mm_f64(A, B), oracle.absprod_np(A, B)
+    Ad, Bd = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+    st = torch.cuda.current_stream().cuda_stream
+    if lib.elv_tf32x3_fused_ok(Ad.data_ptr(), K, Bd.data_ptr(), N, M, N):
+        flags = torch.empty(M + N, dtype=torch.int32, device=dev)
+        C = torch.empty((M, N), device=dev)
+        _lib.check(lib.elv_tf32x3_gemm_fused(Ad.data_ptr(), K, Bd.data_ptr(), N, C.data_ptr(), N, M, N, K,
+                                             flags.data_ptr(), st), "gemm_fused")
+        bp = torch.empty(lib.elv_tf32x3_b_planes_bytes(N, K), dtype=torch.uint8, device=dev)
+        _lib.check(lib.elv_tf32x3_split_b(Bd.data_ptr(), K, N, N, bp.data_ptr(), st), "split_b")
+        C2 = torch.empty((M, N), device=dev)
+        _lib.check(lib.elv_tf32x3_gemm_fused_a(Ad.data_ptr(), K, bp.data_ptr(), Bd.data_ptr(), N, C2.data_ptr(), N,
+                                               M, N, K, flags.data_ptr(), st), "gemm_fused_a")
+        torch.cuda.synchronize()
+        for name, X in (("fused", C), ("fused_a", C2)):
+            ok, worst = oracle.check(X.cpu().numpy(), ref, ab, K)
+            print(f"K7F {name} ok={ok} worst={worst:.3f}", flush=True)
+            assert ok
+    else:
+        print("K7F: not applicable at this shape without ELV_TF32X3_PAIR=32 (skipped)", flush=True)
+    # generated kernels: shared-memory tile mode (a user schedule outside the templates)
+    from paper_2002_02268_b200 import codegen
+    from paper_2002_02268_b200._ref import S
+    st_, nf, tv, rules = S().strategy, S().normal_forms, S().traversals, S().rules
+    n = 256
+    user = st_.seq(nf.dfnf_seq(tv.top_down(schedules.tile(16, 16)),
+                               tv.top_down(st_.seq(tv.is_reduce, rules.make_split(2)))), nf.LOWER_TO_C)
+    term = st_.run_strategy(user, schedules.mm(n, n, n))[0].term
+    A = synth.matrix(n, n, 3, 0)
+    B = synth.matrix(n, n, 3, 1)
+    C = codegen.run(term, [torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)])
+    torch.cuda.synchronize()
+    assert codegen.kernel_for(term).c.mode.startswith("smem-tile")
+    ok, worst = oracle.check(C.cpu().numpy(), oracle.mm_f64(A, B), oracle.absprod_np(A, B), n)
+    print(f"codegen smem-tile ok={ok} worst={worst:.3f}", flush=True)
+    assert ok
     print("sanitize_run: all paths ran")
 
 
