@@ -373,8 +373,8 @@ int elv_tf32x3_gemm_fused_a(const float* A, int lda, const void* b_planes, const
   int rc = check_args(A, B, C, M, N, K, lda, ldb, ldc, true);
   if (rc) return rc;
   if (bad_ptr(flags_a) || bad_ptr(b_planes)) return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: null pointer");
-  if (!tf32x3_fused_ok(A, lda, A, 4, M, N))
-    return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: not applicable (needs >= 148 pair tiles, 16 B alignment)");
+  if (!tf32x3_fused_a_ok(A, lda, M, N))
+    return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: not applicable (needs >= 148 pair tiles, 16 B aligned A)");
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(flags_a, 0, (size_t)M * 4, st) != cudaSuccess)
     return set_error(ELV_ECUDA, "tf32x3_gemm_fused_a: memset");

@@ -112,6 +112,7 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
 bool tc_fixup_enabled();
 const unsigned int* tf32x3_b_planes_flags(const void* b_planes, int N, int K);
 bool tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N);
+bool tf32x3_fused_a_ok(const float* A, int lda, int M, int N);
 int tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N, int K,
                       unsigned int* flag_a, unsigned int* flag_b, cudaStream_t st, const void* b_planes = nullptr,
                       int b_total = 0, int c0 = 0);

@@ -1711,6 +1711,10 @@ static bool fused_shape_ok(const float* A, int lda, const float* B, int ldb, int
 bool tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N) {
   return fused_shape_ok(A, lda, B, ldb, M, N);
 }
+// the A-fused kernel reads only A raw (B comes as planes)
+bool tf32x3_fused_a_ok(const float* A, int lda, int M, int N) {
+  return (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && (lda & 3) == 0 && pair_mode(M, N) == 32;
+}
 
 static int make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
                        uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
