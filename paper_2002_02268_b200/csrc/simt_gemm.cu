@@ -340,6 +340,14 @@ __device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
 #ifndef ELV_K56_FFMA2
 #define ELV_K56_FFMA2 1
 #endif
+// Tuning build only (-DELV_K56_SHFL=1): the north star's
+// "register tiles with warp-shuffle reuse" for cache_write -- each lane reads
+// one value per operand row / column from SMEM and the 8 + 8 fragment values
+// of its 8x8 tile come by __shfl_sync (16 shuffles + 3 LDS.32 per k instead
+// of 4 LDS.128); the same values, so the same bits.
+#ifndef ELV_K56_SHFL
+#define ELV_K56_SHFL 0
+#endif
 #ifndef ELV_K56_MINB
 #define ELV_K56_MINB 2
 #endif
@@ -416,11 +424,27 @@ k56_packed_8x8(const float* __restrict__ A, const float* __restrict__ P, float* 
     auto compute = [&](int buf) {
 #pragma unroll
       for (int k = 0; k < G_BK; ++k) {
+#if ELV_K56_SHFL
+        const float a_lo = As[buf][k][wm * 64 + lane], a_hi = As[buf][k][wm * 64 + 32 + lane];
+        const float b_l = Bs[buf][k][wn * 32 + lane];
+        float av[8];
+        float4 b0, b1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          av[i] = __shfl_sync(0xffffffffu, a_lo, lm * 4 + i);
+          av[4 + i] = __shfl_sync(0xffffffffu, a_hi, lm * 4 + i);
+        }
+        b0.x = __shfl_sync(0xffffffffu, b_l, ln * 4 + 0); b0.y = __shfl_sync(0xffffffffu, b_l, ln * 4 + 1);
+        b0.z = __shfl_sync(0xffffffffu, b_l, ln * 4 + 2); b0.w = __shfl_sync(0xffffffffu, b_l, ln * 4 + 3);
+        b1.x = __shfl_sync(0xffffffffu, b_l, 16 + ln * 4 + 0); b1.y = __shfl_sync(0xffffffffu, b_l, 16 + ln * 4 + 1);
+        b1.z = __shfl_sync(0xffffffffu, b_l, 16 + ln * 4 + 2); b1.w = __shfl_sync(0xffffffffu, b_l, 16 + ln * 4 + 3);
+#else
         const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][trow]);
         const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][trow + 32]);
         const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol]);
         const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][tcol + 16]);
         const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#endif
 #if ELV_K56_FFMA2
         const unsigned long long bp[4] = {pack2(b0.x, b0.y), pack2(b0.z, b0.w), pack2(b1.x, b1.y),
                                           pack2(b1.z, b1.w)};
