@@ -1021,6 +1021,132 @@ k6_sgemm_ffma2(const float* __restrict__ PA, const float* __restrict__ PB, float
   }
 }
 
+// The same kernel with the tiles staged by the TMA engine (ELV_K6_BULK=1;
+// K % 32 == 0): the packed panels are contiguous, so one thread issues a
+// 1-D bulk copy (cp.async.bulk) per operand panel and k-block -- 16 KB of A,
+// 8 x 4 KB of B, B staged panel-major [8][BK][32] -- onto the stage's
+// mbarrier (complete_tx), consumers wait on it instead of cp.async groups +
+// __syncthreads, and each warp releases the stage on an "empty" mbarrier.
+// Same fragments, same FFMA2 sequence: bitwise k6_sgemm_ffma2.
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile("{\n.reg .pred p;\nBW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra BW_%=;\n}\n" ::"r"(
+                   s_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1)
+k6_sgemm_bulk(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
+              int M, int N, int K, int ldc) {
+  extern __shared__ __align__(128) float smem_b[];
+  float* As = smem_b;                               // [STAGES][BK][128]
+  float* Bs = smem_b + CP_STAGES * CP_BK * 128;     // [STAGES][8 panels][BK][32]
+  __shared__ __align__(8) uint64_t full[CP_STAGES], empty[CP_STAGES];
+  constexpr int BM = 128, BN = 256;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lm = lane >> 2, ln = lane & 3;
+  const int trow = wm * 64 + lm * 4;
+  const int tcol = wn * 64 + ln * 4;
+  const bool vecC = aligned16(C) && (ldc & 3) == 0;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nkb = K / CP_BK;
+  if (tid == 0) {
+    for (int i = 0; i < CP_STAGES; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  griddep_wait();                                   // packed operands from k_pack_ab
+  uint32_t g0 = 0;                                  // global stage counter (across tiles)
+  for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, g0 += nkb) {
+    const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+    const int row0 = tc.m * BM, col0 = tc.n * BN;
+    const float* pa = PA + (size_t)tc.m * K * BM;
+    const float* pb = PB + (size_t)(col0 >> 5) * K * kPanel;
+    auto issue = [&](uint32_t g, int kb) {          // thread 0
+      const int slot = g % CP_STAGES;
+      if (g >= CP_STAGES) bar_wait(&empty[slot], ((g / CP_STAGES) & 1) ^ 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[slot])),
+                   "r"((uint32_t)(CP_BK * (BM + BN) * 4)) : "memory");
+      bulk_g2s(As + slot * CP_BK * BM, pa + (size_t)kb * CP_BK * BM, CP_BK * BM * 4, &full[slot]);
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        bulk_g2s(Bs + (slot * 8 + p) * CP_BK * kPanel, pb + ((size_t)p * K + (size_t)kb * CP_BK) * kPanel,
+                 CP_BK * kPanel * 4, &full[slot]);
+    };
+
+    unsigned long long acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0ull;
+
+    if (tid == 0)
+      for (int st = 0; st < CP_STAGES - 1 && st < nkb; ++st) issue(g0 + st, st);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const uint32_t g = g0 + kb;
+      const int slot = g % CP_STAGES;
+      if (tid == 0 && kb + CP_STAGES - 1 < nkb) issue(g + CP_STAGES - 1, kb + CP_STAGES - 1);
+      bar_wait(&full[slot], (g / CP_STAGES) & 1);
+      const float* as = As + slot * CP_BK * BM;
+      const float* bs = Bs + slot * 8 * CP_BK * kPanel;
+      float a[2][8];
+      unsigned long long b[2][8];
+      auto lfrag = [&](int sl, int k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * BM + trow);
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * BM + trow + 32);
+        a[sl][0] = a0.x; a[sl][1] = a0.y; a[sl][2] = a0.z; a[sl][3] = a0.w;
+        a[sl][4] = a1.x; a[sl][5] = a1.y; a[sl][6] = a1.z; a[sl][7] = a1.w;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c = tcol + 16 * h;              // column within the 256-wide tile -> panel c / 32
+          const float4 bv = *reinterpret_cast<const float4*>(bs + ((c >> 5) * CP_BK + k) * kPanel + (c & 31));
+          b[sl][2 * h] = pack2(bv.x, bv.y);
+          b[sl][2 * h + 1] = pack2(bv.z, bv.w);
+        }
+      };
+      lfrag(0, 0);
+#pragma unroll
+      for (int k = 0; k < CP_BK; ++k) {
+        if (k + 1 < CP_BK) lfrag((k + 1) & 1, k + 1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const unsigned long long ai = pack2(a[k & 1][i], a[k & 1][i]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ffma2(acc[i][j], ai, b[k & 1][j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[slot])) : "memory");
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
+      if (gi >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int gj = col0 + tcol + h * 16;
+        float* p = C + (size_t)gi * ldc + gj;
+        const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
+        const float v[4] = {lo.x, lo.y, hi.x, hi.y};
+        if (vecC && gj + 3 < N) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (gj + j < N) p[j] = v[j];
+      }
+    }
+  }
+}
+
 // Small problems (fewer 128x256 tiles than SMs, e.g. 1024^3 -> 32): 64x64
 // tiles so every SM gets work, 64 threads x 8x8 outputs (4 LDS.128 per 32
 // FFMA2, so SMEM bandwidth is not the bound), the same packed operands and
@@ -1335,6 +1461,25 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
     const char* e = getenv("ELV_SGEMM_ORDER");
     order = e ? atoi(e) : 3;   // measured at 32768x32768x8192: FFMA2 60.5 TF; scalar 2x2 FFMA blocks 52.6
     if (order < 0 || order > 3) order = 2;
+  }
+  static int bulk = -1;                     // ELV_K6_BULK=1: TMA bulk-copy staging (K % 32 == 0)
+  if (bulk < 0) bulk = getenv("ELV_K6_BULK") ? atoi(getenv("ELV_K6_BULK")) != 0 : 0;
+  if (bulk && order == 3 && K % CP_BK == 0) {
+    static int battr = -1;
+    int bdev = 0;
+    cudaGetDevice(&bdev);
+    if (battr != bdev) {
+      cudaError_t e = cudaFuncSetAttribute(k6_sgemm_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, CP_SMEM);
+      if (e != cudaSuccess) return set_error(ELV_ECUDA, "sgemm_bulk smem attribute: %s", cudaGetErrorString(e));
+      battr = bdev;
+    }
+    const long long tiles = (long long)((M + 127) / 128) * ((N + 255) / 256);
+    long long grid = num_sms();
+    if (grid > tiles) grid = tiles;
+    cudaError_t e = launch_pdl(k6_sgemm_bulk, dim3((unsigned)grid), dim3(256), (size_t)CP_SMEM, st, packedA, packedB,
+                               C, M, N, K, ldc);
+    if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_bulk: %s", cudaGetErrorString(e));
+    return check_launch("gemm_parallel_bulk");
   }
   auto fn = order == 0 ? k6_sgemm_cp<0> : order == 1 ? k6_sgemm_cp<1> : order == 2 ? k6_sgemm_cp<2>
                                                                                       : k6_sgemm_ffma2;
