@@ -445,3 +445,28 @@ def test_tensor_core_variant_on_a_shape_other_than_the_annotation(cuda, enc):
     Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
     ok, worst = oracle.check(C, oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), 512)
     assert ok, worst
+
+
+def test_k6_bulk_copy_staging_is_bitwise(cuda, tmp_path):
+    """k6_sgemm_bulk (ELV_K6_BULK=1, read once per process: TMA bulk copies of
+    the packed panels + mbarriers instead of the cp.async ring) gives the
+    bits of the default parallel-schedule SIMT kernel."""
+    import subprocess
+    import sys
+    M, N, K = 4096, 2048, 256
+    A, B = _device_inputs(M, N, K, 12, cuda)
+    term = schedules.apply("parallel", M, N, K).term
+    C = interp.run_tensor(term, A, B).cpu().numpy()
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (f"import sys; sys.path.insert(0, {repo!r})\n"
+            "import numpy as np, torch\n"
+            "from paper_2002_02268_b200 import interp, schedules, synth\n"
+            f"M, N, K = {M}, {N}, {K}\n"
+            "A = torch.empty((M, K), device='cuda'); synth.fill_device(A, 12, 0)\n"
+            "B = torch.empty((K, N), device='cuda'); synth.fill_device(B, 12, 1)\n"
+            "C = interp.run_tensor(schedules.apply('parallel', M, N, K).term, A, B)\n"
+            f"np.save({str(tmp_path / 'c.npy')!r}, C.cpu().numpy())\n")
+    env = dict(os.environ, ELV_K6_BULK="1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    Cb = np.load(tmp_path / "c.npy")
+    assert np.array_equal(C.view(np.int32), Cb.view(np.int32))
