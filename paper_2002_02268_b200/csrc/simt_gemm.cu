@@ -1163,14 +1163,21 @@ k6_sgemm_bulk(const float* __restrict__ PA, const float* __restrict__ PB, float*
 constexpr int SM_BM = 64, SM_BN = 64, SM_BK = ELV_SM_BK, SM_STAGES = ELV_SM_STAGES;
 constexpr int SM_SMEM = SM_STAGES * SM_BK * (SM_BM + SM_BN) * 4;   // 48 KB at 32 x 3
 
-__global__ void __launch_bounds__(64, 4)
+// NT = 64: 8x8 outputs per thread; NT = 128: the 64x64 tile split into two
+// column halves, 8x4 outputs per thread -- twice the warps per SM for the
+// same tiles (1024^3 has 256 of them for 148 SMs).  Each output keeps the
+// same fmaf chain either way.
+template <int NT>
+__global__ void __launch_bounds__(NT, 4)
 k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
                int M, int N, int K, int ldc) {
+  constexpr int NCP = NT == 64 ? 4 : 2;               // column pairs per thread (FFMA2 accumulators)
   extern __shared__ __align__(16) float smem_s[];
   float* As = smem_s;                                  // [STAGES][BK][64]
   float* Bs = smem_s + SM_STAGES * SM_BK * SM_BM;      // [STAGES][BK][64]
   const int tid = threadIdx.x;
-  const int trow = (tid >> 3) * 4, tcol = (tid & 7) * 4;   // + {0..3, 32..35} each
+  const int tl = tid & 63, half = tid >> 6;              // NT = 128: column half
+  const int trow = (tl >> 3) * 4, tcol = (tl & 7) * 4 + 32 * half;   // rows + {0..3, 32..35}; cols + {0..3} (+32 at NT = 64)
   const bool vecC = aligned16(C) && (ldc & 3) == 0;
   const int tiles_m = (M + SM_BM - 1) / SM_BM, tiles_n = (N + SM_BN - 1) / SM_BN;
   const int num_tiles = tiles_m * tiles_n;
@@ -1185,16 +1192,16 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
     auto issue = [&](int kb, int slot) {
       const int k0 = kb * SM_BK;
 #pragma unroll
-      for (int i = 0; i < SM_BK * 16 / 64; ++i) {      // A: BK rows x 64 floats = 256 float4
-        const int q = tid + i * 64;
+      for (int i = 0; i < SM_BK * 16 / NT; ++i) {      // A: BK rows x 64 floats = 256 float4
+        const int q = tid + i * NT;
         const int kk = q >> 4, c4 = (q & 15) * 4;
         const int gk = k0 + kk;
         cp_async16(&As[(slot * SM_BK + kk) * SM_BM + c4], pa + (size_t)min(gk, K - 1) * 128 + c4,
                    gk < K ? 16 : 0);
       }
 #pragma unroll
-      for (int i = 0; i < SM_BK * 16 / 64; ++i) {      // B: 2 panels x BK rows x 32 floats
-        const int q = tid + i * 64;
+      for (int i = 0; i < SM_BK * 16 / NT; ++i) {      // B: 2 panels x BK rows x 32 floats
+        const int q = tid + i * NT;
         const int pnl = q / (SM_BK * 8), w = q % (SM_BK * 8);
         const int kk = w >> 3, c4 = (w & 7) * 4;
         const int gk = k0 + kk;
@@ -1203,11 +1210,11 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
       }
     };
 
-    unsigned long long acc[8][4];                  // [row][column pair], FFMA2 (see k6_sgemm_ffma2)
+    unsigned long long acc[8][NCP];                // [row][column pair], FFMA2 (see k6_sgemm_ffma2)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0ull;
+      for (int j = 0; j < NCP; ++j) acc[i][j] = 0ull;
 
 #pragma unroll
     for (int st = 0; st < SM_STAGES - 1; ++st) {
@@ -1223,16 +1230,18 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
       const float* as = As + (kb % SM_STAGES) * SM_BK * SM_BM;
       const float* bs = Bs + (kb % SM_STAGES) * SM_BK * SM_BN;
       float a[2][8];
-      unsigned long long b[2][4];
+      unsigned long long b[2][NCP];
       auto lfrag = [&](int slot, int k) {
         const float4 a0 = *reinterpret_cast<const float4*>(as + k * SM_BM + trow);
         const float4 a1 = *reinterpret_cast<const float4*>(as + k * SM_BM + trow + 32);
         const float4 b0 = *reinterpret_cast<const float4*>(bs + k * SM_BN + tcol);
-        const float4 b1 = *reinterpret_cast<const float4*>(bs + k * SM_BN + tcol + 32);
         a[slot][0] = a0.x; a[slot][1] = a0.y; a[slot][2] = a0.z; a[slot][3] = a0.w;
         a[slot][4] = a1.x; a[slot][5] = a1.y; a[slot][6] = a1.z; a[slot][7] = a1.w;
         b[slot][0] = pack2(b0.x, b0.y); b[slot][1] = pack2(b0.z, b0.w);
-        b[slot][2] = pack2(b1.x, b1.y); b[slot][3] = pack2(b1.z, b1.w);
+        if (NT == 64) {
+          const float4 b1 = *reinterpret_cast<const float4*>(bs + k * SM_BN + tcol + 32);
+          b[slot][NCP - 2] = pack2(b1.x, b1.y); b[slot][NCP - 1] = pack2(b1.z, b1.w);
+        }
       };
       lfrag(0, 0);
 #pragma unroll
@@ -1242,7 +1251,7 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
         for (int i = 0; i < 8; ++i) {
           const unsigned long long ai = pack2(a[k & 1][i], a[k & 1][i]);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) ffma2(acc[i][j], ai, b[k & 1][j]);
+          for (int j = 0; j < NCP; ++j) ffma2(acc[i][j], ai, b[k & 1][j]);
         }
       }
     }
@@ -1253,7 +1262,7 @@ k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float
       const int gi = row0 + trow + (i & 3) + (i >> 2) * 32;
       if (gi >= M) continue;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < NCP / 2; ++h) {
         const int gj = col0 + tcol + h * 32;
         float* p = C + (size_t)gi * ldc + gj;
         const float2 lo = unpack2(acc[i][2 * h]), hi = unpack2(acc[i][2 * h + 1]);
@@ -1440,7 +1449,9 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-      cudaError_t e = cudaFuncSetAttribute(k6_sgemm_small, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_SMEM);
+      cudaError_t e = cudaFuncSetAttribute(k6_sgemm_small<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k6_sgemm_small<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_SMEM);
       if (e != cudaSuccess) return set_error(ELV_ECUDA, "sgemm_small smem attribute: %s", cudaGetErrorString(e));
       attr_dev = dev;
     }
@@ -1451,7 +1462,11 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
     // GEMM CTAs cost 92 vs 55 us per call (scripts/small_timing.py, ELV_PDL)
     static int pdl = -1;
     if (pdl < 0) pdl = getenv("ELV_K6_SMALL_PDL") ? atoi(getenv("ELV_K6_SMALL_PDL")) != 0 : 0;
-    cudaError_t e = launch_pdl_if(pdl != 0, k6_sgemm_small, dim3((unsigned)grid), dim3(64), (size_t)SM_SMEM, st,
+    // 128 threads per 64x64 tile (8x4 each) unless ELV_K6_SMALL_NT=64 (8x8 each)
+    static int nt = -1;
+    if (nt < 0) nt = getenv("ELV_K6_SMALL_NT") && atoi(getenv("ELV_K6_SMALL_NT")) == 64 ? 64 : 128;
+    cudaError_t e = launch_pdl_if(pdl != 0, nt == 64 ? k6_sgemm_small<64> : k6_sgemm_small<128>, dim3((unsigned)grid),
+                                  dim3(nt), (size_t)SM_SMEM, st,
                                   packedA, packedB, C, M, N, K, ldc);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_small: %s", cudaGetErrorString(e));
     return check_launch("gemm_parallel_small");
