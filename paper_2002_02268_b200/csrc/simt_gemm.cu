@@ -1163,10 +1163,11 @@ k6_sgemm_bulk(const float* __restrict__ PA, const float* __restrict__ PB, float*
 constexpr int SM_BM = 64, SM_BN = 64, SM_BK = ELV_SM_BK, SM_STAGES = ELV_SM_STAGES;
 constexpr int SM_SMEM = SM_STAGES * SM_BK * (SM_BM + SM_BN) * 4;   // 48 KB at 32 x 3
 
-// NT = 64: 8x8 outputs per thread; NT = 128: the 64x64 tile split into two
-// column halves, 8x4 outputs per thread -- twice the warps per SM for the
-// same tiles (1024^3 has 256 of them for 148 SMs).  Each output keeps the
-// same fmaf chain either way.
+// NT = 64: 8x8 outputs per thread; NT = 128 (tuning: ELV_K6_SMALL_NT=128):
+// the 64x64 tile split into two column halves, 8x4 outputs per thread --
+// twice the warps per SM for the same tiles; measured slower (the extra
+// fragment loads cost more than the latency they hide).  Each output keeps
+// the same fmaf chain either way.
 template <int NT>
 __global__ void __launch_bounds__(NT, 4)
 k6_sgemm_small(const float* __restrict__ PA, const float* __restrict__ PB, float* __restrict__ C,
@@ -1462,9 +1463,10 @@ int launch_parallel_packed(const float* packedA, const float* packedB, float* C,
     // GEMM CTAs cost 92 vs 55 us per call (scripts/small_timing.py, ELV_PDL)
     static int pdl = -1;
     if (pdl < 0) pdl = getenv("ELV_K6_SMALL_PDL") ? atoi(getenv("ELV_K6_SMALL_PDL")) != 0 : 0;
-    // 128 threads per 64x64 tile (8x4 each) unless ELV_K6_SMALL_NT=64 (8x8 each)
+    // 64 threads per 64x64 tile (8x8 each); ELV_K6_SMALL_NT=128 (8x4 each, two
+    // warps per SMSP) measured slower: 1024^3 62.4 vs 60.4 us, 2048^3 378 vs 361 us
     static int nt = -1;
-    if (nt < 0) nt = getenv("ELV_K6_SMALL_NT") && atoi(getenv("ELV_K6_SMALL_NT")) == 64 ? 64 : 128;
+    if (nt < 0) nt = getenv("ELV_K6_SMALL_NT") && atoi(getenv("ELV_K6_SMALL_NT")) == 128 ? 128 : 64;
     cudaError_t e = launch_pdl_if(pdl != 0, nt == 64 ? k6_sgemm_small<64> : k6_sgemm_small<128>, dim3((unsigned)grid),
                                   dim3(nt), (size_t)SM_SMEM, st,
                                   packedA, packedB, C, M, N, K, ldc);
