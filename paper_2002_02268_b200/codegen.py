@@ -132,7 +132,8 @@ class Gen:
         self.elementwise = True          # mode A: lifted array reduces fold per element
         self.strict_maps = False         # mode B: materialise small computing maps
         self.materialised = 0            # array reduces that had to be materialised
-        self.grid: tuple = ()             # smem-tile mode: explicit 2-D grid of 256-thread blocks
+        self.grid: tuple = ()             # smem-tile mode: explicit 2-D grid of `block`-thread blocks
+        self.block = 128
         self.probing = 0                 # >0 inside shape probes
         self.fold_depth = 0              # >0 inside a per-element fold
 
@@ -580,7 +581,8 @@ class Compiled:
     out_shape: tuple
     threads: int = 1       # threads launched
     mode: str = ""         # "per-scalar", "register-tile TMxTN", "smem-tile ..." or "destination-passing"
-    grid: tuple = ()       # explicit (x, y) grid of 256-thread blocks (smem-tile mode); else 1-D over `threads`
+    grid: tuple = ()       # explicit (x, y) grid (smem-tile mode); else 1-D over `threads`
+    block: int = 128       # threads per block
 
 
 def compile_term(term) -> Compiled:
@@ -613,10 +615,10 @@ def compile_term(term) -> Compiled:
     name = "elv_generated"
     args = ", ".join([f"const float* __restrict__ in{i}" for i in range(len(params))] +
                      ["float* __restrict__ out"])
-    block = 256 if g.grid else 128
+    block = g.block
     src = "\n".join([f'extern "C" __global__ void __launch_bounds__({block}) {name}({args}) {{'] + g.head +
                     g.consts + g.lines + ["}"])
-    return Compiled(name, src, tuple(shp for _, shp in params), out_shape, g.threads, g.mode, g.grid)
+    return Compiled(name, src, tuple(shp for _, shp in params), out_shape, g.threads, g.mode, g.grid, g.block)
 
 
 def _inputs_env(g: Gen, params) -> dict:
@@ -774,7 +776,8 @@ def _register_tile(g: Gen, out_shape: tuple) -> Gen | None:
 # emulation (cpu_source) cannot run __syncthreads: this mode is GPU-only.
 SMEM_TILE = True
 SMEM_MIN_OUTPUTS = 1 << 16            # 256 x 256 outputs and up
-SMEM_TLMAX = 32                       # staged iterations per chunk and site
+SMEM_TLMAX = 32                       # staged iterations per chunk and site (x2: double-buffered)
+SMEM_THREAD_TILE = (8, 4)             # outputs per thread (rows, columns)
 _LOOP0 = re.compile(r"^for \(int (\w+) = 0; \1 < (\d+); \+\+\1\) \{$")
 
 
@@ -880,9 +883,11 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
         return None
     v0, T0 = top[1], top[2]
     pmax = max(max(1, _prod(t for _, t in site["inner"])) for site in sites.values())
+    import os
+    tlmax = int(os.environ.get("ELV_CG_SMEM_TL", SMEM_TLMAX))   # tuning sweeps
     ch = 1
     for c in range(1, T0 + 1):
-        if T0 % c == 0 and c * pmax <= SMEM_TLMAX:
+        if T0 % c == 0 and c * pmax <= tlmax:
             ch = c
     for idx, key in enumerate(order):
         site = sites[key]
@@ -906,16 +911,25 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
             site["tl_fast"] = d_tl == 1
         except Exception:
             return None
+    TM, TN = SMEM_THREAD_TILE
+    import os
+    if os.environ.get("ELV_CG_SMEM_TILE"):                 # tuning sweeps, e.g. 8x4
+        TM, TN = (int(x) for x in os.environ["ELV_CG_SMEM_TILE"].split("x"))
+    if TM not in (2, 4, 8) or TN not in (4, 8):
+        return None
+    nx, ny = 64 // TN, 64 // TM
+    NT = nx * ny                                           # threads per 64 x 64 block
     t = Gen()
     t.consts = g.consts
-    t.head = [f"  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;",
+    t.head = [f"  const int tx = threadIdx.x % {nx}, ty = threadIdx.x / {nx};",
               f"  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;"]
-    t.head += [f"  const int o0_{i} = row0 + 4 * ty + {i};" for i in range(4)]
-    t.head += [f"  const int o1_{j} = col0 + 4 * tx + {j};" for j in range(4)]
+    t.head += [f"  const int o0_{i} = row0 + {TM} * ty + {i};" for i in range(TM)]
+    t.head += [f"  const int o1_{j} = col0 + {TN} * tx + {j};" for j in range(TN)]
     for key in order:
         site = sites[key]
         size = 64 * (site["TL"] + 1) if site["role"] == "r" else site["TL"] * 64
-        t.head.append(f"  __shared__ __align__(16) float {site['name']}[{size}];")
+        site["size"] = size
+        t.head.append(f"  __shared__ __align__(16) float {site['name']}[2 * {size}];")
     names = re.compile(r"\b(" + "|".join(sorted(map(re.escape, locals_), key=len, reverse=True)) + r")\b") \
         if locals_ else None
 
@@ -926,7 +940,7 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
             site = sites[key]
             if key[2] != tuple(loaded):
                 continue
-            rep = f"ra{site['name']}_{i}" if site["role"] == "r" else f"cb{site['name']}.{'xyzw'[j]}"
+            rep = f"ra{site['name']}_{i}" if site["role"] == "r" else f"cb{site['name']}_{j // 4}.{'xyzw'[j % 4]}"
             text = text.replace(f"{inp}[{e}]", rep)
         if names is not None:
             text = names.sub(lambda mm: f"{mm.group(1)}_{i}_{j}", text)
@@ -955,63 +969,91 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
                 site = sites[key]
                 tl = tl_expr(site)
                 if site["role"] == "r":
-                    for i in range(4):
+                    for i in range(TM):
                         t.lines.append(indent + f"const float ra{site['name']}_{i} = "
-                                       f"{site['name']}[(4 * ty + {i}) * {site['TL'] + 1} + ({tl})];")
+                                       f"{site['name']}[buf * {site['size']} + ({TM} * ty + {i}) * {site['TL'] + 1} + ({tl})];")
                 else:
-                    t.lines.append(indent + f"const float4 cb{site['name']} = *reinterpret_cast<const float4*>("
-                                   f"&{site['name']}[({tl}) * 64 + 4 * tx]);")
-            for i in range(4):
-                for j in range(4):
+                    for h in range(TN // 4):
+                        t.lines.append(indent + f"const float4 cb{site['name']}_{h} = *reinterpret_cast<const float4*>("
+                                       f"&{site['name']}[buf * {site['size']} + ({tl}) * 64 + {TN} * tx + {4 * h}]);")
+            for i in range(TM):
+                for j in range(TN):
                     t.lines.append(indent + inst(st, i, j, path))
+
+    def stage_code(base_expr, store, indent):
+        """Load (store=False: into registers stg<site>_<q>) or store (into the
+        buffer half `buf`) the staged values of the chunk starting at
+        outer-loop index `base_expr`."""
+        for key in order:
+            inp, e, _ = key
+            site = sites[key]
+            TL = site["TL"]
+            total = 64 * TL
+            iters = (total + NT - 1) // NT
+            size = 64 * (TL + 1) if site["role"] == "r" else TL * 64
+            for q in range(iters):
+                t.lines.append(indent + "{")
+                t.lines.append(indent + f"  const int idx = threadIdx.x + {NT * q};")
+                guard = f"idx < {total}" if total % NT else None
+                if site["tl_fast"]:
+                    t.lines.append(indent + f"  const int tl = idx % {TL}, rr = idx / {TL};")
+                else:
+                    t.lines.append(indent + f"  const int tl = idx / 64, rr = idx % 64;")
+                if store:
+                    dst = f"rr * {TL + 1} + tl" if site["role"] == "r" else "tl * 64 + rr"
+                    st = f"{site['name']}[buf * {size} + {dst}] = stg{site['name']}_{q};"
+                else:
+                    rem, stride = "tl", 1
+                    for v, tr in reversed(site["inner"]):
+                        t.lines.append(indent + f"  const int {v} = ({rem} / {stride}) % {tr};")
+                        stride *= tr
+                    t.lines.append(indent + f"  const int {v0} = {base_expr} + tl / {stride};")
+                    o = "o0" if site["role"] == "r" else "o1"
+                    base = "row0" if site["role"] == "r" else "col0"
+                    ex = re.sub(rf"\b{o}\b", f"({base} + rr)", e)
+                    st = f"stg{site['name']}_{q} = {inp}[{ex}];"
+                t.lines.append(indent + "  " + (f"if ({guard}) " if guard else "") + st)
+                t.lines.append(indent + "}")
 
     for n in root:
         if n is top:
-            t.lines.append(f"  for (int {v0}_b = 0; {v0}_b < {T0}; {v0}_b += {ch}) {{")
-            t.lines.append("    __syncthreads();")
+            # double-buffered: the next chunk's values are loaded into registers
+            # while the current chunk computes, then stored to the other half
             for key in order:
-                inp, e, _ = key
                 site = sites[key]
-                TL = site["TL"]
-                total = 64 * TL
-                iters = (total + 255) // 256
-                loopvars = site["inner"]
-                t.lines.append("    #pragma unroll")
-                t.lines.append(f"    for (int q = 0; q < {iters}; ++q) {{")
-                t.lines.append(f"      const int idx = threadIdx.x + 256 * q;")
-                if total % 256:
-                    t.lines.append(f"      if (idx >= {total}) break;")
-                if site["tl_fast"]:
-                    t.lines.append(f"      const int tl = idx % {TL}, rr = idx / {TL};")
-                else:
-                    t.lines.append(f"      const int tl = idx / 64, rr = idx % 64;")
-                rem, stride = "tl", 1
-                for v, tr in reversed(loopvars):
-                    t.lines.append(f"      const int {v} = ({rem} / {stride}) % {tr};")
-                    stride *= tr
-                t.lines.append(f"      const int {v0} = {v0}_b + tl / {stride};")
-                o = "o0" if site["role"] == "r" else "o1"
-                base = "row0" if site["role"] == "r" else "col0"
-                ex = re.sub(rf"\b{o}\b", f"({base} + rr)", e)
-                dst = f"rr * {TL + 1} + tl" if site["role"] == "r" else "tl * 64 + rr"
-                t.lines.append(f"      {site['name']}[{dst}] = {inp}[{ex}];")
-                t.lines.append("    }")
-            t.lines.append("    __syncthreads();")
+                iters = (64 * site["TL"] + NT - 1) // NT
+                t.lines.append("  float " + ", ".join(f"stg{site['name']}_{q} = 0.f" for q in range(iters)) + ";")
+            t.lines.append("  int buf = 0;")
+            stage_code("0", False, "  ")
+            stage_code(None, True, "  ")
+            t.lines.append("  __syncthreads();")
+            t.lines.append(f"  for (int {v0}_b = 0; {v0}_b < {T0}; {v0}_b += {ch}, buf ^= 1) {{")
+            t.lines.append(f"    const bool more = {v0}_b + {ch} < {T0};")
+            t.lines.append("    if (more) {")
+            stage_code(f"{v0}_b + {ch}", False, "      ")
+            t.lines.append("    }")
             t.lines.append("    #pragma unroll 4")
             t.lines.append(f"    for (int {v0} = {v0}_b; {v0} < {v0}_b + {ch}; ++{v0}) {{")
             emit_nodes(top[3], "      ", [])
             t.lines.append("    }")
+            t.lines.append("    if (more) {")
+            t.lines.append("      buf ^= 1;")
+            stage_code(None, True, "      ")
+            t.lines.append("      buf ^= 1;")
+            t.lines.append("    }")
+            t.lines.append("    __syncthreads();")
             t.lines.append("  }")
         else:
-            for i in range(4):
-                for j in range(4):
+            for i in range(TM):
+                for j in range(TN):
                     t.lines.append("  " + inst(n[1], i, j, None))
-    for i in range(4):
-        for j in range(4):
+    for i in range(TM):
+        for j in range(TN):
             t.lines.append(f"  out[(long long)o0_{i} * {O1} + o1_{j}] = {inst(out_expr, i, j, None)};")
-    t.threads = O0 * O1 // 16
+    t.threads = O0 * O1 // (TM * TN)
     t.grid = (O1 // 64, O0 // 64)
-    t.mode = f"smem-tile 4x4 (64x64 block, {ch} x {pmax} iterations staged per chunk)"
+    t.block = NT
+    t.mode = f"smem-tile {TM}x{TN} (64x64 block, {ch} x {pmax} iterations staged per chunk)"
     return t
 
 
@@ -1126,7 +1168,8 @@ class Kernel:
         arg_ptrs = np.array([ctypes.addressof(p) for p in ptrs], dtype=np.uint64)
         if self.c.grid:
             gx, gy = self.c.grid
-            _check(d.cuLaunchKernel(self.fn, gx, gy, 1, 256, 1, 1, 0, d.CUstream(stream), arg_ptrs.ctypes.data, 0))
+            _check(d.cuLaunchKernel(self.fn, gx, gy, 1, self.c.block, 1, 1, 0, d.CUstream(stream),
+                                    arg_ptrs.ctypes.data, 0))
             return
         block = 128
         grid = max(1, (total + block - 1) // block)
