@@ -616,7 +616,8 @@ def compile_term(term) -> Compiled:
     args = ", ".join([f"const float* __restrict__ in{i}" for i in range(len(params))] +
                      ["float* __restrict__ out"])
     block = g.block
-    src = "\n".join([f'extern "C" __global__ void __launch_bounds__({block}) {name}({args}) {{'] + g.head +
+    pre = [F32X2_PRELUDE] if g.grid and SMEM_F32X2 else []
+    src = "\n".join(pre + [f'extern "C" __global__ void __launch_bounds__({block}) {name}({args}) {{'] + g.head +
                     g.consts + g.lines + ["}"])
     return Compiled(name, src, tuple(shp for _, shp in params), out_shape, g.threads, g.mode, g.grid, g.block)
 
@@ -977,8 +978,8 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
                         t.lines.append(indent + f"const float4 cb{site['name']}_{h} = *reinterpret_cast<const float4*>("
                                        f"&{site['name']}[buf * {site['size']} + ({tl}) * 64 + {TN} * tx + {4 * h}]);")
             for i in range(TM):
-                for j in range(TN):
-                    t.lines.append(indent + inst(st, i, j, path))
+                insts = [inst(st, i, j, path) for j in range(TN)]
+                t.lines.extend(indent + x for x in (_pair_f32x2(insts) if SMEM_F32X2 else insts))
 
     def stage_code(base_expr, store, indent):
         """Load (store=False: into registers stg<site>_<q>) or store (into the
@@ -1055,6 +1056,51 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
     t.block = NT
     t.mode = f"smem-tile {TM}x{TN} (64x64 block, {ch} x {pmax} iterations staged per chunk)"
     return t
+
+
+_FMA_INST = re.compile(r"^(\w+) = fmaf\(([\w.]+), ([\w.]+), \1\);$")
+_ADD_INST = re.compile(r"^(\w+) = \(\1 \+ (\w+)\);$")
+SMEM_F32X2 = True                     # pair adjacent outputs' fmaf / add into sm_100 f32x2 instructions
+F32X2_PRELUDE = r"""
+__device__ __forceinline__ void elv_fma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  unsigned long long a, b, d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(d0), "f"(d1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+__device__ __forceinline__ void elv_add2(float& d0, float& d1, float b0, float b1) {
+  unsigned long long b, d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(d0), "f"(d1));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(d) : "l"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+"""
+
+
+def _pair_f32x2(insts: list) -> list:
+    """Adjacent outputs' `x = fmaf(a, b, x)` / `x = (x + y)` statements as one
+    fma.rn.f32x2 / add.rn.f32x2 (each lane an IEEE fmaf / add: the same bits,
+    half the FP32 issue slots -- the template kernels' FFMA2)."""
+    out, j = [], 0
+    while j < len(insts):
+        if j + 1 < len(insts):
+            m0, m1 = _FMA_INST.match(insts[j]), _FMA_INST.match(insts[j + 1])
+            if m0 and m1:
+                out.append(f"elv_fma2({m0.group(1)}, {m1.group(1)}, {m0.group(2)}, {m1.group(2)}, "
+                           f"{m0.group(3)}, {m1.group(3)});")
+                j += 2
+                continue
+            a0, a1 = _ADD_INST.match(insts[j]), _ADD_INST.match(insts[j + 1])
+            if a0 and a1:
+                out.append(f"elv_add2({a0.group(1)}, {a1.group(1)}, {a0.group(2)}, {a1.group(2)});")
+                j += 2
+                continue
+        out.append(insts[j])
+        j += 1
+    return out
 
 
 def _prod(xs) -> int:
