@@ -676,7 +676,41 @@ def ladder_cases(dev, reps_small=20, reps_large=5, with_odd=True):
                     "reps": reps})
         del A, B, C, call
         torch.cuda.empty_cache()
+    out.append(_generated_case(dev, flush, reps_small))
     return out
+
+
+def _generated_case(dev, flush, reps, n=1024):
+    """A user schedule outside the seven templates -- tile(16,16) then split(2)
+    of the reduction (reference rules only) -- at 1024^3 through the general
+    compiler (codegen.py: one NVRTC sm_100a kernel, shared-memory tile mode),
+    with the same parity bit."""
+    import torch
+    from paper_2002_02268_b200 import codegen, schedules, synth
+    from paper_2002_02268_b200._ref import S
+    st, nf, tv, rules = S().strategy, S().normal_forms, S().traversals, S().rules
+    strat = st.seq(nf.dfnf_seq(tv.top_down(schedules.tile(16, 16)),
+                               tv.top_down(st.seq(tv.is_reduce, rules.make_split(2)))), nf.LOWER_TO_C)
+    term = st.run_strategy(strat, schedules.mm(n, n, n))[0].term
+    A = torch.empty((n, n), device=dev); synth.fill_device(A, 0, 0)
+    B = torch.empty((n, n), device=dev); synth.fill_device(B, 0, 1)
+    t0 = time.perf_counter()
+    C = codegen.run(term, [A, B])
+    torch.cuda.synchronize()
+    first_s = time.perf_counter() - t0
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        e0.record(); C = codegen.run(term, [A, B]); e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ok, ratio = _parity_rows(A, B, C, n, [0, 1, n // 3, n // 2, n - 1])
+    ms = statistics.median(ts)
+    return {"config": "generated (a user schedule outside the templates)", "variant": "user tile(16,16)+split(2)",
+            "kernel_variant_id": None, "M": n, "N": n, "K": n, "gflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "ms": ms,
+            "mode": codegen.kernel_for(term).c.mode, "first_call_s": first_s, "parity_ok": ok,
+            "parity_worst": ratio, "reps": reps}
 
 
 def run_ladder(args, dev):

@@ -890,10 +890,14 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
     for c in range(1, T0 + 1):
         if T0 % c == 0 and c * pmax <= tlmax:
             ch = c
+    smem_floats = 0
     for idx, key in enumerate(order):
         site = sites[key]
         site["P"] = max(1, _prod(t for _, t in site["inner"]))
         site["TL"] = ch * site["P"]
+        smem_floats += 2 * 64 * (site["TL"] + 1)
+        if smem_floats * 4 > 48 * 1024 or site["TL"] > 128:
+            return None                                  # static shared memory / staging registers
         site["name"] = f"sm{idx}"
         # which staging axis is contiguous in global memory (probe the index)
         loopvars = [(v0, T0)] + site["inner"]
