@@ -70,7 +70,8 @@ def test_tiled_generated_kernel_at_1024(cuda, name):
     assert torch.equal(codegen.run(term, [A, B]), interp.run_tensor(term, A, B))
 
 
-def _user_terms(n):
+def _user_terms(M, N=None, K=None):
+    N, K = N or M, K or M
     from paper_2002_02268_b200._ref import S
     st, nf, tv, rules = S().strategy, S().normal_forms, S().traversals, S().rules
     out = {}
@@ -78,20 +79,22 @@ def _user_terms(n):
                                "tile64_split4": (64, 64, 4)}.items():
         strat = st.seq(nf.dfnf_seq(tv.top_down(schedules.tile(ti, tj)),
                                    tv.top_down(st.seq(tv.is_reduce, rules.make_split(sp)))), nf.LOWER_TO_C)
-        out[name] = st.run_strategy(strat, schedules.mm(n, n, n))[0].term
+        out[name] = st.run_strategy(strat, schedules.mm(M, N, K))[0].term
     return out
 
 
-@pytest.mark.parametrize("n", [256, 1024])
-def test_smem_tile_mode_is_bitwise_the_register_tile_mode(cuda, n, monkeypatch):
+@pytest.mark.parametrize("shape", [(256, 256, 256), (1024, 1024, 1024), (512, 256, 768), (256, 1024, 128)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_smem_tile_mode_is_bitwise_the_register_tile_mode(cuda, shape, monkeypatch):
     """Mode A'' stages each load site's values in shared memory and keeps every
     output's per-scalar statement sequence: the same bits as the register-tile
     (and per-scalar) kernels, for user schedules outside the templates and the
     seven schedules."""
-    terms = _user_terms(n)
-    terms.update({name: schedules.apply(name, n, n, n).term for name in ("blocking", "cacheBlocks", "baseline")})
-    A = torch.empty((n, n), device=cuda); synth.fill_device(A, 7, 0)
-    B = torch.empty((n, n), device=cuda); synth.fill_device(B, 7, 1)
+    M, N, K = shape
+    terms = _user_terms(M, N, K)
+    terms.update({name: schedules.apply(name, M, N, K).term for name in ("blocking", "cacheBlocks", "baseline")})
+    A = torch.empty((M, K), device=cuda); synth.fill_device(A, 7, 0)
+    B = torch.empty((K, N), device=cuda); synth.fill_device(B, 7, 1)
     stream = torch.cuda.current_stream().cuda_stream
     for name, term in terms.items():
         outs = {}
@@ -99,7 +102,7 @@ def test_smem_tile_mode_is_bitwise_the_register_tile_mode(cuda, n, monkeypatch):
             monkeypatch.setattr(codegen, "SMEM_TILE", smem)
             k = codegen.Kernel(codegen.compile_term(term))
             assert k.c.mode.startswith("smem-tile") == smem, (name, k.c.mode)
-            C = torch.empty((n, n), device=cuda)
+            C = torch.empty((M, N), device=cuda)
             k([A, B], C, stream)
             outs[smem] = C
         torch.cuda.synchronize()
