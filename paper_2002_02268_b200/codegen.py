@@ -41,6 +41,7 @@ from __future__ import annotations
 
 import functools
 import itertools
+import os
 import random
 import re
 from dataclasses import dataclass
@@ -684,7 +685,6 @@ def _register_tile(g: Gen, out_shape: tuple) -> Gen | None:
         return None
     O0, O1 = out_shape
     tile = None
-    import os
     shapes = ((8, 4), (4, 4), (2, 2))         # measured at 1024^3: 8x4 13.8, 4x4 12.3, per-scalar 7.4 TF
     if os.environ.get("ELV_CG_TILE"):                   # tuning experiments
         shapes = (tuple(int(x) for x in os.environ["ELV_CG_TILE"].split("x")),) + shapes
@@ -884,7 +884,6 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
         return None
     v0, T0 = top[1], top[2]
     pmax = max(max(1, _prod(t for _, t in site["inner"])) for site in sites.values())
-    import os
     tlmax = int(os.environ.get("ELV_CG_SMEM_TL", SMEM_TLMAX))   # tuning sweeps
     ch = 1
     for c in range(1, T0 + 1):
@@ -917,7 +916,6 @@ def _smem_tile(g: Gen, out_shape: tuple) -> Gen | None:
         except Exception:
             return None
     TM, TN = SMEM_THREAD_TILE
-    import os
     if os.environ.get("ELV_CG_SMEM_TILE"):                 # tuning sweeps, e.g. 8x4
         TM, TN = (int(x) for x in os.environ["ELV_CG_SMEM_TILE"].split("x"))
     if TM not in (2, 4, 8) or TN not in (4, 8):
