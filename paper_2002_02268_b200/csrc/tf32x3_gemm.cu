@@ -312,6 +312,22 @@ __device__ __forceinline__ void mma_chunk(uint32_t d, const uint64_t (&ahi)[CH],
     }
 }
 
+#ifdef ELV_K7_PROF
+// cycle accounting for tuning builds only (scripts/k7_prof.sh):
+// [0] MMA: waiting tempty  [1] MMA: waiting full  [2] MMA: total
+// [3] producer: waiting empty  [4] producer: wave sync  [5] epilogue: waiting tfull
+// [6] epilogue: drain  [7] tiles
+// [5] epilogue: waiting tfull  [6] epilogue: store per tile  [8] epilogue: TMEM drain (ld + add)
+// [9] epilogue: chunks  [10] epilogue: arrive  [11] (1-CTA kernel) entry -> after griddepcontrol.wait
+constexpr int K7_PROF_SLOTS = 12;
+__device__ unsigned long long g_k7_prof[512][K7_PROF_SLOTS];
+#define PROF_T(x) const long long x = clock64()
+#define PROF_ADD(i, v) prof[i] += (unsigned long long)(v)
+#else
+#define PROF_T(x)
+#define PROF_ADD(i, v)
+#endif
+
 template <int TBN, int TBK, bool F16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
@@ -339,6 +355,10 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef ELV_K7_PROF
+  unsigned long long prof[K7_PROF_SLOTS] = {};
+#endif
+  PROF_T(k_entry);
   const TileSched sched{(M + BM - 1) / BM, (N + BN - 1) / BN, group, BN};
   const int num_tiles = sched.tiles_m * sched.tiles_n;
 
@@ -361,6 +381,8 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
   const uint32_t tmem_base = *tmem_holder;
   griddep_wait();                                   // operand planes from the preceding split kernel
   griddep_launch_dependents();                      // the range-guard fix-up may be scheduled (it waits for us)
+  PROF_T(k_ready);
+  PROF_ADD(11, k_ready - k_entry);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -372,7 +394,10 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
         sched.coords(t, m0, n0);
         if (wave_ctr != nullptr && wave > 0) wave_sync_wait(wave_ctr, (unsigned)(wave * gridDim.x));
         for (int kb = 0; kb < num_kb; ++kb) {
+          PROF_T(e0);
           mbar_wait(&empty[s], ph ^ 1);
+          PROF_T(e1);
+          PROF_ADD(3, e1 - e0);
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], STAGE_BYTES);
           const int k0 = kb * TBK;
@@ -390,10 +415,15 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
       // ---------------- MMA issuer: one accumulation chunk per CH stages ----------------
       int s = 0; uint32_t ph = 0;
       uint32_t q = 0;                                  // chunk counter (TMEM buffer q % NBUF)
+      PROF_T(m_start);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        PROF_ADD(7, 1);
         for (int kb = 0; kb < num_kb; kb += CH, ++q) {
           const uint32_t b = q % NBUF;
+          PROF_T(q0);
           mbar_wait(&tempty[b], ((q / NBUF) & 1) ^ 1);
+          PROF_T(f0);
+          PROF_ADD(0, f0 - q0);
           uint64_t ahi[CH], alo[CH], bhi[CH], blo[CH];
           int ss[CH];
 #pragma unroll
@@ -407,6 +437,8 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
             ss[j] = s;
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
+          PROF_T(f1);
+          PROF_ADD(1, f1 - f0);
           tc_fence_after();
           mma_chunk<false, F16, Cfg::KSUB, CH>(tmem_base + b * (uint32_t)BN, ahi, alo, bhi, blo, kIdesc, with_lolo);
 #pragma unroll
@@ -414,6 +446,8 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           tc_commit(&tfull[b]);                                    // chunk complete in buffer b
         }
       }
+      PROF_T(m_end);
+      PROF_ADD(2, m_end - m_start);
     }
   } else {
     // ---------------- epilogue (warps 2..9): C = RN-sum of the chunks ----------------
@@ -432,13 +466,18 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 #pragma unroll 1
       for (int kb = 0; kb < num_kb; kb += CH, ++q) {
         const uint32_t b = q % NBUF;
+        PROF_T(c0);
         mbar_wait(&tfull[b], (q / NBUF) & 1);
         tc_fence_after();
+        PROF_T(c1);
+        PROF_ADD(5, c1 - c0);
+        PROF_ADD(9, 1);
         drain_add<NC>(lane_base + b * (uint32_t)BN, acc);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
       }
+      PROF_T(d1);
       float* crow = C + (size_t)row * ldc;
       const int er = (F16 && row < M) ? pow2_exp(__ldg(inv_s + row)) : 0;
 #pragma unroll
@@ -482,8 +521,14 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
           }
         }
       }
+      PROF_T(d2);
+      PROF_ADD(6, d2 - d1);
     }
   }
+#ifdef ELV_K7_PROF
+  if (lane == 0 && warp <= 2 && blockIdx.x < 512)
+    for (int i = 0; i < K7_PROF_SLOTS; ++i) if (prof[i]) atomicAdd(&g_k7_prof[blockIdx.x][i], prof[i]);
+#endif
 
   tc_fence_before();
   __syncthreads();
@@ -502,21 +547,6 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
 // Per SM this halves the B operand's SMEM reads and L2->SMEM fills relative
 // to the 1-CTA kernel (the 1-CTA kernel measured L1/SMEM throughput 88 %,
 // its limiter), for the same MMA work.
-#ifdef ELV_K7_PROF
-// cycle accounting for tuning builds only (scripts/k7_prof.sh):
-// [0] MMA: waiting tempty  [1] MMA: waiting full  [2] MMA: total
-// [3] producer: waiting empty  [4] producer: wave sync  [5] epilogue: waiting tfull
-// [6] epilogue: drain  [7] tiles
-// [5] epilogue: waiting tfull  [6] epilogue: store per tile  [8] epilogue: TMEM drain (ld + add)
-// [9] epilogue: chunks  [10] epilogue: arrive
-constexpr int K7_PROF_SLOTS = 12;
-__device__ unsigned long long g_k7_prof[512][K7_PROF_SLOTS];
-#define PROF_T(x) const long long x = clock64()
-#define PROF_ADD(i, v) prof[i] += (unsigned long long)(v)
-#else
-#define PROF_T(x)
-#define PROF_ADD(i, v)
-#endif
 
 constexpr int P_BM = 128;                          // rows per CTA (pair: 256)
 // warps: 0 TMA producer, 1 MMA issuer, 2..9 epilogue (two per TMEM lane
