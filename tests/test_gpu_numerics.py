@@ -214,3 +214,25 @@ def test_small_problem_paths_bitwise(cuda, enc, shape, monkeypatch):
         assert torch.equal(torch.nan_to_num(C[r], nan=7.0), torch.nan_to_num(C6[r], nan=7.0))
     for c in (2, N - 1):
         assert torch.equal(torch.nan_to_num(C[:, c], nan=7.0), torch.nan_to_num(C6[:, c], nan=7.0))
+
+
+@pytest.mark.parametrize("enc", ENCODINGS)
+def test_small_problem_fixup_with_padded_operands(cuda, enc):
+    """The in-kernel range-guard fix-up reads A and B through their leading
+    dimensions: strided (padded) operands give the bits of contiguous ones."""
+    M, N, K = 768, 640, 1024
+    Ab = torch.empty((M, K + 20), device=cuda)
+    Bb = torch.empty((K, N + 36), device=cuda)
+    synth.fill_device(Ab, 6, 0)
+    synth.fill_device(Bb, 6, 1)
+    A, B = Ab[:, :K], Bb[:, :N]
+    A[11, 5] = 2.0 ** -110
+    B[7, 300] = float("inf")
+    term = schedules.apply("parallel", M, N, K).term
+    C = _tc(term, A, B, enc)
+    Cc = _tc(term, A.contiguous(), B.contiguous(), enc)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.nan_to_num(C, nan=7.0), torch.nan_to_num(Cc, nan=7.0))
+    C6 = interp.run_tensor(term, A.contiguous(), B.contiguous(), tf32x3=False)
+    assert torch.equal(torch.nan_to_num(C[11], nan=7.0), torch.nan_to_num(C6[11], nan=7.0))
+    assert torch.equal(torch.nan_to_num(C[:, 300], nan=7.0), torch.nan_to_num(C6[:, 300], nan=7.0))
