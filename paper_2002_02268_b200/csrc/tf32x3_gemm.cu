@@ -556,20 +556,26 @@ constexpr int P_EPI_WARPS = 8;
 constexpr int P_BN = 256;                          // columns per pair tile (128 per CTA staged)
 // BKT = K elements per stage; F16: operands are scaled fp16 hi/lo planes
 // (2 B per element, kind::f16, 16 K per MMA) instead of tf32 (4 B, 8 K).
-template <int BKT, bool F16 = false> struct PairCfg {
+// PBN: columns per pair tile -- 256 for large problems; 128 / 64 for small
+// ones, where wide tiles would leave SMs idle (the narrow pair still reads
+// half of B per SM and issues M = 256 MMAs, unlike the 1-CTA kernel).
+template <int BKT, bool F16 = false, int PBN = P_BN> struct PairCfg {
   static constexpr int EB = F16 ? 2 : 4;                   // bytes per element
   static constexpr int ROW_BYTES = BKT * EB;                // 64 or 128 (swizzle width)
-  static constexpr int STAGES = ROW_BYTES == 128 ? 3 : 6;
   static constexpr int A_TILE = P_BM * ROW_BYTES;           // 8 / 16 KB
-  static constexpr int B_TILE = (P_BN / 2) * ROW_BYTES;     // this CTA's half of Bt
+  static constexpr int B_TILE = (PBN / 2) * ROW_BYTES;      // this CTA's half of Bt
   static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+  static constexpr int STAGES = PBN == 256 ? (ROW_BYTES == 128 ? 3 : 6)
+                                           : ((192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES);
+  static constexpr int NBUF = 512 / PBN;                     // TMEM chunk buffers
   // epilogue staging for TMA stores of C: one 32 x 32 fp32 tile (4 KB) per epilogue warp
   static constexpr int EPI_BYTES = 8 * 32 * 32 * 4;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 256 + 1024;
+  static constexpr int BAR_BYTES = PBN == 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES + 1024;
   static constexpr int KSUB = BKT / (F16 ? 16 : 8);         // MMAs per product per stage
   // idesc: D f32; A/B type tf32 (2) or f16 (0); K-major both; N, M
   static constexpr uint32_t IDESC = (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
-                                    ((uint32_t)(P_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+                                    ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -675,21 +681,22 @@ __device__ __forceinline__ void tc_mma_pair_sc11(uint32_t d_tmem, uint64_t a_des
                  : "memory");
 }
 
-template <int BKT, bool F16, bool TMA_C>
+template <int BKT, bool F16, bool TMA_C, int PBN = P_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_NUM_THREADS, 1)
 k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                const __grid_constant__ CUtensorMap map_c,
                float* __restrict__ C, int M, int N, int ldc, int num_kb, int with_lolo, int group,
                unsigned int* __restrict__ wave_ctr, const float* __restrict__ inv_s,
-               const float* __restrict__ inv_t, int l2_hints) {
-  using Cfg = PairCfg<BKT, F16>;
+               const float* __restrict__ inv_t, int l2_hints, const FixArgs fix, int K) {
+  using Cfg = PairCfg<BKT, F16, PBN>;
+  constexpr int NBUF = Cfg::NBUF;
   constexpr int P_STAGES = Cfg::STAGES;
   constexpr int P_A_TILE = Cfg::A_TILE;
   constexpr int P_B_TILE = Cfg::B_TILE;
   constexpr int P_STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr uint32_t kIdescPair = Cfg::IDESC;
-  constexpr int NC = P_BN / 2 / 32;                  // 32-column groups per epilogue warp (its half)
+  constexpr int NC = PBN / 2 / 32;                   // 32-column groups per epilogue warp (its half)
   constexpr int CH = ChunkK<F16>::value / BKT;           // stages per accumulation chunk
   static_assert(CH >= 1 && CH * BKT == ChunkK<F16>::value, "chunk length");
   extern __shared__ uint8_t smem_raw[];
@@ -697,9 +704,9 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
   uint8_t* epi_stage = smem + P_STAGES * P_STAGE_BYTES;      // 1 KB-aligned (stages are)
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + Cfg::EPI_BYTES);
   uint64_t* empty = full + P_STAGES;
-  uint64_t* tfull = empty + P_STAGES;                // [2]
-  uint64_t* tempty = tfull + 2;                      // [2] (leader's copy counts both CTAs' warps)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + P_STAGES;                // [NBUF]
+  uint64_t* tempty = tfull + NBUF;                   // [NBUF] (leader's copy counts both CTAs' warps)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef ELV_K7_PROF
@@ -707,7 +714,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
 #endif
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int tiles_m = (M + 2 * P_BM - 1) / (2 * P_BM), tiles_n = (N + P_BN - 1) / P_BN;
+  const int tiles_m = (M + 2 * P_BM - 1) / (2 * P_BM), tiles_n = (N + PBN - 1) / PBN;
   const int num_tiles = tiles_m * tiles_n;
   const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
 
@@ -716,7 +723,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     tma_prefetch_desc(&map_bhi); tma_prefetch_desc(&map_blo);
     if (TMA_C) tma_prefetch_desc(&map_c);
     for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * P_EPI_WARPS); }
+    for (int b = 0; b < NBUF; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * P_EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -741,7 +748,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
     const int gm = min(tiles_m - first_m, GROUP);
     const int in = t - g * per_group;
     m0 = (first_m + in % gm) * 2 * P_BM;
-    n0 = (in / gm) * P_BN;
+    n0 = (in / gm) * PBN;
   };
 
   if (warp == 0) {
@@ -759,7 +766,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
         if (wave_ctr != nullptr && wave > 0) wave_sync_wait(wave_ctr, (unsigned)(wave * gridDim.x));
         PROF_T(w1);
         PROF_ADD(4, w1 - w0);
-        const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (P_BN / 2);
+        const int ma = m0 + (int)rank * P_BM, nb = n0 + (int)rank * (PBN / 2);
         for (int kb = 0; kb < num_kb; ++kb) {
           PROF_T(e0);
           mbar_wait(&empty[s], ph ^ 1);
@@ -805,9 +812,9 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         PROF_ADD(7, 1);
         for (int kb = 0; kb < num_kb; kb += CH, ++q) {
-          const uint32_t b = q & 1;
+          const uint32_t b = q % NBUF;
           PROF_T(q0);
-          mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
+          mbar_wait(&tempty[b], ((q / NBUF) & 1) ^ 1);
           PROF_T(f0);
           PROF_ADD(0, f0 - q0);
           uint64_t ahi[CH], alo[CH], bhi[CH], blo[CH];
@@ -827,7 +834,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           PROF_T(f1);
           PROF_ADD(1, f1 - f0);
           tc_fence_after();
-          mma_chunk<true, F16, Cfg::KSUB, CH>(tmem_base + b * (uint32_t)P_BN, ahi, alo, bhi, blo, kIdescPair,
+          mma_chunk<true, F16, Cfg::KSUB, CH>(tmem_base + b * (uint32_t)PBN, ahi, alo, bhi, blo, kIdescPair,
                                               with_lolo);
 #pragma unroll
           for (int j = 0; j < CH; ++j) tc_commit_pair(&empty[ss[j]]);   // frees the slots in both CTAs
@@ -850,18 +857,18 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       int m0, n0;
       coords(t, m0, n0);
       const int row = m0 + (int)rank * P_BM + g * 32 + lane;
-      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (P_BN / 2));
+      const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (PBN / 2));
       float acc[NC * 32];
 #pragma unroll
       for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
 #pragma unroll 1
       for (int kb = 0; kb < num_kb; kb += CH, ++q) {
-        const uint32_t b = q & 1;
+        const uint32_t b = q % NBUF;
         PROF_T(c0);
-        mbar_wait(&tfull[b], (q >> 1) & 1);
+        mbar_wait(&tfull[b], (q / NBUF) & 1);
         tc_fence_after();
         PROF_T(c1);
-        drain_add<NC>(lane_base + b * (uint32_t)P_BN, acc);
+        drain_add<NC>(lane_base + b * (uint32_t)PBN, acc);
         tc_fence_before();
         __syncwarp();
         PROF_T(c2);
@@ -877,7 +884,7 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       const int er = (F16 && row < M) ? pow2_exp(__ldg(inv_s + row)) : 0;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        const int col = n0 + h * (P_BN / 2) + c * 32;
+        const int col = n0 + h * (PBN / 2) + c * 32;
         float* v = acc + c * 32;
         if (F16) unscale_chunk(v, er, col < N - lane ? __ldg(inv_t + col + lane) : 1.f);
         if (TMA_C) {
@@ -915,6 +922,30 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       }
       PROF_T(d2);
       PROF_ADD(6, d2 - d1);
+      if (PBN != P_BN && fix.A != nullptr) {
+        // range-guard fix-up of this thread's outputs (the narrow small-problem pairs; see k7_tf32x3):
+        // after this warp's C stores have completed (TMA bulk stores are async)
+        if (TMA_C) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          __syncwarp();
+        }
+        const bool frow = row < M && __ldg(fix.flag_a + row) != 0u;
+#pragma unroll 1
+        for (int c = 0; c < NC; ++c) {
+          const int col0 = n0 + h * (PBN / 2) + c * 32;
+          const unsigned int fcol =
+              __ballot_sync(0xffffffffu, col0 + lane < N && __ldg(fix.flag_b + col0 + lane) != 0u);
+          if (row >= M || (!frow && fcol == 0u)) continue;
+          for (int j = 0; j < 32 && col0 + j < N; ++j) {
+            if (!frow && !((fcol >> j) & 1u)) continue;
+            const float* a = fix.A + (size_t)row * fix.lda;
+            const float* bb = fix.B + col0 + j;
+            float sacc = 0.f;
+            for (int k = 0; k < K; ++k) sacc = fmaf(__ldg(a + k), __ldg(bb + (size_t)k * fix.ldb), sacc);
+            C[(size_t)row * ldc + col0 + j] = sacc;
+          }
+        }
+      }
     }
   }
 #ifdef ELV_K7_PROF
@@ -1686,16 +1717,16 @@ static bool c_store_tma() {
 // K = 8192 for 8 fp16 / 4 tf32 m-tiles, half the 126 MB L2
 template <bool F16> static int pair_group() { return (!F16 && l2_hints()) ? 4 : 8; }
 
-template <int BKT, bool F16 = false>
+template <int BKT, bool F16 = false, int PBN = P_BN>
 static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C, int M,
                        int N, int K, int Kp, int ldc, int dev, cudaStream_t st, const float* inv_s = nullptr,
-                       const float* inv_t = nullptr) {
-  using Cfg = PairCfg<BKT, F16>;
+                       const float* inv_t = nullptr, FixArgs* fix = nullptr) {
+  using Cfg = PairCfg<BKT, F16, PBN>;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   int rc = make_map(&ma_hi, a_hi, M, Kp, P_BM, BKT, F16);
   if (!rc) rc = make_map(&ma_lo, a_lo, M, Kp, P_BM, BKT, F16);
-  if (!rc) rc = make_map(&mb_hi, b_hi, N, Kp, P_BN / 2, BKT, F16);
-  if (!rc) rc = make_map(&mb_lo, b_lo, N, Kp, P_BN / 2, BKT, F16);
+  if (!rc) rc = make_map(&mb_hi, b_hi, N, Kp, PBN / 2, BKT, F16);
+  if (!rc) rc = make_map(&mb_lo, b_lo, N, Kp, PBN / 2, BKT, F16);
   if (rc) return rc;
   // C through TMA bulk stores when it can be described by a tensor map
   // (16 B-aligned base and pitch); otherwise the register-store epilogue
@@ -1710,21 +1741,23 @@ static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, con
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
-  auto kern = tma_c ? k7_tf32x3_pair<BKT, F16, true> : k7_tf32x3_pair<BKT, F16, false>;
+  auto kern = tma_c ? k7_tf32x3_pair<BKT, F16, true, PBN> : k7_tf32x3_pair<BKT, F16, false, PBN>;
   static int attr_dev[2] = {-1, -1};
   if (attr_dev[tma_c] != dev) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3 pair smem attribute: %s", cudaGetErrorString(e));
     attr_dev[tma_c] = dev;
   }
-  const int tiles = ((M + 255) / 256) * ((N + P_BN - 1) / P_BN);
+  const int tiles = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
   int clusters = num_sms() / 2;
   if (clusters > tiles) clusters = tiles;
   unsigned int* ctr = tiles > clusters ? wave_counter(dev, st) : nullptr;   // one wave: nothing to sync
   cudaError_t e = launch_pdl(kern, dim3(2 * clusters), dim3(P_NUM_THREADS),
                              (size_t)Cfg::SMEM_BYTES, st, ma_hi, ma_lo, mb_hi, mb_lo, mc, C, M, N, ldc, Kp / BKT,
-                             F16 ? 0 : with_lolo(K), tile_group(pair_group<F16>()), ctr, inv_s, inv_t, l2_hints());
+                             F16 ? 0 : with_lolo(K), tile_group(pair_group<F16>()), ctr, inv_s, inv_t, l2_hints(),
+                             fix != nullptr ? *fix : FixArgs{}, K);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "gemm_parallel_tf32x3_pair: %s", cudaGetErrorString(e));
+  if (fix != nullptr) fix->applied = 1;
   return check_launch("gemm_parallel_tf32x3_pair");
 }
 // K7F (the split fused into the GEMM, one launch) is bitwise the planes path
@@ -1969,6 +2002,16 @@ static int one_cta_bk(int bn) {
   return bn == 256 ? 16 : 32;
 }
 
+// Small problems (fewer 256x256 pair tiles than SMs): the narrow CTA-pair
+// kernel (PBN = 128 / 64 columns per pair) instead of the 1-CTA kernel when
+// ELV_SMALL_PAIR=128 / 64 (read per call; 0 = the 1-CTA kernel)
+static int small_pair_bn(int M, int N) {
+  (void)M;
+  (void)N;
+  const int v = env_int("ELV_SMALL_PAIR", 0);
+  return (v == 64 || v == 128) ? v : 0;
+}
+
 int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int M, int N, int K, int ldc,
                        cudaStream_t st, int a_total, int r0, int b_total, int c0, FixArgs* fix) {
   const int Kp = (int)kpad(K);
@@ -1983,6 +2026,10 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   const int pm = pair_mode(M, N);
   if (pm == 16) return launch_pair<16>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
   if (pm == 32) return launch_pair<32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st);
+  const int spb = small_pair_bn(M, N);
+  if (spb == 64) return launch_pair<32, false, 64>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
+  if (spb == 128)
+    return launch_pair<32, false, 128>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
   const int bn = one_cta_bn(M, N);
   if (one_cta_bk(bn) == 32) {
     if (bn == 64) return launch_one<64, 32>(a_hi, a_lo, b_hi, b_lo, C, M, N, K, Kp, ldc, dev, st, nullptr, nullptr, fix);
@@ -2479,6 +2526,10 @@ int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   cudaGetDevice(&dev);
   if (pair_mode(M, N) != 0)
     return launch_pair<64, true>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv);
+  const int spb = small_pair_bn(M, N);
+  if (spb == 64) return launch_pair<64, true, 64>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
+  if (spb == 128)
+    return launch_pair<64, true, 128>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
   // fewer pair tiles than SMs: the 1-CTA kernel, 128 B stage rows for the
   // narrow N tiles, 64 B for N = 256 (keeps 4 stages)
   const int bn = one_cta_bn(M, N);

@@ -236,3 +236,21 @@ def test_small_problem_fixup_with_padded_operands(cuda, enc):
     C6 = interp.run_tensor(term, A.contiguous(), B.contiguous(), tf32x3=False)
     assert torch.equal(torch.nan_to_num(C[11], nan=7.0), torch.nan_to_num(C6[11], nan=7.0))
     assert torch.equal(torch.nan_to_num(C[:, 300], nan=7.0), torch.nan_to_num(C6[:, 300], nan=7.0))
+
+
+@pytest.mark.parametrize("enc", ENCODINGS)
+@pytest.mark.parametrize("pbn", ["64", "128"])
+def test_narrow_pair_kernel_bitwise(cuda, enc, pbn, monkeypatch):
+    """The narrow CTA-pair kernel for small problems (ELV_SMALL_PAIR, read per
+    call; measured slower, so opt-in) gives the bits of the 1-CTA kernel,
+    guarded rows / columns included (its own in-kernel fix-up)."""
+    M, N, K = 1000, 1031, 777
+    A, B = make(M, N, K, "uniform", cuda, seed=13)
+    A[2, 3] = 2.0 ** -110
+    B[4, 1030] = -(2.0 ** -110)
+    term = schedules.apply_padded("parallel", M, N, K).term
+    ref = _tc(term, A, B, enc).clone()
+    monkeypatch.setenv("ELV_SMALL_PAIR", pbn)
+    C = _tc(term, A, B, enc)
+    torch.cuda.synchronize()
+    assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
