@@ -674,10 +674,26 @@ def ladder_cases(dev, reps_small=20, reps_large=5, with_odd=True):
             tot.append(e0.elapsed_time(e2)); comp.append(e1.elapsed_time(e2))
         ok, ratio = _parity_rows(A, B, C, K, [0, 1, M // 3, M // 2, M - 1])
         ms = statistics.median(tot)
+        # the same call replayed as one CUDA graph (launch-bound small problems)
+        g_ms = None
+        if M * N * K <= 2 ** 33:
+            C.zero_()
+            g = call.graph()
+            gts = []
+            for _ in range(reps):
+                flush.zero_()
+                e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                e0.record(stream); g.replay(); e1.record(stream)
+                torch.cuda.synchronize()
+                gts.append(e0.elapsed_time(e1))
+            g_ms = statistics.median(gts)
+            gok, _ = _parity_rows(A, B, C, K, [0, 1, M // 3, M // 2, M - 1])
+            ok = ok and gok
         peak, bound, _ = roofline_peak(v, peaks, n_sms, None)
         ach = 2.0 * M * N * K / (statistics.median(comp) * 1e-3) / 1e12
         out.append({"config": cfg, "variant": v, "kernel_variant_id": p.variant, "M": M, "N": N, "K": K,
                     "gflops": 2.0 * M * N * K / (ms * 1e-3) / 1e9, "ms": ms,
+                    "gflops_graph": 2.0 * M * N * K / (g_ms * 1e-3) / 1e9 if g_ms else None, "ms_graph": g_ms,
                     "kernel_ms": statistics.median(comp), "kernel_tflops": ach, "roofline_bound": bound,
                     "peak_tflops": peak, "frac": ach / peak, "parity_ok": ok, "parity_worst": ratio,
                     "reps": reps})

@@ -169,6 +169,29 @@ class GemmCall:
         self.compute()
         return self.C
 
+    def graph(self) -> "torch.cuda.CUDAGraph":
+        """The call's launches (prepare + compute: memsets, kernels, PDL
+        edges) captured once into a CUDA graph on a side stream; `replay()`
+        re-runs them as one graph launch on the current stream -- the host
+        launch overhead of a small call (several ctypes calls and launches)
+        is paid once.  Same kernels, same arguments, same bits."""
+        if getattr(self, "_graph", None) is None:
+            self()                                      # first launches outside capture (attributes, modules)
+            torch.cuda.synchronize(self.A.device)
+            cap = torch.cuda.Stream(self.A.device)
+            ws = (self.ws.data_ptr() if self.ws is not None else None, self.ws_bytes, cap.cuda_stream)
+            p, A, B, C = self.p, self.A, self.B, self.C
+            prep = (p.variant, A.data_ptr(), B.data_ptr(), p.M, p.N, p.K, A.stride(0), B.stride(0), *ws)
+            comp = (p.variant, A.data_ptr(), B.data_ptr(), C.data_ptr(), p.M, p.N, p.K, A.stride(0),
+                    B.stride(0), C.stride(0), *ws)
+            g = torch.cuda.CUDAGraph()
+            cap.wait_stream(torch.cuda.current_stream(self.A.device))
+            with torch.cuda.graph(g, stream=cap):
+                _lib.check(self._prep_fn(*prep), "elv_gemm_prepare (graph capture)")
+                _lib.check(self._comp_fn(*comp), "elv_gemm_compute (graph capture)")
+            self._graph = g
+        return self._graph
+
 
 def run_tensor(e, A: torch.Tensor, B: torch.Tensor, out=None, stream=None,
                tf32x3: bool | None = None, tc_encoding: str | None = None) -> torch.Tensor:

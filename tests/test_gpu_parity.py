@@ -470,3 +470,21 @@ def test_k6_bulk_copy_staging_is_bitwise(cuda, tmp_path):
     subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
     Cb = np.load(tmp_path / "c.npy")
     assert np.array_equal(C.view(np.int32), Cb.view(np.int32))
+
+
+@pytest.mark.parametrize("variant", ["parallel", "parallel_tf32x3", "parallel_fp16x3", "cacheBlocks"])
+def test_gemmcall_graph_replay_bitwise(cuda, variant):
+    """GemmCall.graph(): the call's launches (memsets, PDL-chained kernels)
+    captured once and replayed give the bits of direct calls."""
+    M, N, K = 1024, 768, 1024
+    name, tf = _sched(variant)
+    A, B = _device_inputs(M, N, K, 31, cuda)
+    p = dispatch.decode(schedules.apply(name, M, N, K).term, [(M, K), (K, N)], tf32x3=tf, tc_encoding=_enc(variant))
+    C = torch.empty((M, N), device=cuda)
+    call = interp.GemmCall(p, A, B, C)
+    ref = call().clone()
+    g = call.graph()
+    C.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
