@@ -135,3 +135,41 @@ def test_register_tile_mode_is_bitwise_the_per_scalar_code(name, tmp_path, monke
     np.testing.assert_array_equal(a, b)
     ref = np.array(S().interp.run(term, [x.tolist() for x in args]), np.float64)
     assert np.all(np.abs(b - ref) <= 64 * 4 * 2.0 ** -23)
+
+
+def test_smem_tile_mode_source_and_host_guard(monkeypatch):
+    """A contraction of at least 256 x 256 outputs compiles in the shared-memory
+    tile mode (GPU-only: staged chunks, __syncthreads, f32x2-paired fmaf); the
+    host emulation refuses it, and with the mode off the same term falls back
+    to the register-tile mode (what the host tests compile)."""
+    from paper_2002_02268_b200._ref import S
+    s = S()
+    st, nf, tv, rules = s.strategy, s.normal_forms, s.traversals, s.rules
+    strat = st.seq(nf.dfnf_seq(tv.top_down(schedules.tile(16, 16)),
+                               tv.top_down(st.seq(tv.is_reduce, rules.make_split(2)))), nf.LOWER_TO_C)
+    term = st.run_strategy(strat, schedules.mm(256, 256, 64))[0].term
+    c = codegen.compile_term(term)
+    assert c.mode.startswith("smem-tile") and c.grid == (4, 4) and c.block == 128
+    assert "__syncthreads" in c.source and "fma.rn.f32x2" in c.source and "elv_fma2(" in c.source
+    with pytest.raises(codegen.CodegenError):
+        codegen.cpu_source(c)
+    monkeypatch.setattr(codegen, "SMEM_TILE", False)
+    c2 = codegen.compile_term(term)
+    assert c2.mode.startswith("register-tile") and not c2.grid
+    # outputs below the threshold, or not multiples of 64, never use it
+    monkeypatch.setattr(codegen, "SMEM_TILE", True)
+    small = st.run_strategy(strat, schedules.mm(64, 64, 64))[0].term
+    assert not codegen.compile_term(small).mode.startswith("smem-tile")
+
+
+def test_gemmcall_launch_counts():
+    """GemmCall.count_launches: the library's launches per call (the bench's
+    gpu_launches claim), by variant and problem size."""
+    from types import SimpleNamespace as P
+    from paper_2002_02268_b200.interp import GemmCall
+    assert GemmCall.count_launches(P(variant=0, M=64, N=64, K=64)) == 1
+    assert GemmCall.count_launches(P(variant=6, M=4096, N=4096, K=4096)) == 2          # packs + GEMM
+    assert GemmCall.count_launches(P(variant=7, M=1024, N=1024, K=1024)) == 2          # split + GEMM (fix-up inside)
+    assert GemmCall.count_launches(P(variant=7, M=32768, N=32768, K=8192)) == 3        # + separate fix-up
+    assert GemmCall.count_launches(P(variant=8, M=32768, N=32768, K=8192)) == 4        # 2 prepare + GEMM + fix-up
+    assert GemmCall.count_launches(P(variant=8, M=1024, N=1024, K=256)) == 2           # K < 512 runs as 7
