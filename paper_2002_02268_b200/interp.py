@@ -118,10 +118,11 @@ class GemmCall:
     phases (elv_gemm_prepare: operand layout transform; elv_gemm_compute:
     the GEMM kernel) so callers can time or overlap them separately.
     Launches per call: prepare 0 (variants 0-3), 1 (4, 5: packB; 6: packB, or
-    packA+packB fused; 7: fused hi/lo split of A and B); compute 1."""
+    packA+packB fused; 7: fused hi/lo split of A and B), 2 (8: [A rows | B
+    maxima], B split); compute 1, or 2 for the tensor-core variants when the
+    range-guard fix-up runs as its own launch (see count_launches)."""
 
     PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 2}   # 8: [A rows | B max], B split
-    COMPUTE_LAUNCHES = {7: 2, 8: 2}     # tensor-core GEMM + range-guard fix-up; others: 1
 
     @classmethod
     def count_launches(cls, p) -> int:
@@ -153,16 +154,24 @@ class GemmCall:
         self._comp_args = (p.variant, A.data_ptr(), B.data_ptr(), C.data_ptr(), p.M, p.N, p.K, A.stride(0),
                            B.stride(0), C.stride(0), *ws)
         self._prep_fn, self._comp_fn = self.lib.elv_gemm_prepare, self.lib.elv_gemm_compute
+        self._dev = A.device.index
+
+    def _on_device(self, fn, args, what):
+        # the C ABI launches into the current device's context: switch only
+        # when the operands live elsewhere (a device guard costs ~2 us per use)
+        if torch.cuda.current_device() != self._dev:
+            with torch.cuda.device(self._dev):
+                rc = fn(*args)
+        else:
+            rc = fn(*args)
+        if rc:
+            _lib.check(rc, what)
 
     def prepare(self):
-        rc = self._prep_fn(*self._prep_args)
-        if rc:
-            _lib.check(rc, "elv_gemm_prepare")
+        self._on_device(self._prep_fn, self._prep_args, "elv_gemm_prepare")
 
     def compute(self):
-        rc = self._comp_fn(*self._comp_args)
-        if rc:
-            _lib.check(rc, "elv_gemm_compute")
+        self._on_device(self._comp_fn, self._comp_args, "elv_gemm_compute")
 
     def __call__(self):
         self.prepare()
@@ -186,7 +195,7 @@ class GemmCall:
                     B.stride(0), C.stride(0), *ws)
             g = torch.cuda.CUDAGraph()
             cap.wait_stream(torch.cuda.current_stream(self.A.device))
-            with torch.cuda.graph(g, stream=cap):
+            with torch.cuda.device(self._dev), torch.cuda.graph(g, stream=cap):
                 _lib.check(self._prep_fn(*prep), "elv_gemm_prepare (graph capture)")
                 _lib.check(self._comp_fn(*comp), "elv_gemm_compute (graph capture)")
             self._graph = g
