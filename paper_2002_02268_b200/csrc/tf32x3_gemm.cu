@@ -1635,11 +1635,31 @@ static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
+static int one_cta_bn(int M, int N);
+
+// Mainloop cycles per accumulation chunk (64 k fp16 / 32 k tf32: 12 MMAs of
+// k16 / k8) of one CTA whose MMAs are n_mma wide and whose SMEM holds
+// n_smem columns of B: max(tensor pipe, 12 x 128 n / 256 = 6 n; shared
+// memory, the TMA writes of the hi/lo planes plus the three products'
+// operand reads, 10 B per row or column and k (fp16; tf32 20 B over half
+// the k) = 640 B per chunk at 128 B/clk = 5 (128 + n_smem)).  The MMA-rate
+// probe (scripts/probes/mma_rate.cu, profiles/r2/small/mma_rate_probe.jsonl)
+// measured SMEM-operand MMAs at 48 / 64 / 128 cycles for N = 64 / 128 / 256.
+static double chunk_cycles(int n_mma, int n_smem) {
+  const double mma = 6.0 * n_mma, smem = 5.0 * (128 + n_smem);
+  return mma > smem ? mma : smem;
+}
+
 // Kernel choice.  Default: the cta_group::2 kernel with BK=32 (128B swizzle)
 // when there are at least as many 256x256 pair tiles as SMs (measured at
 // 32768^2 x 8192 under the power cap: 251-256 TF vs 244-245 TF for the 1-CTA
-// kernel, scripts/gpu_pairws.sh), else the 1-CTA kernel (twice the tiles for
-// small problems).  ELV_TF32X3_PAIR=0 / 16 / 32 forces a choice.
+// kernel, scripts/gpu_pairws.sh) or when its modelled mainloop is shorter
+// than the 1-CTA kernel's: a pair's CTA holds half of B, so it streams
+// 5 (128 + 128) SMEM cycles per 1536 MMA cycles, where a 1-CTA 128 x 256 tile
+// needs 1920 (mid-size problems, e.g. 2048^3 fp16 55.3 -> 48.2 us, 3072^3
+// 151.6 -> 122.9 us, bitwise the same; profiles/r2/small/mid_pair.jsonl);
+// else the 1-CTA kernel (more, narrower tiles for small problems: 1024^3,
+// 1536^3).  ELV_TF32X3_PAIR=0 / 16 / 32 forces a choice.
 static int pair_mode(int M, int N) {
   static int forced = -2;
   if (forced == -2) {
@@ -1648,8 +1668,14 @@ static int pair_mode(int M, int N) {
     if (forced != -1 && forced != 0 && forced != 16 && forced != 32) forced = -1;
   }
   if (forced >= 0) return forced;
+  const long long sms = num_sms();
   const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
-  return pair_tiles >= num_sms() ? 32 : 0;
+  if (pair_tiles >= sms) return 32;
+  const double pair = (double)((pair_tiles + sms / 2 - 1) / (sms / 2)) * chunk_cycles(256, 128);
+  const int bn = one_cta_bn(M, N);
+  const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  const double one = (double)((tiles + sms - 1) / sms) * chunk_cycles(bn, bn);
+  return pair < one ? 32 : 0;
 }
 // Wave counter (library-internal scratch, 4 bytes) zeroed on the launch
 // stream before every launch; ELV_WAVE_SYNC=0 disables the sync.  One counter

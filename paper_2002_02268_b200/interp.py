@@ -113,6 +113,36 @@ def gemm(p: dispatch.KernelPlan, A: torch.Tensor, B: torch.Tensor,
     return out
 
 
+def _one_cta_bn(M: int, N: int, sms: int) -> int:
+    """N tile of the 1-CTA tensor-core kernel (csrc/tf32x3_gemm.cu one_cta_bn)."""
+    best, best_cost = 256, 1e30
+    for bn, eff in ((256, 1.0), (128, 0.95), (64, 0.67)):
+        tiles = -(-M // 128) * -(-N // bn)
+        cost = -(-tiles // sms) * bn / eff
+        if cost < best_cost * 0.999:
+            best, best_cost = bn, cost
+    return best
+
+
+def _chunk_cycles(n_mma: int, n_smem: int) -> float:
+    return max(6.0 * n_mma, 5.0 * (128 + n_smem))
+
+
+def pair_kernel(M: int, N: int, sms: int = 148) -> bool:
+    """Whether the library runs the cta_group::2 kernel for an M x N
+    tensor-core GEMM (csrc/tf32x3_gemm.cu pair_mode, defaults): at least one
+    256x256 pair tile per SM, or a shorter modelled mainloop than the 1-CTA
+    kernel's -- per accumulation chunk max(tensor pipe 6 n, shared memory
+    5 (128 + B columns held)) cycles, times the waves."""
+    pair_tiles = -(-M // 256) * -(-N // 256)
+    if pair_tiles >= sms:
+        return True
+    pair = -(-pair_tiles // (sms // 2)) * _chunk_cycles(256, 128)
+    bn = _one_cta_bn(M, N, sms)
+    one = -(-(-(-M // 128) * -(-N // bn)) // sms) * _chunk_cycles(bn, bn)
+    return pair < one
+
+
 class GemmCall:
     """A bound kernel call with its workspace, split into the two C-ABI
     phases (elv_gemm_prepare: operand layout transform; elv_gemm_compute:
@@ -132,8 +162,7 @@ class GemmCall:
         K < 512 runs variant 8 as 7."""
         if p.variant not in (7, 8):
             return cls.PREPARE_LAUNCHES[p.variant] + 1
-        pair = ((p.M + 255) // 256) * ((p.N + 255) // 256) >= 148
-        compute = 2 if pair else 1
+        compute = 2 if pair_kernel(p.M, p.N) else 1
         if p.variant == 8 and p.K >= 512:
             return 2 + compute
         return 1 + compute

@@ -173,3 +173,16 @@ def test_gemmcall_launch_counts():
     assert GemmCall.count_launches(P(variant=7, M=32768, N=32768, K=8192)) == 3        # + separate fix-up
     assert GemmCall.count_launches(P(variant=8, M=32768, N=32768, K=8192)) == 4        # 2 prepare + GEMM + fix-up
     assert GemmCall.count_launches(P(variant=8, M=1024, N=1024, K=256)) == 2           # K < 512 runs as 7
+    assert GemmCall.count_launches(P(variant=8, M=2048, N=2048, K=2048)) == 4          # mid-size: pair kernel
+
+
+def test_pair_kernel_choice_model():
+    """interp.pair_kernel (the library's pair / 1-CTA choice): the 1-CTA
+    kernel for the paper's 1024^3 and for 1536^3 (measured faster there), the
+    cta_group::2 kernel from 2048^3 up (profiles/r2/small/mid_pair.jsonl) and
+    whenever there are at least as many pair tiles as SMs."""
+    from paper_2002_02268_b200.interp import pair_kernel
+    assert not pair_kernel(1024, 1024) and not pair_kernel(1536, 1536) and not pair_kernel(1000, 1031)
+    assert not pair_kernel(4096, 256)
+    assert pair_kernel(2048, 2048) and pair_kernel(3072, 3072) and pair_kernel(2560, 2560)
+    assert pair_kernel(32768, 32768) and pair_kernel(4096 * 4, 2048)

@@ -73,6 +73,7 @@ SHAPES = [
     (3584, 3072, 200),       # K < 512: the lo.lo correction is on
     (8192, 8192, 2048),      # 1024 pair tiles: multi-wave, wave-synchronised producers
     (2304, 4352, 8),         # K shorter than one k-block
+    (2048, 2048, 1024),      # 64 pair tiles: mid-size, the pair kernel by the SMEM/MMA model
 ]
 
 

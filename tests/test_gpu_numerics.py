@@ -14,6 +14,8 @@ inside the fp32 bound for every input class, not only U(-1,1):
     parallel schedule's SIMT kernel, K6).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -254,3 +256,52 @@ def test_narrow_pair_kernel_bitwise(cuda, enc, pbn, monkeypatch):
     C = _tc(term, A, B, enc)
     torch.cuda.synchronize()
     assert torch.equal(C.view(torch.int32), ref.view(torch.int32))
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repo!r})
+from paper_2002_02268_b200 import interp, schedules, synth
+M, N, K = {M}, {N}, {K}
+A = torch.empty((M, K), device="cuda"); B = torch.empty((K, N), device="cuda")
+synth.fill_device(A, 17, 0); synth.fill_device(B, 17, 1)
+A[5, 7] = 2.0 ** -110; B[9, N - 1] = -(2.0 ** -110)
+t = schedules.apply_padded("parallel", M, N, K).term
+for enc in ("tf32", "fp16"):
+    np.save({out!r} + enc + ".npy", interp.run_tensor(t, A, B, tf32x3=True, tc_encoding=enc).cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048, 2048), (2000, 1800, 777), (1100, 4100, 600)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_mid_size_pair_choice_bitwise(cuda, tmp_path, shape):
+    """Mid-size problems (fewer 256x256 pair tiles than SMs) run the
+    cta_group::2 kernel when its modelled mainloop is shorter than the 1-CTA
+    kernel's (interp.pair_kernel mirrors the library's choice): the bits are
+    the 1-CTA kernel's (ELV_TF32X3_PAIR=0, read once per process, so a
+    subprocess each), ragged tiles and range-guarded rows / columns
+    included, and sampled rows are within the oracle bound."""
+    import subprocess
+    import sys
+    M, N, K = shape
+    assert interp.pair_kernel(M, N)
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("default", "0"):
+        out = str(tmp_path / f"c_{mode}_")
+        env = dict(os.environ)
+        env.pop("ELV_TF32X3_PAIR", None)
+        if mode == "0":
+            env["ELV_TF32X3_PAIR"] = "0"
+        subprocess.run([sys.executable, "-c", _PAIR_SCRIPT.format(repo=repo, M=M, N=N, K=K, out=out)],
+                       env=env, check=True, timeout=300)
+        outs[mode] = {enc: np.load(out + enc + ".npy") for enc in ENCODINGS}
+    A = torch.empty((M, K), device=cuda); B = torch.empty((K, N), device=cuda)
+    synth.fill_device(A, 17, 0); synth.fill_device(B, 17, 1)
+    A[5, 7] = 2.0 ** -110
+    B[9, N - 1] = -(2.0 ** -110)
+    rows = [0, 5, 9, 255, 256, M // 2, M - 1]
+    for enc in ENCODINGS:
+        assert np.array_equal(outs["default"][enc].view(np.int32), outs["0"][enc].view(np.int32)), enc
+        C = torch.from_numpy(outs["default"][enc]).to(cuda)
+        assert _worst(C, A, B, K, rows=rows) <= 1.0, enc
