@@ -460,6 +460,20 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
       sched.coords(t, m0, n0);
       const int row = m0 + g * 32 + lane;
       const uint32_t lane_base = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * (BN / 2));
+      // the tile's unscaling exponents / factors and range-guard flags are
+      // final (griddep_wait above): load them before the chunk loop, so their
+      // latency hides behind the MMAs instead of the tile's tail (1024^3 fp16:
+      // the store phase was ~2.8K cycles against ~0.6K for tf32)
+      const int er = (F16 && row < M) ? pow2_exp(__ldg(inv_s + row)) : 0;
+      const bool frow = fix.A != nullptr && row < M && __ldg(fix.flag_a + row) != 0u;
+      float it[NC];
+      unsigned int fb[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int col = n0 + h * (BN / 2) + c * 32;
+        it[c] = (F16 && col < N - lane) ? __ldg(inv_t + col + lane) : 1.f;
+        fb[c] = (fix.A != nullptr && col + lane < N) ? __ldg(fix.flag_b + col + lane) : 0u;
+      }
       float acc[NC * 32];
 #pragma unroll
       for (int i = 0; i < NC * 32; ++i) acc[i] = 0.f;
@@ -479,12 +493,11 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
       }
       PROF_T(d1);
       float* crow = C + (size_t)row * ldc;
-      const int er = (F16 && row < M) ? pow2_exp(__ldg(inv_s + row)) : 0;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int col = n0 + h * (BN / 2) + c * 32;
         float* v = acc + c * 32;
-        if (F16) unscale_chunk(v, er, col < N - lane ? __ldg(inv_t + col + lane) : 1.f);
+        if (F16) unscale_chunk(v, er, it[c]);
         if (row < M && col < N) {
           if (vecC && col + 31 < N) {
 #pragma unroll
@@ -504,12 +517,15 @@ k7_tf32x3(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ C
         // k_tc_fixup -- an fmaf chain over k ascending from 0 -- after the
         // thread's own stores above (program order; flags are complete: the
         // split finished before griddepcontrol.wait returned)
-        const bool frow = row < M && __ldg(fix.flag_a + row) != 0u;
+        unsigned int fcols[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) fcols[c] = __ballot_sync(0xffffffffu, fb[c] != 0u);
 #pragma unroll 1
         for (int c = 0; c < NC; ++c) {
           const int col0 = n0 + h * (BN / 2) + c * 32;
-          const unsigned int fcol =
-              __ballot_sync(0xffffffffu, col0 + lane < N && __ldg(fix.flag_b + col0 + lane) != 0u);
+          unsigned int fcol = fcols[0];
+#pragma unroll
+          for (int i = 1; i < NC; ++i) fcol = c == i ? fcols[i] : fcol;   // register select (no local array)
           if (row >= M || (!frow && fcol == 0u)) continue;
           for (int j = 0; j < 32 && col0 + j < N; ++j) {
             if (!frow && !((fcol >> j) & 1u)) continue;
