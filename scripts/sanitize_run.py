@@ -36,6 +36,21 @@ def main():
             ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
             print(f"{v:16s} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
             assert ok
+    # mid-size, ragged: the cta_group::2 kernel by the pair / 1-CTA model (no env), guard rows included
+    M, N, K = 1100, 2100, 600
+    assert interp.pair_kernel(M, N)
+    A = synth.matrix(M, K, 6, 0)
+    B = synth.matrix(K, N, 6, 1)
+    A[1099, 5] = 2.0 ** -110
+    ref, ab = oracle.mm_f64(A, B), oracle.absprod_np(A, B)
+    for enc in ("tf32", "fp16"):
+        term = schedules.apply_padded("parallel", M, N, K).term
+        C = interp.run_tensor(term, torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), tf32x3=True,
+                              tc_encoding=enc)
+        torch.cuda.synchronize()
+        ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
+        print(f"mid-size pair {enc} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
+        assert ok
     # range guard: marked rows / columns recomputed by the fix-up (both encodings)
     M, N, K = 160, 200, 576
     A = synth.matrix(M, K, 8, 0)
