@@ -162,7 +162,9 @@ class GemmCall:
         K < 512 runs variant 8 as 7."""
         if p.variant not in (7, 8):
             return cls.PREPARE_LAUNCHES[p.variant] + 1
-        compute = 2 if pair_kernel(p.M, p.N) else 1
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count \
+            if torch.cuda.is_available() else 148
+        compute = 2 if pair_kernel(p.M, p.N, sms) else 1
         if p.variant == 8 and p.K >= 512:
             return 2 + compute
         return 1 + compute
