@@ -2044,7 +2044,7 @@ static int one_cta_bk(int bn) {
   return bn == 256 ? 16 : 32;
 }
 
-// Small problems (fewer 256x256 pair tiles than SMs): the narrow CTA-pair
+// Small problems (pair_mode 0): the narrow CTA-pair
 // kernel (PBN = 128 / 64 columns per pair) instead of the 1-CTA kernel when
 // ELV_SMALL_PAIR=128 / 64 (read per call; 0 = the 1-CTA kernel)
 static int small_pair_bn(int M, int N) {
@@ -2572,7 +2572,7 @@ int fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
   if (spb == 64) return launch_pair<64, true, 64>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
   if (spb == 128)
     return launch_pair<64, true, 128>(A.hi, A.lo, B.hi, B.lo, C, M, N, K, Kp, ldc, dev, st, A.inv, B.inv, fix);
-  // fewer pair tiles than SMs: the 1-CTA kernel, 128 B stage rows for the
+  // pair_mode 0 (small problems): the 1-CTA kernel, 128 B stage rows for the
   // narrow N tiles, 64 B for N = 256 (keeps 4 stages)
   const int bn = one_cta_bn(M, N);
   if (bn == 64)

@@ -158,7 +158,8 @@ class GemmCall:
     def count_launches(cls, p) -> int:
         """Kernel launches of one call (the library's defaults): the
         tensor-core variants fold the range-guard fix-up into the 1-CTA GEMM
-        (fewer 256x256 tiles than SMs); the 3xFP16 prepare is two launches;
+        (the small problems `pair_kernel` leaves to it); the 3xFP16 prepare
+        is two launches;
         K < 512 runs variant 8 as 7."""
         if p.variant not in (7, 8):
             return cls.PREPARE_LAUNCHES[p.variant] + 1

@@ -191,7 +191,7 @@ def test_bench_shape_checksums_adversarial(cuda, enc, kind):
 @pytest.mark.parametrize("shape", [(1024, 1024, 1024), (1000, 1031, 777), (130, 70, 516), (640, 768, 1024)],
                          ids=lambda s: "x".join(map(str, s)))
 def test_small_problem_paths_bitwise(cuda, enc, shape, monkeypatch):
-    """Small problems (fewer 256x256 tiles than SMs): the 1-CTA GEMM runs the
+    """Small problems (the 1-CTA kernel by the pair / 1-CTA model): the 1-CTA GEMM runs the
     range-guard fix-up itself and, for 3xFP16 with K <= 1024, the prepare is
     one launch (k16_prep_fused, B column slabs in shared memory).  Both give
     the bits of the separate launches (ELV_TC_FIXUP_INKERNEL=0,
