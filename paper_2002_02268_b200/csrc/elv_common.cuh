@@ -49,6 +49,35 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return launch_pdl_if(true, kern, grid, block, smem, st, std::forward<Args>(args)...);
 }
 
+// Preferred L1 / shared-memory carveout of the light-SMEM kernels that run
+// next to the big-SMEM GEMMs (prepare kernels before them, the range-guard
+// fix-up PDL-scheduled during them): asking for the maximum shared carveout
+// keeps every SM in the GEMM's configuration, so a PDL-launched GEMM (or
+// fix-up) CTA can become resident beside a finishing neighbour instead of
+// waiting for the SM to drain and reconfigure.  Measured slower (the
+// prepare kernels lose their L1: 1024^3 3xFP16 call 27.6 -> 29.7 us, bench
+// prepass 1.25 -> 1.35 ms; profiles/r2/experiments/carveout_ab.txt), so
+// off by default; ELV_PREP_CARVEOUT=1 (read once per process) turns it on.
+inline bool prep_carveout_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ELV_PREP_CARVEOUT");
+    v = e ? (atoi(e) != 0) : 0;
+  }
+  return v != 0;
+}
+#define ELV_PREFER_MAX_SMEM(fn)                                                                          \
+  do {                                                                                                   \
+    static int elv_carveout_dev_ = -1;                                                                   \
+    int elv_cur_dev_ = 0;                                                                                \
+    cudaGetDevice(&elv_cur_dev_);                                                                        \
+    if (elv_carveout_dev_ != elv_cur_dev_ && prep_carveout_enabled()) {                                 \
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,                           \
+                           (int)cudaSharedmemCarveoutMaxShared);                                         \
+      elv_carveout_dev_ = elv_cur_dev_;                                                                  \
+    }                                                                                                    \
+  } while (0)
+
 constexpr int kPanel = 32;          // packB block (rules.py:516 default 32)
 constexpr int kPackAlign = 256;     // packed column count padded to 8 panels (widest SIMT tile)
 

@@ -1373,6 +1373,7 @@ int launch_pack_b(const float* B, float* packedB, int K, int N, int ldb, cudaStr
   const long long cap = (long long)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  ELV_PREFER_MAX_SMEM(k_pack_b);
   k_pack_b<<<(unsigned)blocks, 256, 0, st>>>(B, packedB, K, N, ldb, panels, vecB);
   return check_launch("pack_b");
 }
@@ -1433,6 +1434,7 @@ int launch_pack_ab(const float* B, float* packedB, int K, int N, int ldb, const 
   const int gxa = (K + 31) / 32, gya = (M + 127) / 128 * 4;
   const long long blocks = gb + (long long)gxa * gya;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "pack_ab: problem too large for one launch");
+  ELV_PREFER_MAX_SMEM(k_pack_ab);
   k_pack_ab<<<(unsigned)blocks, 256, 0, st>>>(B, packedB, K, N, ldb, panels, vecB, (int)gb, A, packedA, M, lda, gxa);
   return check_launch("pack_ab");
 }

@@ -1932,6 +1932,7 @@ int tc_fixup(const float* A, int lda, const float* B, int ldb, bool b_packed, fl
   const long long blocks = (long long)(M + FIX_SEG - 1) / FIX_SEG + (N + FIX_SEG - 1) / FIX_SEG;
   if (blocks <= 0) return ELV_OK;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tc_fixup: problem too large");
+  ELV_PREFER_MAX_SMEM(k_tc_fixup);
   const cudaError_t e = launch_pdl(k_tc_fixup, dim3((unsigned)blocks), dim3(FIX_T), 0, st, A, lda, B, ldb,
                                    (int)b_packed, C, ldc, M, N, K, flag_a, flag_b);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "tc_fixup: %s", cudaGetErrorString(e));
@@ -2103,6 +2104,7 @@ int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
   unsigned int* flags = ws_tail_flags(ws, M, N, K);
   if (cudaMemsetAsync(flags, 0, (size_t)(M + N) * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3: memset");
+  ELV_PREFER_MAX_SMEM(k_split_ab);
   k_split_ab<<<(unsigned)blocks, 256, 0, st>>>(A, ahi, alo, M, lda, vec, gxa, gya, B, bhi, blo, N, ldb, gxb, K, Kp,
                                                flags, flags + M);
   return check_launch("tf32x3_split_ab");
@@ -2645,6 +2647,8 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   const long long ga = warp_rows ? (M + 7) / 8 : M;
   const long long blocks = ga + (long long)gxb * gyb;
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
+  ELV_PREFER_MAX_SMEM(k16_prep_ab);
+  ELV_PREFER_MAX_SMEM(k16_split_transpose_b<false>);
   k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax,
                                                 warp_rows, slab, PA.flag, PB.flag);
   if (cudaPeekAtLastError() != cudaSuccess) return check_launch("fp16x3_prepare");
