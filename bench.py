@@ -639,8 +639,9 @@ def ladder_cases(dev, reps_small=20, reps_large=5, with_odd=True):
     """configs[1] (every strategy at 1024^3), configs[2] (8192^3: the packed
     strategies and both tensor-core encodings) and configs[4] (odd shapes,
     every strategy) as records: GFLOP/s per call (prepass + kernel back to
-    back, L2 flushed before every rep), the kernel's TFLOP/s (timed in
-    separate reps) and roofline fraction,
+    back, L2 flushed before every rep; also warm-L2 back to back and
+    replayed as a CUDA graph), the kernel's TFLOP/s (timed in separate reps)
+    and roofline fraction,
     and a parity bit on sampled rows."""
     import torch
     from paper_2002_02268_b200 import dispatch, interp, schedules, synth
@@ -684,6 +685,16 @@ def ladder_cases(dev, reps_small=20, reps_large=5, with_odd=True):
             comp.append(e1.elapsed_time(e2))
         ok, ratio = _parity_rows(A, B, C, K, [0, 1, M // 3, M // 2, M - 1])
         ms = statistics.median(tot)
+        # warm L2 (1024^3 fits in L2): the call back to back, no flush
+        w_ms = None
+        if M * N * K <= 2 ** 31:
+            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            e0.record(stream)
+            for _ in range(reps):
+                call()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            w_ms = e0.elapsed_time(e1) / reps
         # the same call replayed as one CUDA graph (launch-bound small problems)
         g_ms = None
         if M * N * K <= 2 ** 33:
@@ -704,6 +715,7 @@ def ladder_cases(dev, reps_small=20, reps_large=5, with_odd=True):
         out.append({"config": cfg, "variant": v, "kernel_variant_id": p.variant, "M": M, "N": N, "K": K,
                     "gflops": 2.0 * M * N * K / (ms * 1e-3) / 1e9, "ms": ms,
                     "gflops_graph": 2.0 * M * N * K / (g_ms * 1e-3) / 1e9 if g_ms else None, "ms_graph": g_ms,
+                    "gflops_warm_l2": 2.0 * M * N * K / (w_ms * 1e-3) / 1e9 if w_ms else None, "ms_warm_l2": w_ms,
                     "kernel_ms": statistics.median(comp), "kernel_tflops": ach, "roofline_bound": bound,
                     "peak_tflops": peak, "frac": ach / peak, "parity_ok": ok, "parity_worst": ratio,
                     "reps": reps})
