@@ -70,8 +70,8 @@ inline bool prep_carveout_enabled() {
   do {                                                                                                   \
     static int elv_carveout_dev_ = -1;                                                                   \
     int elv_cur_dev_ = 0;                                                                                \
-    cudaGetDevice(&elv_cur_dev_);                                                                        \
-    if (elv_carveout_dev_ != elv_cur_dev_ && prep_carveout_enabled()) {                                 \
+    if (prep_carveout_enabled() && cudaGetDevice(&elv_cur_dev_) == cudaSuccess &&                        \
+        elv_carveout_dev_ != elv_cur_dev_) {                                                             \
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,                           \
                            (int)cudaSharedmemCarveoutMaxShared);                                         \
       elv_carveout_dev_ = elv_cur_dev_;                                                                  \
