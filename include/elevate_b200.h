@@ -120,7 +120,9 @@ int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
  * tcgen05 pair kernel reads raw fp32 A (M x K, lda) and B (K x N row-major,
  * ldb) by TMA and splits them in shared memory; bitwise the result of
  * split_a ; split_b ; gemm_planes.  Applicable (elv_tf32x3_fused_ok) when the
- * problem has >= 148 256x256 tiles and A, B, lda, ldb are 16-byte aligned;
+ * library runs the CTA-pair kernel at this shape (>= 148 256x256 tiles, or a
+ * mid-size problem where its modelled mainloop beats the 1-CTA kernel's) and
+ * A, B, lda, ldb are 16-byte aligned;
  * elv_gemm / elv_gemm_compute (variant 7) use it then only with
  * ELV_TF32X3_FUSED=1 (measured slower than the planes path).  `flags` is caller
  * scratch of (M + N) u32: zeroed and filled with the range-guard marks, and

@@ -359,7 +359,7 @@ int elv_tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, floa
   if (rc) return rc;
   if (bad_ptr(flags)) return set_error(ELV_EINVAL, "tf32x3_gemm_fused: null flags");
   if (!tf32x3_fused_ok(A, lda, B, ldb, M, N))
-    return set_error(ELV_EINVAL, "tf32x3_gemm_fused: not applicable (needs >= 148 pair tiles, 16 B alignment)");
+    return set_error(ELV_EINVAL, "tf32x3_gemm_fused: not applicable (needs the pair kernel -- the pair / 1-CTA model -- and 16 B alignment)");
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(flags, 0, (size_t)(M + N) * 4, st) != cudaSuccess)
     return set_error(ELV_ECUDA, "tf32x3_gemm_fused: memset");
@@ -374,7 +374,7 @@ int elv_tf32x3_gemm_fused_a(const float* A, int lda, const void* b_planes, const
   if (rc) return rc;
   if (bad_ptr(flags_a) || bad_ptr(b_planes)) return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: null pointer");
   if (!tf32x3_fused_a_ok(A, lda, M, N))
-    return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: not applicable (needs >= 148 pair tiles, 16 B aligned A)");
+    return set_error(ELV_EINVAL, "tf32x3_gemm_fused_a: not applicable (needs the pair kernel -- the pair / 1-CTA model -- and a 16 B aligned A)");
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(flags_a, 0, (size_t)M * 4, st) != cudaSuccess)
     return set_error(ELV_ECUDA, "tf32x3_gemm_fused_a: memset");
