@@ -272,7 +272,7 @@ for enc in ("tf32", "fp16"):
 """
 
 
-@pytest.mark.parametrize("shape", [(2048, 2048, 2048), (2000, 1800, 777), (1100, 4100, 600)],
+@pytest.mark.parametrize("shape", [(2048, 2048, 2048), (2000, 1800, 777), (1100, 4100, 600), (2048, 2000, 300)],
                          ids=lambda s: "x".join(map(str, s)))
 def test_mid_size_pair_choice_bitwise(cuda, tmp_path, shape):
     """Mid-size problems (fewer 256x256 pair tiles than SMs) run the
