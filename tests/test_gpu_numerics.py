@@ -27,7 +27,8 @@ pytestmark = pytest.mark.gpu
 
 CLASSES = ("uniform", "positive", "dominant", "outlier_rows", "outlier_cols", "huge", "tiny", "dynamic")
 ENCODINGS = ("tf32", "fp16")
-SHAPES = [(512, 768, 1024), (300, 520, 640), (1024, 1024, 4096)]
+SHAPES = [(512, 768, 1024), (300, 520, 640), (1024, 1024, 4096),
+          (2048, 2304, 1024)]      # mid-size: the cta_group::2 kernel (interp.pair_kernel)
 
 
 def make(M, N, K, kind, dev, seed=5):
