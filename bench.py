@@ -353,7 +353,10 @@ def main():
     ap.add_argument("--N", type=int, default=32768)
     ap.add_argument("--K", type=int, default=8192)
     ap.add_argument("--workload", default="rowshard", choices=["rowshard", "ladder", "binomial"])
-    ap.add_argument("--chunks", type=int, default=4, help="packedB broadcast chunks (N>1)")
+    # 6: the one-rank measurement + broadcast model at 8 ranks (4096-row shards)
+    # puts 6 chunks 1-4 points above 4 (a smaller first chunk, ~1 % more
+    # GEMM time); profiles/r2/experiments/rowshard_rank_model_chunks.jsonl
+    ap.add_argument("--chunks", type=int, default=6, help="packedB broadcast chunks (N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ladder", action="store_true")

@@ -10,7 +10,8 @@ on arrival, GEMM + fix-up per chunk) in a one-process world on
 and per-chunk GEMM times, then models
   step_8 = T_rank + bcast(chunk 0) + sum_c max(0, bcast(chunk c) - gemm(chunk c-1))
   efficiency = T1 / (8 * step_8)
-for NCCL broadcast bus bandwidths of 300 / 450 / 600 GB/s.
+for NCCL broadcast bus bandwidths of 300 / 450 / 600 GB/s, for each chunk
+count in CHUNKS (default 4, the bench's).
 """
 import json
 import os
@@ -27,12 +28,12 @@ N, K = 32768, 8192
 B = torch.empty((K, N), device=dev); synth.fill_device(B, 0, 1)
 
 
-def step_time(M, reps=5):
+def step_time(M, reps=5, chunks=4):
     term = schedules.apply("parallel", 32768, N, K).term
     plan = dispatch.decode(term, [(M, K), (K, N)], tf32x3=True, tc_encoding="fp16")
     A = torch.empty((M, K), device=dev); synth.fill_device(A, 0, 0)
     C = torch.empty((M, N), device=dev)
-    pipe = distributed.PipelinedRowShardGemm(plan, N, K, dev)
+    pipe = distributed.PipelinedRowShardGemm(plan, N, K, dev, chunks=chunks)
     for _ in range(2):
         pipe.step(A, B, C)
     torch.cuda.synchronize()
@@ -45,14 +46,15 @@ def step_time(M, reps=5):
 
 
 t1, _ = step_time(32768, reps=3)
-tr, chunks = step_time(4096)
-widths = [n1 - n0 for n0, n1 in chunks]
-gemm_c = [tr * w / N for w in widths]                       # per-chunk share of the rank's step
-out = {"T1_ms": t1, "T_rank_ms_4096_rows": tr, "chunks": widths, "model": []}
-for bw in (300, 450, 600):
-    b = [((w + 255) // 256) * 256 * K * 4 / (bw * 1e9) * 1e3 for w in widths]   # ms per chunk broadcast
-    exposed = b[0] + sum(max(0.0, b[c] - gemm_c[c - 1]) for c in range(1, len(b)))
-    step8 = tr + exposed
-    out["model"].append({"nccl_broadcast_busbw_GBps": bw, "exposed_broadcast_ms": exposed, "step_8_ms": step8,
-                         "efficiency_8": t1 / (8 * step8)})
-print(json.dumps(out), flush=True)
+for nchunks in [int(c) for c in os.environ.get("CHUNKS", "4").split(",")]:
+    tr, chunks = step_time(4096, chunks=nchunks)
+    widths = [n1 - n0 for n0, n1 in chunks]
+    gemm_c = [tr * w / N for w in widths]                       # per-chunk share of the rank's step
+    out = {"T1_ms": t1, "T_rank_ms_4096_rows": tr, "chunks": widths, "model": []}
+    for bw in (300, 450, 600):
+        b = [((w + 255) // 256) * 256 * K * 4 / (bw * 1e9) * 1e3 for w in widths]   # ms per chunk broadcast
+        exposed = b[0] + sum(max(0.0, b[c] - gemm_c[c - 1]) for c in range(1, len(b)))
+        step8 = tr + exposed
+        out["model"].append({"nccl_broadcast_busbw_GBps": bw, "exposed_broadcast_ms": exposed, "step_8_ms": step8,
+                             "efficiency_8": t1 / (8 * step8)})
+    print(json.dumps(out), flush=True)
