@@ -129,6 +129,14 @@ int elv_tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
  * the range-guard fix-up is run before returning (asynchronously on
  * `stream`). */
 int elv_tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N);
+
+/* The tensor-core kernel the library picks by default for an M x N output
+ * on a GPU with `sms` SMs (no environment overrides): 1 = the CTA-pair
+ * kernel (one 256x256 tile per pair), 0 = the 1-CTA kernel, whose N tile
+ * (256 / 128 / 64) is written to *bn when bn is not NULL; ELV_EINVAL for
+ * bad sizes.  No device work: callers use it to count launches (the pair
+ * kernel's range-guard fix-up is a separate launch). */
+int elv_tc_kernel_choice(int M, int N, int sms, int* bn);
 int elv_tf32x3_gemm_fused(const float* A, int lda, const float* B, int ldb, float* C, int ldc,
                           int M, int N, int K, unsigned int* flags, void* stream);
 /* The same kernel with B already split (elv_tf32x3_split_b / _split_b_packed

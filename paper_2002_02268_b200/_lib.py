@@ -23,7 +23,7 @@ EXPORTS = (
     "elv_nccl_destroy", "elv_gemm_rowshard", "elv_last_error", "elv_abi_version",
     "elv_variant_name", "elv_tf32x3_a_planes_bytes", "elv_tf32x3_b_planes_bytes",
     "elv_tf32x3_split_a", "elv_tf32x3_split_b", "elv_tf32x3_split_b_packed",
-    "elv_tf32x3_gemm_planes", "elv_tf32x3_fused_ok", "elv_tf32x3_gemm_fused", "elv_tf32x3_gemm_fused_a",
+    "elv_tf32x3_gemm_planes", "elv_tc_kernel_choice", "elv_tf32x3_fused_ok", "elv_tf32x3_gemm_fused", "elv_tf32x3_gemm_fused_a",
     "elv_binomial", "elv_binomial_variant_name",
     "elv_gemm_host", "elv_gemm_host_workspace_bytes", "elv_gemm_host_tiles", "elv_gemm_host_trace", "elv_copy2d",
     "elv_fp16x3_a_planes_bytes", "elv_fp16x3_b_planes_bytes", "elv_fp16x3_applicable", "elv_fp16x3_split_a",
@@ -75,6 +75,7 @@ def load():
         "elv_tf32x3_split_b_packed": (c_int, [c_vp, c_int, c_int, c_vp, c_vp]),
         "elv_tf32x3_gemm_planes": (c_int, [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_vp]),
         "elv_tf32x3_fused_ok": (c_int, [c_vp, c_int, c_vp, c_int, c_int, c_int]),
+        "elv_tc_kernel_choice": (c_int, [c_int, c_int, c_int, c_vp]),
         "elv_tf32x3_gemm_fused": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp]),
         "elv_tf32x3_gemm_fused_a": (c_int, [c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_int, c_int, c_int, c_int, c_vp,
                                             c_vp]),

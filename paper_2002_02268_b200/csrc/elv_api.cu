@@ -348,6 +348,11 @@ int elv_fp16x3_gemm_planes(const void* a_planes, const void* b_planes, float* C,
   return fp16x3_gemm_planes(a_planes, b_planes, C, M, N, K, ldc, (cudaStream_t)stream);
 }
 
+int elv_tc_kernel_choice(int M, int N, int sms, int* bn) {
+  if (M < 1 || N < 1 || sms < 2) return ELV_EINVAL;
+  return tc_kernel_choice(M, N, sms, bn);
+}
+
 int elv_tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N) {
   if (bad_ptr(A) || bad_ptr(B) || M < 1 || N < 1) return 0;
   return tf32x3_fused_ok(A, lda, B, ldb, M, N) ? 1 : 0;

@@ -139,6 +139,7 @@ int tf32x3_gemm_planes(const void* a_planes, const void* b_planes, float* C, int
                        cudaStream_t st, int a_total = 0, int r0 = 0, int b_total = 0, int c0 = 0,
                        FixArgs* fix = nullptr);
 bool tc_fixup_enabled();
+int tc_kernel_choice(int M, int N, int sms, int* bn);
 const unsigned int* tf32x3_b_planes_flags(const void* b_planes, int N, int K);
 bool tf32x3_fused_ok(const float* A, int lda, const float* B, int ldb, int M, int N);
 bool tf32x3_fused_a_ok(const float* A, int lda, int M, int N);

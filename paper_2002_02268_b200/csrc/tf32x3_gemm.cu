@@ -1652,6 +1652,7 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 static int one_cta_bn(int M, int N);
+static int one_cta_bn_model(int M, int N, long long sms);
 
 // Mainloop cycles per accumulation chunk (64 k fp16 / 32 k tf32: 12 MMAs of
 // k16 / k8) of one CTA whose MMAs are n_mma wide and whose SMEM holds
@@ -1664,6 +1665,18 @@ static int one_cta_bn(int M, int N);
 static double chunk_cycles(int n_mma, int n_smem) {
   const double mma = 6.0 * n_mma, smem = 5.0 * (128 + n_smem);
   return mma > smem ? mma : smem;
+}
+
+// The default kernel choice (no environment overrides) for `sms` SMs, given
+// the 1-CTA kernel's N tile: pair when there is at least one 256x256 pair
+// tile per SM or its modelled mainloop is shorter (see pair_mode).
+static bool pair_model(int M, int N, long long sms, int bn) {
+  const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
+  if (pair_tiles >= sms) return true;
+  const double pair = (double)((pair_tiles + sms / 2 - 1) / (sms / 2)) * chunk_cycles(256, 128);
+  const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  const double one = (double)((tiles + sms - 1) / sms) * chunk_cycles(bn, bn);
+  return pair < one;
 }
 
 // Kernel choice.  Default: the cta_group::2 kernel with BK=32 (128B swizzle)
@@ -1684,14 +1697,7 @@ static int pair_mode(int M, int N) {
     if (forced != -1 && forced != 0 && forced != 16 && forced != 32) forced = -1;
   }
   if (forced >= 0) return forced;
-  const long long sms = num_sms();
-  const long long pair_tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
-  if (pair_tiles >= sms) return 32;
-  const double pair = (double)((pair_tiles + sms / 2 - 1) / (sms / 2)) * chunk_cycles(256, 128);
-  const int bn = one_cta_bn(M, N);
-  const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-  const double one = (double)((tiles + sms - 1) / sms) * chunk_cycles(bn, bn);
-  return pair < one ? 32 : 0;
+  return pair_model(M, N, num_sms(), one_cta_bn(M, N)) ? 32 : 0;
 }
 // Wave counter (library-internal scratch, 4 bytes) zeroed on the launch
 // stream before every launch; ELV_WAVE_SYNC=0 disables the sync.  One counter
@@ -1990,17 +1996,28 @@ static int one_cta_bn(int M, int N) {
     if (forced != 64 && forced != 128 && forced != 256) forced = -1;
   }
   if (forced > 0) return forced;
+  return one_cta_bn_model(M, N, num_sms());
+}
+static int one_cta_bn_model(int M, int N, long long sms) {
   const int bns[3] = {256, 128, 64};
   const double eff[3] = {1.0, 0.95, 0.67};
   int best = 256;
   double best_cost = 1e30;
   for (int i = 0; i < 3; ++i) {
     const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bns[i] - 1) / bns[i]);
-    const long long waves = (tiles + num_sms() - 1) / num_sms();
+    const long long waves = (tiles + sms - 1) / sms;
     const double cost = (double)waves * bns[i] / eff[i];
     if (cost < best_cost * 0.999) { best_cost = cost; best = bns[i]; }
   }
   return best;
+}
+
+// elv_tc_kernel_choice: the default choice as data, for callers that count
+// launches (interp.GemmCall.count_launches mirrors it; tests compare the two)
+int tc_kernel_choice(int M, int N, int sms, int* bn) {
+  const int b = one_cta_bn_model(M, N, sms);
+  if (bn != nullptr) *bn = b;
+  return pair_model(M, N, sms, b) ? 1 : 0;
 }
 
 template <int TBN, int TBK, bool F16 = false>

@@ -165,7 +165,9 @@ class GemmCall:
             return cls.PREPARE_LAUNCHES[p.variant] + 1
         sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count \
             if torch.cuda.is_available() else 148
-        compute = 2 if pair_kernel(p.M, p.N, sms) else 1
+        # the library's own rule (elv_tc_kernel_choice); pair_kernel mirrors it
+        pair = _lib.load().elv_tc_kernel_choice(max(p.M, 1), max(p.N, 1), sms, None) == 1
+        compute = 2 if pair else 1
         if p.variant == 8 and p.K >= 512:
             return 2 + compute
         return 1 + compute

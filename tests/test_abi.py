@@ -84,3 +84,22 @@ def test_runtime_errors_map_to_runtime_error():
         _lib.check(_lib.ELV_ECUDA, "x")
     with pytest.raises(RuntimeError):
         _lib.check(_lib.ELV_ENCCL, "x")
+
+
+def test_kernel_choice_matches_the_python_mirror():
+    """elv_tc_kernel_choice (the library's default pair / 1-CTA rule; no
+    device work) agrees with interp.pair_kernel / _one_cta_bn, which
+    GemmCall.count_launches (the bench's gpu_launches claim) uses, over a
+    sweep of output shapes and SM counts."""
+    import ctypes
+    from paper_2002_02268_b200 import _lib, interp
+    lib = _lib.load()
+    bn = ctypes.c_int(0)
+    shapes = [(m, n) for m in (1, 100, 128, 257, 640, 1000, 1024, 1536, 2048, 2304, 3072, 4096, 8192, 32768)
+              for n in (1, 64, 256, 513, 1031, 1024, 2048, 2304, 4096, 32768)]
+    for sms in (148, 132, 160):
+        for m, n in shapes:
+            pair = lib.elv_tc_kernel_choice(m, n, sms, ctypes.byref(bn))
+            assert pair == int(interp.pair_kernel(m, n, sms)), (m, n, sms)
+            assert bn.value == interp._one_cta_bn(m, n, sms), (m, n, sms)
+    assert lib.elv_tc_kernel_choice(0, 10, 148, None) == _lib.ELV_EINVAL
