@@ -488,3 +488,30 @@ def test_gemmcall_graph_replay_bitwise(cuda, variant):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(C, ref)
+
+
+@pytest.mark.parametrize("variant,shape", [
+    ("parallel", (1024, 1024, 1024)), ("cacheBlocks", (1024, 1024, 1024)), ("baseline", (512, 512, 512)),
+    ("parallel_tf32x3", (1024, 1024, 1024)), ("parallel_fp16x3", (1024, 1024, 1024)),
+    ("parallel_tf32x3", (2048, 2048, 1024)), ("parallel_fp16x3", (2048, 2048, 1024)),
+    ("parallel_fp16x3", (1024, 1024, 256))], ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+def test_launch_count_claim_matches_the_profiler(cuda, variant, shape):
+    """GemmCall.count_launches -- the per-call basis of the bench's
+    `gpu_launches` -- equals the kernels the CUDA profiler (CUPTI, via
+    torch.profiler) records for one call: 1-CTA vs pair kernel (in-kernel
+    vs separate range-guard fix-up), the 3xFP16 two-kernel prepare, K < 512
+    running the fp16 request as 3xTF32, the SIMT pack kernels."""
+    M, N, K = shape
+    name, tf = _sched(variant)
+    A, B = _device_inputs(M, N, K, 41, cuda)
+    p = dispatch.decode(schedules.apply(name, M, N, K).term, [(M, K), (K, N)], tf32x3=tf, tc_encoding=_enc(variant))
+    C = torch.empty((M, N), device=cuda)
+    call = interp.GemmCall(p, A, B, C)
+    call()
+    torch.cuda.synchronize()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        call()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+             and "elv" in e.name]
+    assert len(names) == call.launches, (call.launches, names)
