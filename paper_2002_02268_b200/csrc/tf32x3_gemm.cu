@@ -772,7 +772,13 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
       // ---------------- TMA producer (both CTAs) ----------------
       const uint32_t full0 = mapa_rank(smem_u32(&full[0]), 0);
       const uint64_t pol_a = l2_policy_evict_last();
-      const uint64_t pol_b = l2_hints >= 2 ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t pol_b = (l2_hints & 3) >= 2 ? l2_policy_evict_first() : l2_policy_evict_normal();
+      // bit 2 (ELV_SERPENTINE=1, an experiment): odd waves walk the k-blocks
+      // backwards, so they start on the slabs of the m-group's A panels the
+      // previous wave left in L2.  Each element's chunk sums then run in the
+      // order of its wave's parity: within the tolerance, but no longer
+      // bitwise the 1-CTA kernel / other tilings, hence off by default.
+      const bool serp = (l2_hints & 4) != 0;
       int s = 0; uint32_t ph = 0;
       int wave = 0;
       for (int t = cluster_id; t < num_tiles; t += num_clusters, ++wave) {
@@ -790,9 +796,9 @@ k7_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constan
           PROF_ADD(3, e1 - e0);
           uint8_t* st = smem + s * P_STAGE_BYTES;
           const uint32_t bar = full0 + (uint32_t)(s * 8);
-          const int k0 = kb * BKT;
+          const int k0 = (serp && (wave & 1)) ? (num_kb - 1 - kb) * BKT : kb * BKT;
           if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);   // both CTAs' bytes
-          if (l2_hints) {
+          if (l2_hints & 3) {
             tma_load_2d_pair_hint(&map_ahi, bar, st, k0, ma, pol_a);
             tma_load_2d_pair_hint(&map_alo, bar, st + P_A_TILE, k0, ma, pol_a);
             tma_load_2d_pair_hint(&map_bhi, bar, st + 2 * P_A_TILE, k0, nb, pol_b);
@@ -1739,11 +1745,13 @@ static unsigned int* wave_counter(int dev, cudaStream_t st) {
   return c;
 }
 
-// L2 residency hints in the pair kernel (ELV_L2_HINTS, default on): the
-// m-group's A panels evict_last, B evict_first
+// L2 residency hints in the pair kernel (ELV_L2_HINTS, default off: 1 = the
+// m-group's A panels evict_last, 2 = also B evict_first), plus bit 2 for the
+// serpentine k order of odd waves (ELV_SERPENTINE=1, default off; see the
+// producer).  One flags word, read once per process.
 static int l2_hints() {
   static int v = -2;
-  if (v == -2) v = env_int("ELV_L2_HINTS", 0);
+  if (v == -2) v = (env_int("ELV_L2_HINTS", 0) & 3) | (env_int("ELV_SERPENTINE", 0) ? 4 : 0);
   return v;
 }
 
@@ -1763,7 +1771,7 @@ static bool c_store_tma() {
 // m-tiles per L2 raster group of the pair kernel: with L2 hints the group's A
 // panels (group x 256 rows x K of hi+lo planes) stay resident -- 64 MB at
 // K = 8192 for 8 fp16 / 4 tf32 m-tiles, half the 126 MB L2
-template <bool F16> static int pair_group() { return (!F16 && l2_hints()) ? 4 : 8; }
+template <bool F16> static int pair_group() { return (!F16 && (l2_hints() & 3)) ? 4 : 8; }
 
 template <int BKT, bool F16 = false, int PBN = P_BN>
 static int launch_pair(const void* a_hi, const void* a_lo, const void* b_hi, const void* b_lo, float* C, int M,

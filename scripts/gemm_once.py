@@ -35,5 +35,9 @@ for _ in range(reps):
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1))
 ms = statistics.median(times)
-print(json.dumps({"enc": "fp16" if f16 else "tf32", "M": M, "N": N, "K": K, "l2_hints": os.environ.get("ELV_L2_HINTS", "1"),
-                  "ms": ms, "TF": 2.0 * M * N * K / ms / 1e9, "times": times}), flush=True)
+out = {"enc": "fp16" if f16 else "tf32", "M": M, "N": N, "K": K, "l2_hints": os.environ.get("ELV_L2_HINTS", "0"),
+       "serpentine": os.environ.get("ELV_SERPENTINE", "0"), "ms": ms, "TF": 2.0 * M * N * K / ms / 1e9,
+       "times": times}
+if os.environ.get("SAVE_C"):          # a sample of C rows for comparing k orders (every 97th row)
+    torch.save(C[::97].cpu(), os.environ["SAVE_C"])
+print(json.dumps(out), flush=True)

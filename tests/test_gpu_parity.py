@@ -515,3 +515,38 @@ def test_launch_count_claim_matches_the_profiler(cuda, variant, shape):
     names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
              and "elv" in e.name]
     assert len(names) == call.launches, (call.launches, names)
+
+
+@pytest.mark.parametrize("variant", ["parallel_tf32x3", "parallel_fp16x3"])
+def test_serpentine_k_order_opt_in(cuda, tmp_path, variant):
+    """ELV_SERPENTINE=1 (an experiment, off by default): odd waves of the pair
+    kernel walk the k-blocks backwards.  Results stay within the tau = 1
+    bound of the f64 oracle; the first wave's tiles (even parity) keep the
+    default bits, and later waves' bits differ (the knob is live)."""
+    import subprocess
+    import sys
+    M, N, K = 8192, 8192, 1024                   # 1024 pair tiles: ~14 waves of 74
+    name, tf = _sched(variant)
+    enc = _enc(variant)
+    A, B = _device_inputs(M, N, K, 23, cuda)
+    term = schedules.apply(name, M, N, K).term
+    C = interp.run_tensor(term, A, B, tf32x3=tf, tc_encoding=enc).cpu().numpy()
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (f"import sys; sys.path.insert(0, {repo!r})\n"
+            "import numpy as np, torch\n"
+            "from paper_2002_02268_b200 import interp, schedules, synth\n"
+            f"M, N, K = {M}, {N}, {K}\n"
+            "A = torch.empty((M, K), device='cuda'); synth.fill_device(A, 23, 0)\n"
+            "B = torch.empty((K, N), device='cuda'); synth.fill_device(B, 23, 1)\n"
+            f"C = interp.run_tensor(schedules.apply({name!r}, M, N, K).term, A, B, tf32x3={tf}, tc_encoding={enc!r})\n"
+            f"np.save({str(tmp_path / 'c.npy')!r}, C.cpu().numpy())\n")
+    env = dict(os.environ, ELV_SERPENTINE="1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    Cs = np.load(tmp_path / "c.npy")
+    # wave 0 = tiles 0..73 of raster group 0 (8 m-tiles, n-major): rows < 2048, cols < 9 * 256
+    assert np.array_equal(C[:2048, :2304].view(np.int32), Cs[:2048, :2304].view(np.int32))
+    assert not np.array_equal(C.view(np.int32), Cs.view(np.int32))
+    rows = slice(0, M, 61)
+    Ah, Bh = A.cpu().numpy()[rows], B.cpu().numpy()
+    ok, worst = oracle.check(Cs[rows], oracle.mm_f64(Ah, Bh), oracle.absprod_np(Ah, Bh), K)
+    assert ok, f"serpentine {variant}: worst err/bound {worst:.3g}"
