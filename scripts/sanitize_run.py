@@ -51,6 +51,20 @@ def main():
         ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
         print(f"mid-size pair {enc} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
         assert ok
+    if os.environ.get("ELV_SERPENTINE") == "1":
+        # more pair tiles than clusters (80 > 74): an odd wave walks its k-blocks backwards
+        M, N, K = 2560, 2048, 512
+        A = synth.matrix(M, K, 9, 0)
+        B = synth.matrix(K, N, 9, 1)
+        ref, ab = oracle.mm_f64(A, B), oracle.absprod_np(A, B)
+        for enc in ("tf32", "fp16"):
+            term = schedules.apply_padded("parallel", M, N, K).term
+            C = interp.run_tensor(term, torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), tf32x3=True,
+                                  tc_encoding=enc)
+            torch.cuda.synchronize()
+            ok, worst = oracle.check(C.cpu().numpy(), ref, ab, K)
+            print(f"serpentine pair {enc} {M}x{N}x{K} ok={ok} worst={worst:.3f}", flush=True)
+            assert ok
     # range guard: marked rows / columns recomputed by the fix-up (both encodings)
     M, N, K = 160, 200, 576
     A = synth.matrix(M, K, 8, 0)
