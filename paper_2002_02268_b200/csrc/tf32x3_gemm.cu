@@ -1030,8 +1030,10 @@ __device__ __forceinline__ void split_a_block(const float* __restrict__ A, float
       x.z = k + 2 < K ? __ldg(src + 2) : 0.f;
       x.w = k + 3 < K ? __ldg(src + 3) : 0.f;
     }
-    if (tf32_out_of_window(x.x) || tf32_out_of_window(x.y) || tf32_out_of_window(x.z) || tf32_out_of_window(x.w))
+    if (tf32_out_of_window(x.x) || tf32_out_of_window(x.y) || tf32_out_of_window(x.z) || tf32_out_of_window(x.w)) {
+      griddep_wait();                             // flags zeroed by k_zero_u32 (PDL launch; no-op otherwise)
       flag[r] = 1u;
+    }
     const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
     const float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
                                  tf32_rna(x.w - h.w));
@@ -1070,7 +1072,10 @@ __device__ __forceinline__ void split_transpose_b_block(const float* __restrict_
     const int n = n0 + ty + 8 * r, k = k0 + tx;
     if (n < N && k < Kp) {
       const float x = t[tx][ty + 8 * r];
-      if (tf32_out_of_window(x)) flag[n] = 1u;
+      if (tf32_out_of_window(x)) {
+        griddep_wait();                           // flags zeroed by k_zero_u32 (PDL launch; no-op otherwise)
+        flag[n] = 1u;
+      }
       const float h = tf32_rna(x);
       hi[(size_t)n * Kp + k] = h;
       lo[(size_t)n * Kp + k] = tf32_rna(x - h);
@@ -1095,6 +1100,26 @@ k_split_ab(const float* __restrict__ A, float* __restrict__ ahi, float* __restri
   const int b = blockIdx.x, ga = gxa * gya;
   if (b < ga) split_a_block(A, ahi, alo, M, K, lda, Kp, vecA, b % gxa, b / gxa, gya, flag_a);
   else split_transpose_b_block<false>(B, bhi, blo, K, N, ldb, Kp, (b - ga) % gxb, (b - ga) / gxb, flag_b);
+  // PDL-launched behind k_zero_u32 (elv_gemm's prepare): our completion must
+  // imply the flags' zeroing is done, since the GEMM / fix-up that wait for
+  // us read them -- blocks that set no flag wait here, after their split
+  griddep_wait();
+}
+
+// Zeroes n words and lets its PDL dependent start at once: replaces a
+// cudaMemsetAsync before the prepare kernels (a memset node serialises the
+// chain; the dependents overlap their loads with it and wait
+// (griddepcontrol.wait) only before touching the zeroed words).
+__global__ void __launch_bounds__(256) k_zero_u32(unsigned int* __restrict__ p, size_t n) {
+  griddep_launch_dependents();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0u;
+}
+static int zero_words(unsigned int* p, size_t n, cudaStream_t st) {
+  if (n == 0) return ELV_OK;
+  const size_t want = (n + 1023) / 1024;
+  const unsigned blocks = (unsigned)(want < 148 ? want : 148);
+  k_zero_u32<<<blocks, 256, 0, st>>>(p, n);
+  return cudaPeekAtLastError() == cudaSuccess ? ELV_OK : check_launch("zero_words");
 }
 
 // ----------------------------------------------------------------------------
@@ -2128,10 +2153,14 @@ int tf32x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "tf32x3: problem too large for one split launch");
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) && (lda & 3) == 0;
   unsigned int* flags = ws_tail_flags(ws, M, N, K);
-  if (cudaMemsetAsync(flags, 0, (size_t)(M + N) * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3: memset");
+  // flags zeroed by a kernel the split follows with PDL (it overlaps the
+  // split's loads; the split waits only before setting a flag and at its end)
+  int rc = zero_words(flags, (size_t)(M + N), st);
+  if (rc) return rc;
   ELV_PREFER_MAX_SMEM(k_split_ab);
-  k_split_ab<<<(unsigned)blocks, 256, 0, st>>>(A, ahi, alo, M, lda, vec, gxa, gya, B, bhi, blo, N, ldb, gxb, K, Kp,
-                                               flags, flags + M);
+  const cudaError_t e = launch_pdl(k_split_ab, dim3((unsigned)blocks), dim3(256), 0, st, A, ahi, alo, M, lda, vec, gxa,
+                                   gya, B, bhi, blo, N, ldb, gxb, K, Kp, flags, flags + M);
+  if (e != cudaSuccess) return set_error(ELV_ECUDA, "tf32x3_split_ab: %s", cudaGetErrorString(e));
   return check_launch("tf32x3_split_ab");
 }
 
@@ -2214,6 +2243,7 @@ __device__ __forceinline__ void col_max_slab(const float* __restrict__ B, int K,
   const int k0 = by * slab, k1 = min(K, k0 + slab);
   float m = 0.f;
   for (int k = k0; k < k1; ++k) m = fmaxf(m, fabsf(ld_b_elem<PACKED>(B, K, ldb, k, j)));
+  griddep_wait();                                 // maxima zeroed by k_zero_u32 (PDL launch; no-op otherwise)
   atomicMax(maxbits + j, __float_as_uint(m));
 }
 template <bool PACKED>
@@ -2654,7 +2684,11 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
                                               (int)(ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0));
     return check_launch("fp16x3_prepare_fused");
   }
-  if (cudaMemsetAsync(tmax, 0, (size_t)N * 4, st) != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3: memset");
+  // the column maxima are zeroed by a kernel that k16_prep_ab follows with
+  // PDL: its A rows and B slab loads overlap the zeroing, the B blocks wait
+  // (griddepcontrol.wait) only before their atomicMax
+  int zrc = zero_words(tmax, (size_t)N, st);
+  if (zrc) return zrc;
   // Short rows: one warp per A row (2: row in registers, when float4 loads
   // are legal; 1: two scalar passes); ELV_FP16X3_WARP_ROWS caps the mode
   // (0 = one block per row).  Column-maximum slabs shrink from 64 rows
@@ -2674,9 +2708,9 @@ int fp16x3_prepare(const float* A, const float* B, int M, int N, int K, int lda,
   if (blocks > 0x7fffffffLL) return set_error(ELV_EINVAL, "fp16x3: problem too large for one prepare launch");
   ELV_PREFER_MAX_SMEM(k16_prep_ab);
   ELV_PREFER_MAX_SMEM(k16_split_transpose_b<false>);
-  k16_prep_ab<<<(unsigned)blocks, 256, 0, st>>>(A, M, K, lda, Kp, PA.s, PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax,
-                                                warp_rows, slab, PA.flag, PB.flag);
-  if (cudaPeekAtLastError() != cudaSuccess) return check_launch("fp16x3_prepare");
+  const cudaError_t ep = launch_pdl(k16_prep_ab, dim3((unsigned)blocks), dim3(256), 0, st, A, M, K, lda, Kp, PA.s,
+                                    PA.inv, PA.hi, PA.lo, B, N, ldb, gxb, tmax, warp_rows, slab, PA.flag, PB.flag);
+  if (ep != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3_prepare: %s", cudaGetErrorString(ep));
   const cudaError_t e = launch_pdl(k16_split_transpose_b<false>, dim3((N + 31) / 32, (Kp + 63) / 64), dim3(256), 0, st, B, K,
                                    N, ldb, Kp, (const unsigned int*)tmax, PB.hi, PB.lo, PB.inv, PB.flag);
   if (e != cudaSuccess) return set_error(ELV_ECUDA, "fp16x3_prepare: %s", cudaGetErrorString(e));

@@ -148,19 +148,19 @@ class GemmCall:
     phases (elv_gemm_prepare: operand layout transform; elv_gemm_compute:
     the GEMM kernel) so callers can time or overlap them separately.
     Launches per call: prepare 0 (variants 0-3), 1 (4, 5: packB; 6: packB, or
-    packA+packB fused; 7: fused hi/lo split of A and B), 2 (8: [A rows | B
-    maxima], B split); compute 1, or 2 for the tensor-core variants when the
+    packA+packB fused), 2 (7: guard-flag zeroing, fused hi/lo split of A and
+    B), 3 (8: column-maxima zeroing, [A rows | B maxima], B split) -- each
+    prepare PDL-chained; compute 1, or 2 for the tensor-core variants when the
     range-guard fix-up runs as its own launch (see count_launches)."""
 
-    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 1, 8: 2}   # 8: [A rows | B max], B split
+    PREPARE_LAUNCHES = {0: 0, 1: 0, 2: 0, 3: 0, 4: 1, 5: 1, 6: 1, 7: 2, 8: 3}
 
     @classmethod
     def count_launches(cls, p) -> int:
         """Kernel launches of one call (the library's defaults): the
         tensor-core variants fold the range-guard fix-up into the 1-CTA GEMM
-        (the small problems `pair_kernel` leaves to it); the 3xFP16 prepare
-        is two launches;
-        K < 512 runs variant 8 as 7."""
+        (the small problems `pair_kernel` leaves to it); the prepare counts
+        as PREPARE_LAUNCHES; K < 512 runs variant 8 as 7."""
         if p.variant not in (7, 8):
             return cls.PREPARE_LAUNCHES[p.variant] + 1
         sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count \
@@ -169,8 +169,8 @@ class GemmCall:
         pair = _lib.load().elv_tc_kernel_choice(max(p.M, 1), max(p.N, 1), sms, None) == 1
         compute = 2 if pair else 1
         if p.variant == 8 and p.K >= 512:
-            return 2 + compute
-        return 1 + compute
+            return cls.PREPARE_LAUNCHES[8] + compute
+        return cls.PREPARE_LAUNCHES[7] + compute
 
     def __init__(self, p: dispatch.KernelPlan, A, B, C, stream=None):
         self.lib = _lib.load()

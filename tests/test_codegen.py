@@ -169,11 +169,11 @@ def test_gemmcall_launch_counts():
     from paper_2002_02268_b200.interp import GemmCall
     assert GemmCall.count_launches(P(variant=0, M=64, N=64, K=64)) == 1
     assert GemmCall.count_launches(P(variant=6, M=4096, N=4096, K=4096)) == 2          # packs + GEMM
-    assert GemmCall.count_launches(P(variant=7, M=1024, N=1024, K=1024)) == 2          # split + GEMM (fix-up inside)
-    assert GemmCall.count_launches(P(variant=7, M=32768, N=32768, K=8192)) == 3        # + separate fix-up
-    assert GemmCall.count_launches(P(variant=8, M=32768, N=32768, K=8192)) == 4        # 2 prepare + GEMM + fix-up
-    assert GemmCall.count_launches(P(variant=8, M=1024, N=1024, K=256)) == 2           # K < 512 runs as 7
-    assert GemmCall.count_launches(P(variant=8, M=2048, N=2048, K=2048)) == 4          # mid-size: pair kernel
+    assert GemmCall.count_launches(P(variant=7, M=1024, N=1024, K=1024)) == 3          # zero + split + GEMM (fix-up inside)
+    assert GemmCall.count_launches(P(variant=7, M=32768, N=32768, K=8192)) == 4        # + separate fix-up
+    assert GemmCall.count_launches(P(variant=8, M=32768, N=32768, K=8192)) == 5        # 3 prepare + GEMM + fix-up
+    assert GemmCall.count_launches(P(variant=8, M=1024, N=1024, K=256)) == 3           # K < 512 runs as 7
+    assert GemmCall.count_launches(P(variant=8, M=2048, N=2048, K=2048)) == 5          # mid-size: pair kernel
 
 
 def test_pair_kernel_choice_model():
